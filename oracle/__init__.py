@@ -1,0 +1,248 @@
+"""Python face of the float64 CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs — never by the product package
+paper_2111_05188_b200/.  It shares no code with the CUDA path; both consume the
+same seeded inputs from paper_2111_05188_b200/synth.py (which holds no
+arithmetic of the method).
+
+Everything here is argument marshalling (numpy <-> C) except ``actor_flat``,
+which lays the per-layer weight matrices out in the oracle's own unpadded
+float64 layout (documented in oracle.c, ``orc_actor_mu``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["make", "-s", "-C", _HERE, "liboracle.so"])
+    return _LIB_PATH
+
+
+class _Cfg(C.Structure):
+    _fields_ = [
+        ("n_envs", C.c_int), ("n_stocks", C.c_int), ("n_feat", C.c_int), ("horizon", C.c_int),
+        ("h_max", C.c_int), ("n_agents", C.c_int),
+        ("C0", C.c_double), ("cost", C.c_double), ("scale", C.c_double), ("gamma", C.c_double),
+        ("seed", C.c_uint64), ("env_offset", C.c_int64), ("T_data", C.c_int64),
+    ]
+
+
+class _State(C.Structure):
+    _fields_ = [
+        ("cash", C.c_void_p), ("asset", C.c_void_p), ("disc", C.c_void_p), ("gpow", C.c_void_p),
+        ("ep_ret", C.c_void_p), ("hold", C.c_void_p), ("start", C.c_void_p), ("k", C.c_void_p),
+    ]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB_PATH)
+        vp, i, i64, u64, d = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double
+        L.orc_philox4x32_10.argtypes = [vp, vp, vp]
+        L.orc_normals.argtypes = [u64, i64, u64, i, vp]
+        L.orc_map_action.argtypes = [d, i]
+        L.orc_map_action.restype = i
+        L.orc_reset.argtypes = [C.POINTER(_Cfg), C.POINTER(_State)]
+        L.orc_obs.argtypes = [C.POINTER(_Cfg), vp, vp, C.POINTER(_State), i, vp]
+        L.orc_env_step.argtypes = [C.POINTER(_Cfg), vp, C.POINTER(_State), i, vp, vp, vp, vp, vp]
+        L.orc_env_step.restype = i
+        L.orc_actor_weight_count.argtypes = [i, i, i, i]
+        L.orc_actor_weight_count.restype = i64
+        L.orc_actor_mu.argtypes = [vp, i, i, i, i, i, vp, vp, vp]
+        L.orc_sample.argtypes = [i, vp, vp, vp, i, vp, vp]
+        L.orc_sample.restype = d
+        L.orc_rollout.argtypes = [C.POINTER(_Cfg), vp, vp, C.POINTER(_State), i, i, vp, vp, vp, i, i, i,
+                                  u64, vp, vp, vp, vp, vp, vp, vp, vp, vp, i]
+        L.orc_rollout.restype = i64
+        L.orc_gae.argtypes = [i, i, vp, vp, vp, vp, d, d, vp, vp, vp]
+        L.orc_fitness.argtypes = [i, i, vp, vp]
+        L.orc_select_elite.argtypes = [i, vp, i, vp]
+        L.orc_select_elite.restype = i
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------------------
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def normals(seed: int, env_global: int, step: int, n: int) -> np.ndarray:
+    z = np.zeros(n, dtype=np.float64)
+    lib().orc_normals(seed, env_global, step, n, _p(z))
+    return z
+
+
+def map_action(u: float, h_max: int) -> int:
+    return int(lib().orc_map_action(float(u), int(h_max)))
+
+
+def actor_flat(W, b, log_std) -> np.ndarray:
+    """Oracle weight layout: W_1, b_1, ..., W_out, b_out, log_std (float64)."""
+    parts = []
+    for Wl, bl in zip(W, b):
+        parts.append(np.asarray(Wl, dtype=np.float64).ravel())
+        parts.append(np.asarray(bl, dtype=np.float64).ravel())
+    parts.append(np.asarray(log_std, dtype=np.float64).ravel())
+    return np.ascontiguousarray(np.concatenate(parts))
+
+
+def actor_mu(w_flat: np.ndarray, obs: np.ndarray, n_hidden: int, hidden: int, n: int, act: int = 0) -> np.ndarray:
+    """mu for each row of obs [B, obs_dim] (float64)."""
+    obs = np.ascontiguousarray(obs, dtype=np.float64)
+    B, od = obs.shape
+    assert w_flat.size == lib().orc_actor_weight_count(od, n_hidden, hidden, n)
+    mu = np.zeros((B, n), dtype=np.float64)
+    scratch = np.zeros(2 * hidden, dtype=np.float64)
+    for r in range(B):
+        lib().orc_actor_mu(_p(w_flat), od, n_hidden, hidden, n, act, _p(obs[r]), _p(mu[r]), _p(scratch))
+    return mu
+
+
+def sample(mu, log_std, z, deterministic=False):
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    ls = np.ascontiguousarray(log_std, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    n = mu.size
+    raw = np.zeros(n)
+    u = np.zeros(n)
+    lp = lib().orc_sample(n, _p(mu), _p(ls), _p(z), int(deterministic), _p(raw), _p(u))
+    return raw, u, lp
+
+
+# ---------------------------------------------------------------------------
+class Env:
+    """Batched oracle environment: N independent envs stepped sequentially."""
+
+    def __init__(self, close, feat, n_envs, horizon, h_max=100, C0=1e6, cost=0.002, scale=1.0,
+                 gamma=0.99, seed=0, env_offset=0, n_agents=1):
+        self.close = np.ascontiguousarray(close, dtype=np.float32)
+        T_data, n = self.close.shape
+        feat = np.zeros((T_data, 0, n), np.float32) if feat is None else feat
+        self.feat = np.ascontiguousarray(feat, dtype=np.float32)
+        f = self.feat.shape[1]
+        self.n, self.f, self.N = n, f, n_envs
+        self.obs_dim = 1 + 2 * n + n * f
+        self.cfg = _Cfg(n_envs, n, f, horizon, h_max, n_agents, C0, cost, scale, gamma, seed,
+                        env_offset, T_data)
+        N = n_envs
+        self.cash = np.zeros(N)
+        self.asset = np.zeros(N)
+        self.disc = np.zeros(N)
+        self.gpow = np.zeros(N)
+        self.ep_ret = np.zeros(N)
+        self.hold = np.zeros((N, n), dtype=np.int32)
+        self.start = np.zeros(N, dtype=np.int64)
+        self.k = np.zeros(N, dtype=np.int64)
+        self._st = _State(*[a.ctypes.data for a in (self.cash, self.asset, self.disc, self.gpow,
+                                                    self.ep_ret, self.hold, self.start, self.k)])
+
+    def reset(self, start_rows):
+        self.start[:] = np.asarray(start_rows, dtype=np.int64)
+        lib().orc_reset(C.byref(self.cfg), C.byref(self._st))
+
+    def obs(self, e=None):
+        if e is None:
+            return np.stack([self.obs(i) for i in range(self.N)])
+        o = np.zeros(self.obs_dim)
+        lib().orc_obs(C.byref(self.cfg), _p(self.close), _p(self.feat), C.byref(self._st), int(e), _p(o))
+        return o
+
+    def step_env(self, e, a):
+        a = np.ascontiguousarray(a, dtype=np.int32)
+        r = np.zeros(1)
+        nt = np.zeros(1, dtype=np.int64)
+        hp = np.zeros(self.n, dtype=np.int32)
+        cp = np.zeros(1)
+        d = lib().orc_env_step(C.byref(self.cfg), _p(self.close), C.byref(self._st), int(e), _p(a),
+                               _p(r), _p(nt), _p(hp), _p(cp))
+        return float(r[0]), bool(d), int(nt[0]), hp, float(cp[0])
+
+    def account_value(self, e):
+        t = self.start[e] + self.k[e]
+        return float(self.cash[e] + np.dot(self.close[t].astype(np.float64), self.hold[e].astype(np.float64)))
+
+    def rollout(self, T, mode="inject", u=None, a_rep=None, weights=None, n_hidden=0, hidden=0, act=0,
+                step0=0, nthreads=1, want=("obs", "rew", "done")):
+        """mode: inject (u [T,N,n] f32), replay (a_rep [T,N,n] i16), sample, deterministic.
+        weights: [n_agents, count] float64 (actor_flat per agent)."""
+        N, n, od = self.N, self.n, self.obs_dim
+        modes = {"inject": 0, "replay": 1, "sample": 2, "deterministic": 3}
+        out = {}
+
+        def buf(name, shape, dt):
+            if name in want:
+                out[name] = np.zeros(shape, dtype=dt)
+                return out[name]
+            return None
+
+        obs = buf("obs", (T + 1, N, od), np.float64)
+        mu = buf("mu", (T, N, n), np.float64)
+        raw = buf("raw", (T, N, n), np.float64)
+        logp = buf("logp", (T, N), np.float64)
+        rew = buf("rew", (T, N), np.float64)
+        done = buf("done", (T, N), np.uint8)
+        a_out = buf("a_int", (T, N, n), np.int32)
+        hold_out = buf("hold", (T, N, n), np.int32)
+        cash_out = buf("cash", (T, N), np.float64)
+        u = None if u is None else np.ascontiguousarray(u, dtype=np.float32)
+        a_rep = None if a_rep is None else np.ascontiguousarray(a_rep, dtype=np.int16)
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+        ties = lib().orc_rollout(C.byref(self.cfg), _p(self.close), _p(self.feat), C.byref(self._st), int(T),
+                                 modes[mode], _p(u), _p(a_rep), _p(w), int(n_hidden), int(hidden), int(act),
+                                 int(step0), _p(obs), _p(mu), _p(raw), _p(logp), _p(rew), _p(done), _p(a_out),
+                                 _p(hold_out), _p(cash_out), int(nthreads))
+        out["near_ties"] = int(ties)
+        return out
+
+
+# ---------------------------------------------------------------------------
+def gae(r, v, d, boot, gamma, lam):
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.uint8)
+    boot = np.ascontiguousarray(boot, dtype=np.float64)
+    T, N = r.shape
+    adv = np.zeros((T, N))
+    ret = np.zeros((T, N))
+    mag = np.zeros((T, N))
+    lib().orc_gae(T, N, _p(r), _p(v), _p(d), _p(boot), float(gamma), float(lam), _p(adv), _p(ret), _p(mag))
+    return adv, ret, mag
+
+
+def fitness(ep_ret, n_agents):
+    ep = np.ascontiguousarray(ep_ret, dtype=np.float64)
+    J = np.zeros(n_agents)
+    lib().orc_fitness(ep.size, n_agents, _p(ep), _p(J))
+    return J
+
+
+def select_elite(J, k):
+    J = np.ascontiguousarray(J, dtype=np.float64)
+    plan = np.zeros(J.size, dtype=np.int32)
+    rc = lib().orc_select_elite(J.size, _p(J), int(k), _p(plan))
+    if rc != 0:
+        raise ValueError("orc_select_elite rejected its arguments")
+    return plan
