@@ -1,0 +1,277 @@
+/*
+ * pod.h — C ABI of libpod.so, the B200-native (sm_100a) hot path of
+ * FinRL-Podracer (arXiv 2111.05188): a massively vectorised stock-trading
+ * rollout, its GAE scan and generational-evolution elite selection.
+ *
+ * Citations: "P:Lx" = PAPER.md line x (/root/reference, LaTeX source of the
+ * paper); "S:Lx" = SPEC.md line x; "R#k" = reading k in DESIGN.md §3.
+ *
+ * Conventions for every entry point
+ *   - Plain C types only.  Pointers marked [dev] are CUDA device pointers, [host]
+ *     are host pointers.  `stream` is a cudaStream_t passed as void*.
+ *   - The CALLER owns all device memory (market tensors, workspace,
+ *     trajectories, actor parameters, outputs).  The library owns only the
+ *     opaque handles, the TMA descriptors and CUDA graphs cached in them, and
+ *     the NCCL communicator.  Nothing is allocated inside a hot call
+ *     (pod_rollout, pod_gae, pod_select_elite).
+ *   - Calls are stream-ordered and asynchronous unless stated otherwise; a
+ *     buffer must stay alive until the stream work that uses it completes.
+ *   - Every function returns a pod_status.  Argument errors are detected on
+ *     the host and returned synchronously without launching anything; the
+ *     thread-local pod_last_error() gives a one-line reason.  Device-side
+ *     faults (non-finite actor mean or account value) set a device error word
+ *     that pod_env_check() and pod_env_read_state() turn into
+ *     POD_ERR_NONFINITE.
+ *   - A handle is not thread-safe; distinct handles are independent.
+ *   - Compute capability must be 10.0 (B200, sm_100a): there is no fallback
+ *     path of any kind (POD_ERR_UNSUPPORTED otherwise).
+ */
+#ifndef POD_H
+#define POD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POD_ABI_VERSION 1
+#define POD_ENV_TILE 32      /* envs per tile: one warp; a tile shares its episode start row */
+#define POD_MAX_HIDDEN_LAYERS 4
+
+typedef enum {
+    POD_OK = 0,
+    POD_ERR_ARG = 1,          /* bad scalar argument or NULL where required            */
+    POD_ERR_SHAPE = 2,        /* inconsistent or unsupported sizes                      */
+    POD_ERR_RANGE = 3,        /* start row out of range of the market data */
+    POD_ERR_WORKSPACE = 4,    /* workspace too small or misaligned                      */
+    POD_ERR_CUDA = 5,         /* a CUDA runtime/driver call failed                      */
+    POD_ERR_NCCL = 6,         /* NCCL missing or a collective failed                    */
+    POD_ERR_NONFINITE = 7,    /* non-finite mean action / account value / fitness       */
+    POD_ERR_UNSUPPORTED = 8   /* device is not sm_100, or a shape outside kernel limits */
+} pod_status;
+
+const char* pod_status_string(pod_status s);
+/* Detail of the last failing call on this thread ("" if none). */
+const char* pod_last_error(void);
+int pod_abi_version(void);
+
+typedef struct pod_env pod_env_t;    /* opaque */
+typedef struct pod_comm pod_comm_t;  /* opaque */
+
+/* Environment configuration (§3; defaults).
+ *   n_envs          N, envs on this process/GPU (>= 1; ragged last tile allowed)
+ *   n_stocks        n (1..102 with n_feat = 3: obs_dim = 1+2n+nf must be <= 512)
+ *   n_feat          f indicator channels (3 = MACD, RSI, CCI)
+ *   n_agents        P_local; envs are split into n_agents contiguous equal groups,
+ *                   group a acts with agent a's parameters (N % n_agents == 0)
+ *   horizon         H, episode length in steps (R#10)
+ *   h_max           max shares per ticker per step (R#7; >= 1)
+ *   env_offset      global id of env 0 — the Philox counter uses global env ids so
+ *                   results do not depend on the GPU count (R#14)
+ *   initial_capital C0 > 0 (P:L415 $1,000,000)
+ *   cost_rate       c in [0,1) of traded notional, both sides (P:L415 0.2%, R#1–2)
+ *   reward_scale    r = reward_scale * (v_{t+1} - v_t) (R#8)
+ *   gamma           discount in (0,1] for the fitness J (Eq. 1)
+ *   seed            Philox key for the action noise (R#14)                         */
+typedef struct {
+    int32_t n_envs;
+    int32_t n_stocks;
+    int32_t n_feat;
+    int32_t n_agents;
+    int32_t horizon;
+    int32_t h_max;
+    int64_t env_offset;
+    double initial_capital;
+    double cost_rate;
+    double reward_scale;
+    double gamma;
+    uint64_t seed;
+} pod_env_config;
+
+/* Market tensors [dev], float32, row-major, immutable while a handle uses them:
+ *   close [T_data][n] > 0 closing prices p_t
+ *   feat  [T_data][f][n] indicator channels, channel-major, pre-scaled (R#9)   */
+typedef struct {
+    const float* close;
+    const float* feat;
+    int64_t T_data;   /* 2 <= T_data < 2^31 */
+} pod_market;
+
+/* Actor MLP parameters [dev] ("policy ... maps a state to an action
+ * vector over n stocks"; Gaussian head R#12; hidden activation R#13).
+ * `params` holds n_agents contiguous slabs of param_bytes each, laid out as
+ * pod_actor_layout() reports: bf16 weight matrices W_l[out][in_pad] (row-major,
+ * K-major for the tensor cores; pad columns/rows must be finite, zero is
+ * recommended), then float32 biases and float32 log_std.  param_bytes must be
+ * >= layout.param_bytes and a multiple of 16; params must be 16-byte aligned. */
+typedef struct {
+    int32_t n_hidden;   /* 1..POD_MAX_HIDDEN_LAYERS */
+    int32_t hidden;     /* 64, 128, 192, 256 or 512 */
+    int32_t act;        /* 0 = ReLU, 1 = tanh       */
+    int32_t reserved;
+    const void* params;
+    size_t param_bytes;
+} pod_actor;
+
+typedef struct {
+    int32_t obs_dim;       /* 1 + 2n + n f                                   */
+    int32_t k_pad;         /* obs_dim rounded up to 64 (obs row stride)       */
+    int32_t n_out_pad;     /* n rounded up to 16 (head rows)                  */
+    int32_t n_layers;      /* n_hidden + 1                                    */
+    size_t w_offset[POD_MAX_HIDDEN_LAYERS + 1];   /* bytes, bf16 [out_l][in_l] */
+    int32_t w_rows[POD_MAX_HIDDEN_LAYERS + 1];    /* out_l (padded)            */
+    int32_t w_cols[POD_MAX_HIDDEN_LAYERS + 1];    /* in_l  (padded)            */
+    size_t b_offset[POD_MAX_HIDDEN_LAYERS + 1];   /* bytes, float32 [out_l]    */
+    size_t log_std_offset;                        /* bytes, float32 [n_out_pad] */
+    size_t param_bytes;                           /* minimal slab size, %1024==0 */
+} pod_actor_layout;
+
+/* Trajectory buffers [dev] (transitions stay as tensors in
+ * contiguous GPU memory).  T = rollout length, N = n_envs.
+ *   obs      bf16 [T+1][N][k_pad]  s_0..s_T; pad columns written as 0     (required)
+ *   act      f32  [T][N][n]        raw (pre-tanh) sampled action          (required unless injected)
+ *   logp     f32  [T][N]           log pi(raw | s_t)                      (required unless injected)
+ *   rew      f32  [T][N]           r_t (Eq. 2, R#8)                       (required)
+ *   done     u8   [T][N]           episode ended at this transition       (required)
+ *   mu       f32  [T][N][n]        actor mean                             (optional, NULL)
+ *   dbg_aint i16  [T][N][n]        executed integer action a_t            (optional)
+ *   dbg_hold i32  [T][N][n]        h_{t+1} after the trade, before reset  (optional)
+ *   dbg_cash f64  [T][N]           b_{t+1} after the trade, before reset  (optional) */
+typedef struct {
+    uint16_t* obs;
+    float* act;
+    float* logp;
+    float* rew;
+    uint8_t* done;
+    float* mu;
+    int16_t* dbg_aint;
+    int32_t* dbg_hold;
+    double* dbg_cash;
+} pod_traj;
+
+/* ---------------------------------------------------------------- layout */
+/* Parameter-slab layout for an actor over this config's observation (host
+ * only, no device work).  Errors: POD_ERR_ARG / POD_ERR_UNSUPPORTED. */
+pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                pod_actor_layout* out);
+
+/* ----------------------------------------------------------- environment */
+/* Bytes of device workspace a handle for `cfg` needs (host only). */
+pod_status pod_env_workspace_size(const pod_env_config* cfg, size_t* bytes);
+
+/* Validate cfg (S:L139 invariants: C0 > 0, 0 <= c < 1, h_max >= 1,
+ * 0 < gamma <= 1), check the device is sm_100, and bind market + workspace
+ * (ws [dev], >= pod_env_workspace_size bytes, 256-byte aligned).  The env
+ * state is undefined until pod_env_reset.  Errors: ARG, SHAPE, WORKSPACE,
+ * UNSUPPORTED, CUDA. */
+pod_status pod_env_create(const pod_env_config* cfg, const pod_market* market, void* ws,
+                          size_t ws_bytes, pod_env_t** out);
+pod_status pod_env_destroy(pod_env_t* env);
+
+/* Reset every env (R#17): b = C0, h = 0, k = 0, t = s, where s is
+ * the episode start row of the env's tile.
+ *   tile_start_rows [host] int64 [ceil(N/32)], each with s + H <= T_data - 1
+ *                   (else POD_ERR_RANGE); NULL = draw them from the config seed.
+ *   obs0            [dev] bf16 [N][k_pad] or NULL: also write s_0.
+ * Resets the action-noise step counter to 0.  Stream-ordered. */
+pod_status pod_env_reset(pod_env_t* env, const int64_t* tile_start_rows, uint16_t* obs0, void* stream);
+
+/* Run T >= 1 lockstep steps of all envs (a batched environment that
+ * takes a batch of actions and returns a batch of transitions).  Per step t:
+ *   1. actor mean mu = MLP(s_t) on tcgen05 tensor cores (bf16 x bf16 -> f32),
+ *      raw = mu + exp(log_std) z, z ~ N(0,1) from Philox4x32-10 +
+ *      Box–Muller (R#12, R#14), logp, u = tanh(raw), a = sgn(u) floor(|u| h_max
+ *      + 1/2) (R#6);  deterministic != 0: raw = mu (z = 0);
+ *      injected_u [dev] f32 [T][N][n] in [-1,1] (or NULL) replaces 1. by a = map(u)
+ *      and leaves act/logp/mu untouched;
+ *   2. env step (Eqs. 3–4, reward Eq. 2, readings R#1–5, R#18):
+ *      sells then greedy buys in ticker order with a float64 cash ledger,
+ *      r = scale (v' - v), done = (k+1 == H) or (t+1 == T_data-1), auto-reset
+ *      with the terminal transition reported;
+ *   3. s_{t+1} written to obs[t+1].
+ * obs[0] is first written from the carried state, so buffers need not persist
+ * across calls; obs[T] is the bootstrap state.  fitness_out [dev] f64
+ * [n_agents] or NULL: afterwards J_a = mean over agent a's envs of the
+ * discounted return of each env's last completed episode (Eq. 1, R#15).
+ * Errors (host, synchronous): ARG, SHAPE, UNSUPPORTED, CUDA. */
+pod_status pod_rollout(pod_env_t* env, const pod_actor* actor, int32_t T, const pod_traj* traj,
+                       const float* injected_u, int32_t deterministic, double* fitness_out,
+                       void* stream);
+
+/* Fitness J of the current state (same definition as pod_rollout's). */
+pod_status pod_env_fitness(pod_env_t* env, double* fitness_out, void* stream);
+
+/* Copy the carried state to caller buffers [dev] (any may be NULL):
+ * hold i32 [N][n] (env-major), cash/asset/ep_ret f64 [N].  Synchronises the
+ * stream and returns POD_ERR_NONFINITE if the device error word is set. */
+pod_status pod_env_read_state(pod_env_t* env, int32_t* hold, double* cash, double* asset,
+                              double* ep_ret, void* stream);
+
+/* Synchronise `stream` and report (then clear) the device error word. */
+pod_status pod_env_check(pod_env_t* env, void* stream);
+
+/* ---------------------------------------------------------------- GAE */
+/* Generalised advantage estimation over [T][N] (R#11; PPO P:L472):
+ *   delta_t = r_t + gamma (1-d_t) V_{t+1} - V_t,  V_T = boot,
+ *   A_t = delta_t + gamma lambda (1-d_t) A_{t+1}, A_T = 0,  R_t = A_t + V_t.
+ * rew, val f32 [T][N], done u8 [T][N], boot f32 [N] -> adv, ret f32 [T][N], all
+ * [dev], row-major (time-major).  T, N >= 1.  Errors: ARG, CUDA. */
+pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, const float* boot,
+                   int32_t T, int32_t N, float gamma, float lambda, float* adv, float* ret,
+                   void* stream);
+
+/* -------------------------------------------------- generational evolution */
+/* Selector plan ("redistributes the agents with the highest scores to
+ * form a new population", R#16), host only: rank agents by
+ * (J desc, id asc); the first k are elites and keep their parameters; the
+ * eliminated slots, in ascending id, take elites in rank order, round-robin.
+ * fitness [host] f64 [P_total] -> plan [host] i32 [P_total] (source agent
+ * of every slot).  Errors: ARG (k outside [1,P_total], P_total < 1),
+ * NONFINITE. */
+pod_status pod_elite_plan(const double* fitness, int32_t P_total, int32_t k, int32_t* plan);
+
+/* One parameter-slab transfer of a plan, as seen from `rank`:
+ * kind 0 = local device copy src_local -> dst_local, 1 = send slab src_local
+ * to `peer`, 2 = receive into dst_local from `peer`.  Global agent g lives on
+ * rank g / P_local at local index g % P_local. */
+typedef struct {
+    int32_t kind;
+    int32_t peer;
+    int32_t src_local;
+    int32_t dst_local;
+} pod_transfer;
+
+/* Transfers `rank` must execute to realise `plan` (host only).  Sends and
+ * receives between a pair of ranks appear in the same (ascending slot)
+ * order on both sides.  *n_ops gets the count; POD_ERR_ARG if max_ops is too
+ * small or the plan is not a valid elite plan. */
+pod_status pod_elite_transfers(const int32_t* plan, int32_t P_total, int32_t P_local, int32_t rank,
+                               pod_transfer* ops, int32_t max_ops, int32_t* n_ops);
+
+/* NCCL communicator over one process per GPU (libnccl.so.2 is loaded at
+ * pod_comm_init; the torch process group only carries the 128-byte id). */
+pod_status pod_comm_unique_id(uint8_t id[128]);
+pod_status pod_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank,
+                         int32_t max_agents_local, pod_comm_t** out);
+pod_status pod_comm_destroy(pod_comm_t* comm);
+
+/* One generation's selection step across all ranks:
+ *   1. ncclAllGather of fitness_local [dev] f64 [P_local] -> [P_total];
+ *   2. one stream synchronisation and a D2H copy of P_total doubles;
+ *   3. the identical pod_elite_plan on every rank, written to h_plan [host]
+ *      i32 [P_total];
+ *   4. grouped ncclSend/ncclRecv (+ local cudaMemcpyAsync) moving elite
+ *      parameter slabs into the eliminated slots of params [dev]
+ *      [P_local][param_bytes] ("sending the network parameters").
+ * Synchronous w.r.t. the plan (step 2), asynchronous for the slab moves.
+ * Errors: ARG, NONFINITE, NCCL, CUDA. */
+pod_status pod_select_elite(pod_comm_t* comm, const double* fitness_local, int32_t P_local, int32_t k,
+                            void* params, size_t param_bytes, int32_t* h_plan, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POD_H */

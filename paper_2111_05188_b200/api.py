@@ -1,0 +1,243 @@
+"""Thin Python binding over libpod.so (same names as the C ABI).
+
+PyTorch supplies device memory, streams and process groups; every step of the
+hot path runs in libpod's CUDA kernels.  Nothing here computes the method:
+functions allocate or lay out buffers and marshal pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, load
+
+ENV_TILE = 32
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def make_config(n_envs, n_stocks, n_feat, horizon, n_agents=1, h_max=100, env_offset=0, initial_capital=1e6,
+                cost_rate=0.002, reward_scale=1.0, gamma=0.99, seed=0) -> _lib.EnvConfig:
+    return _lib.EnvConfig(n_envs, n_stocks, n_feat, n_agents, horizon, h_max, env_offset, initial_capital, cost_rate,
+                          reward_scale, gamma, seed)
+
+
+def config_from_workload(w, n_envs=None, env_offset=0) -> _lib.EnvConfig:
+    return make_config(n_envs or w.n_envs, w.n_stocks, w.n_feat, w.horizon, w.n_agents, w.h_max, env_offset, w.C0,
+                       w.cost, w.reward_scale, w.gamma, w.seed)
+
+
+def actor_layout(cfg: _lib.EnvConfig, n_hidden: int, hidden: int) -> _lib.ActorLayout:
+    L = _lib.ActorLayout()
+    check(load().pod_actor_layout_get(C.byref(cfg), n_hidden, hidden, C.byref(L)), "pod_actor_layout_get")
+    return L
+
+
+def pod_env_workspace_size(cfg: _lib.EnvConfig) -> int:
+    b = C.c_size_t(0)
+    check(load().pod_env_workspace_size(C.byref(cfg), C.byref(b)), "pod_env_workspace_size")
+    return int(b.value)
+
+
+def pack_actor_params(cfg: _lib.EnvConfig, agents: Sequence, n_hidden: int, hidden: int,
+                      device="cuda") -> torch.Tensor:
+    """Lay out per-agent weights (synth.ActorWeights: W[l] [out, in] bf16-representable float32,
+    b[l], log_std) in the slab format of pod_actor_layout: returns uint8 [P, param_bytes]."""
+    L = actor_layout(cfg, n_hidden, hidden)
+    pb = int(L.param_bytes)
+    slab = np.zeros((len(agents), pb), dtype=np.uint8)
+    for a, w in enumerate(agents):
+        for l in range(L.n_layers):
+            rows, cols = L.w_rows[l], L.w_cols[l]
+            Wp = torch.zeros((rows, cols), dtype=torch.bfloat16)
+            Wl = torch.from_numpy(np.ascontiguousarray(w.W[l], dtype=np.float32))
+            Wp[: Wl.shape[0], : Wl.shape[1]] = Wl.to(torch.bfloat16)
+            raw = Wp.view(torch.uint8).numpy().ravel()
+            o = int(L.w_offset[l])
+            slab[a, o : o + raw.size] = raw
+            bp = np.zeros(rows, dtype=np.float32)
+            bp[: w.b[l].size] = w.b[l]
+            o = int(L.b_offset[l])
+            slab[a, o : o + 4 * rows] = bp.view(np.uint8)
+        ls = np.zeros(L.n_out_pad, dtype=np.float32)
+        ls[: w.log_std.size] = w.log_std
+        o = int(L.log_std_offset)
+        slab[a, o : o + 4 * L.n_out_pad] = ls.view(np.uint8)
+    return torch.from_numpy(slab).to(device)
+
+
+@dataclass
+class Trajectory:
+    obs: torch.Tensor                  # bf16 [T+1, N, k_pad]
+    act: Optional[torch.Tensor]        # f32 [T, N, n]
+    logp: Optional[torch.Tensor]       # f32 [T, N]
+    rew: torch.Tensor                  # f32 [T, N]
+    done: torch.Tensor                 # u8 [T, N]
+    mu: Optional[torch.Tensor] = None
+    dbg_aint: Optional[torch.Tensor] = None
+    dbg_hold: Optional[torch.Tensor] = None
+    dbg_cash: Optional[torch.Tensor] = None
+
+    @staticmethod
+    def allocate(T: int, N: int, n: int, k_pad: int, device="cuda", debug=False, mu=False, sampled=True):
+        z = dict(device=device)
+        return Trajectory(
+            obs=torch.empty((T + 1, N, k_pad), dtype=torch.bfloat16, **z),
+            act=torch.empty((T, N, n), dtype=torch.float32, **z) if sampled else None,
+            logp=torch.empty((T, N), dtype=torch.float32, **z) if sampled else None,
+            rew=torch.empty((T, N), dtype=torch.float32, **z),
+            done=torch.empty((T, N), dtype=torch.uint8, **z),
+            mu=torch.empty((T, N, n), dtype=torch.float32, **z) if (mu or debug) and sampled else None,
+            dbg_aint=torch.empty((T, N, n), dtype=torch.int16, **z) if debug else None,
+            dbg_hold=torch.empty((T, N, n), dtype=torch.int32, **z) if debug else None,
+            dbg_cash=torch.empty((T, N), dtype=torch.float64, **z) if debug else None,
+        )
+
+    def c(self) -> _lib.Traj:
+        return _lib.Traj(*[None if x is None else x.data_ptr() for x in
+                           (self.obs, self.act, self.logp, self.rew, self.done, self.mu, self.dbg_aint,
+                            self.dbg_hold, self.dbg_cash)])
+
+
+class Env:
+    """pod_env_t handle.  Owns (via torch) its workspace; the market tensors
+    must stay alive as long as the Env (it keeps references)."""
+
+    def __init__(self, cfg: _lib.EnvConfig, close: torch.Tensor, feat: Optional[torch.Tensor]):
+        L = load()
+        assert close.is_cuda and close.dtype == torch.float32 and close.is_contiguous()
+        self.cfg = cfg
+        self.close = close
+        self.feat = feat
+        self.T_data = int(close.shape[0])
+        self.market = _lib.Market(close.data_ptr(), None if feat is None else feat.data_ptr(), self.T_data)
+        self.ws = torch.empty(pod_env_workspace_size(cfg), dtype=torch.uint8, device=close.device)
+        h = C.c_void_p()
+        check(L.pod_env_create(C.byref(cfg), C.byref(self.market), _ptr(self.ws), self.ws.numel(), C.byref(h)),
+              "pod_env_create")
+        self.h = h
+        self.N = cfg.n_envs
+        self.n = cfg.n_stocks
+        self.n_tiles = (self.N + ENV_TILE - 1) // ENV_TILE
+        od = 1 + 2 * cfg.n_stocks + cfg.n_stocks * cfg.n_feat
+        self.obs_dim = od
+        self.k_pad = (od + 63) // 64 * 64
+
+    def close_handle(self):
+        if getattr(self, "h", None):
+            load().pod_env_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close_handle()
+        except Exception:
+            pass
+
+    def reset(self, tile_starts: Optional[np.ndarray] = None, obs0: Optional[torch.Tensor] = None, stream=None):
+        st = None
+        if tile_starts is not None:
+            st = np.ascontiguousarray(tile_starts, dtype=np.int64)
+            assert st.size == self.n_tiles
+        check(load().pod_env_reset(self.h, None if st is None else st.ctypes.data_as(C.c_void_p), _ptr(obs0),
+                                   _stream(stream)), "pod_env_reset")
+
+    def rollout(self, T: int, traj: Trajectory, actor: Optional[_lib.Actor] = None,
+                injected_u: Optional[torch.Tensor] = None, deterministic=False,
+                fitness_out: Optional[torch.Tensor] = None, stream=None):
+        check(load().pod_rollout(self.h, None if actor is None else C.byref(actor), int(T), C.byref(traj.c()),
+                                 _ptr(injected_u), 1 if deterministic else 0, _ptr(fitness_out), _stream(stream)),
+              "pod_rollout")
+
+    def fitness(self, out: torch.Tensor, stream=None):
+        check(load().pod_env_fitness(self.h, _ptr(out), _stream(stream)), "pod_env_fitness")
+
+    def read_state(self, stream=None):
+        dev = self.close.device
+        hold = torch.empty((self.N, self.n), dtype=torch.int32, device=dev)
+        cash = torch.empty(self.N, dtype=torch.float64, device=dev)
+        asset = torch.empty(self.N, dtype=torch.float64, device=dev)
+        ep = torch.empty(self.N, dtype=torch.float64, device=dev)
+        check(load().pod_env_read_state(self.h, _ptr(hold), _ptr(cash), _ptr(asset), _ptr(ep), _stream(stream)),
+              "pod_env_read_state")
+        return hold, cash, asset, ep
+
+    def check(self, stream=None):
+        check(load().pod_env_check(self.h, _stream(stream)), "pod_env_check")
+
+
+def make_actor(n_hidden: int, hidden: int, params: torch.Tensor, act: int = 0) -> _lib.Actor:
+    return _lib.Actor(n_hidden, hidden, act, 0, params.data_ptr(), params.shape[1] if params.dim() == 2 else params.numel())
+
+
+def pod_gae(rew, val, done, boot, gamma, lam, adv=None, ret=None, stream=None):
+    T, N = rew.shape
+    adv = torch.empty_like(rew) if adv is None else adv
+    ret = torch.empty_like(rew) if ret is None else ret
+    check(load().pod_gae(_ptr(rew), _ptr(val), _ptr(done), _ptr(boot), T, N, float(gamma), float(lam), _ptr(adv),
+                         _ptr(ret), _stream(stream)), "pod_gae")
+    return adv, ret
+
+
+def pod_elite_plan(fitness: np.ndarray, k: int) -> np.ndarray:
+    f = np.ascontiguousarray(fitness, dtype=np.float64)
+    plan = np.zeros(f.size, dtype=np.int32)
+    check(load().pod_elite_plan(f.ctypes.data_as(C.c_void_p), f.size, int(k), plan.ctypes.data_as(C.c_void_p)),
+          "pod_elite_plan")
+    return plan
+
+
+def pod_elite_transfers(plan: np.ndarray, P_local: int, rank: int):
+    p = np.ascontiguousarray(plan, dtype=np.int32)
+    ops = (_lib.Transfer * (2 * p.size + 2))()
+    n = C.c_int32(0)
+    check(load().pod_elite_transfers(p.ctypes.data_as(C.c_void_p), p.size, int(P_local), int(rank), ops, len(ops),
+                                     C.byref(n)), "pod_elite_transfers")
+    return [(ops[i].kind, ops[i].peer, ops[i].src_local, ops[i].dst_local) for i in range(n.value)]
+
+
+class Comm:
+    """NCCL communicator of libpod (one process per GPU).  The torch process
+    group (if any) only broadcasts the 128-byte unique id."""
+
+    def __init__(self, nranks: int, rank: int, max_agents_local: int, group=None):
+        L = load()
+        uid = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            check(L.pod_comm_unique_id(uid.ctypes.data_as(C.c_void_p)), "pod_comm_unique_id")
+        if nranks > 1:
+            import torch.distributed as dist
+            t = torch.from_numpy(uid.astype(np.int64))
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, 0, group=group)
+            uid = t.cpu().numpy().astype(np.uint8)
+        h = C.c_void_p()
+        check(L.pod_comm_init(uid.ctypes.data_as(C.c_void_p), nranks, rank, max_agents_local, C.byref(h)),
+              "pod_comm_init")
+        self.h = h
+        self.nranks, self.rank = nranks, rank
+
+    def select_elite(self, fitness_local: torch.Tensor, k: int, params: torch.Tensor, stream=None) -> np.ndarray:
+        P_local = fitness_local.numel()
+        plan = np.zeros(P_local * self.nranks, dtype=np.int32)
+        check(load().pod_select_elite(self.h, _ptr(fitness_local), P_local, int(k), _ptr(params), params.shape[1],
+                                      plan.ctypes.data_as(C.c_void_p), _stream(stream)), "pod_select_elite")
+        return plan
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            load().pod_comm_destroy(self.h)
+            self.h = None

@@ -1,0 +1,584 @@
+// pod_api.cu — host side of libpod.so: the C ABI declared in include/pod.h.
+// Validation, workspace carving, TMA descriptor encoding (cuTensorMapEncodeTiled
+// through cudaGetDriverEntryPoint, so the library links no libcuda), the
+// rollout driver (T x {actor, env-step} captured once into a CUDA graph and
+// replayed), GAE and fitness launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "actor_kernel.cuh"
+#include "env_kernel.cuh"
+#include "gae_kernel.cuh"
+#include "pod.h"
+#include "pod_internal.h"
+
+using namespace pod;
+
+// ------------------------------------------------------------ error helpers
+static thread_local char g_last_error[512] = "";
+
+pod_status pod_fail(pod_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+#define POD_CUDA(call)                                                                                \
+    do {                                                                                              \
+        cudaError_t _e = (call);                                                                      \
+        if (_e != cudaSuccess) return pod_fail(POD_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+    } while (0)
+
+extern "C" const char* pod_status_string(pod_status s) {
+    switch (s) {
+        case POD_OK: return "POD_OK";
+        case POD_ERR_ARG: return "POD_ERR_ARG";
+        case POD_ERR_SHAPE: return "POD_ERR_SHAPE";
+        case POD_ERR_RANGE: return "POD_ERR_RANGE";
+        case POD_ERR_WORKSPACE: return "POD_ERR_WORKSPACE";
+        case POD_ERR_CUDA: return "POD_ERR_CUDA";
+        case POD_ERR_NCCL: return "POD_ERR_NCCL";
+        case POD_ERR_NONFINITE: return "POD_ERR_NONFINITE";
+        case POD_ERR_UNSUPPORTED: return "POD_ERR_UNSUPPORTED";
+    }
+    return "POD_ERR_UNKNOWN";
+}
+extern "C" const char* pod_last_error(void) { return g_last_error; }
+extern "C" int pod_abi_version(void) { return POD_ABI_VERSION; }
+
+static inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------ device check
+pod_status pod_require_sm100() {
+    static thread_local int ok_dev = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return pod_fail(POD_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+    if (dev == ok_dev) return POD_OK;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return pod_fail(POD_ERR_UNSUPPORTED, "device %d is sm_%d%d; libpod is built for sm_100a only", dev, major, minor);
+    ok_dev = dev;
+    return POD_OK;
+}
+
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// bf16 tensor, rank 2 or 3, 128B swizzle, box inner 64 elements (128 B)
+static pod_status encode_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                              const uint64_t* strides_bytes, const uint32_t* box) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t d[3], s[2];
+    cuuint32_t b[3], es[3] = {1, 1, 1};
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+    }
+    for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank), const_cast<void*>(base), d, s, b,
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return POD_OK;
+}
+
+// ------------------------------------------------------------ layout
+static pod_status dims_of(const pod_env_config* c, int* obs_dim, int* k_pad, int* n_out_pad) {
+    if (!c) return pod_fail(POD_ERR_ARG, "config is NULL");
+    if (c->n_stocks < 1 || c->n_feat < 0) return pod_fail(POD_ERR_ARG, "n_stocks >= 1 and n_feat >= 0 required");
+    *obs_dim = 1 + 2 * c->n_stocks + c->n_stocks * c->n_feat;
+    *k_pad = static_cast<int>(round_up(static_cast<size_t>(*obs_dim), 64));
+    *n_out_pad = static_cast<int>(round_up(static_cast<size_t>(c->n_stocks), 16));
+    if (*k_pad > ENV_MAX_KPAD || c->n_stocks > ENV_MAX_STOCKS)
+        return pod_fail(POD_ERR_UNSUPPORTED, "obs_dim %d exceeds the kernel limit (k_pad <= %d, n <= %d)", *obs_dim,
+                        ENV_MAX_KPAD, ENV_MAX_STOCKS);
+    return POD_OK;
+}
+
+extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                           pod_actor_layout* out) {
+    if (!out) return pod_fail(POD_ERR_ARG, "out is NULL");
+    int od = 0, kp = 0, nop = 0;
+    pod_status st = dims_of(cfg, &od, &kp, &nop);
+    if (st) return st;
+    if (n_hidden < 1 || n_hidden > POD_MAX_HIDDEN_LAYERS)
+        return pod_fail(POD_ERR_UNSUPPORTED, "n_hidden must be in [1, %d]", POD_MAX_HIDDEN_LAYERS);
+    if (!(hidden == 64 || hidden == 128 || hidden == 192 || hidden == 256 || hidden == 512))
+        return pod_fail(POD_ERR_UNSUPPORTED, "hidden must be one of 64, 128, 192, 256, 512");
+    if (nop > 256) return pod_fail(POD_ERR_UNSUPPORTED, "n_stocks > 256");
+    memset(out, 0, sizeof(*out));
+    out->obs_dim = od;
+    out->k_pad = kp;
+    out->n_out_pad = nop;
+    out->n_layers = n_hidden + 1;
+    size_t off = 0;
+    for (int l = 0; l <= n_hidden; ++l) {
+        out->w_rows[l] = l == n_hidden ? nop : hidden;
+        out->w_cols[l] = l == 0 ? kp : hidden;
+        out->w_offset[l] = off;
+        off += static_cast<size_t>(out->w_rows[l]) * out->w_cols[l] * 2;
+        off = round_up(off, 128);
+    }
+    for (int l = 0; l <= n_hidden; ++l) {
+        out->b_offset[l] = off;
+        off += static_cast<size_t>(out->w_rows[l]) * 4;
+        off = round_up(off, 128);
+    }
+    out->log_std_offset = off;
+    off += static_cast<size_t>(nop) * 4;
+    out->param_bytes = round_up(off, 1024);
+    return POD_OK;
+}
+
+// ------------------------------------------------------------ env handle
+struct GraphKey {
+    int32_t T, deterministic, n_hidden, hidden, act, pad_;
+    const void* ptrs[12];
+    size_t param_bytes;
+};
+
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t last_use;
+};
+
+struct pod_env {
+    pod_env_config cfg;
+    pod_market market;
+    int obs_dim, k_pad, n_out_pad, n_tiles, per_agent;
+    // workspace carve
+    int32_t* hold;
+    int16_t* aint;
+    double *cash, *asset, *disc, *ep_ret, *tile_gpow;
+    int32_t *tile_start, *tile_k;
+    uint64_t* step;
+    uint32_t* err;
+    int32_t* h_starts;   // pinned staging for reset
+    cudaStream_t cap_stream;
+    std::vector<GraphEntry> graphs;
+    uint64_t use_clock;
+    bool use_graphs;
+};
+
+struct WsLayout {
+    size_t hold, aint, cash, asset, disc, ep_ret, tile_start, tile_k, tile_gpow, step, err, total;
+};
+
+static WsLayout ws_layout(const pod_env_config* c) {
+    WsLayout w{};
+    const size_t N = static_cast<size_t>(c->n_envs), n = static_cast<size_t>(c->n_stocks);
+    const size_t NT = (N + POD_ENV_TILE - 1) / POD_ENV_TILE;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = round_up(off + bytes, 256);
+        return o;
+    };
+    w.hold = take(n * N * 4);
+    w.aint = take(n * N * 2);
+    w.cash = take(N * 8);
+    w.asset = take(N * 8);
+    w.disc = take(N * 8);
+    w.ep_ret = take(N * 8);
+    w.tile_start = take(NT * 4);
+    w.tile_k = take(NT * 4);
+    w.tile_gpow = take(NT * 8);
+    w.step = take(8);
+    w.err = take(4);
+    w.total = off;
+    return w;
+}
+
+static pod_status check_config(const pod_env_config* c) {
+    if (!c) return pod_fail(POD_ERR_ARG, "config is NULL");
+    if (c->n_envs < 1) return pod_fail(POD_ERR_ARG, "n_envs must be >= 1");
+    if (c->n_agents < 1 || c->n_envs % c->n_agents != 0)
+        return pod_fail(POD_ERR_ARG, "n_agents must be >= 1 and divide n_envs");
+    if (c->horizon < 1) return pod_fail(POD_ERR_ARG, "horizon must be >= 1");
+    if (c->h_max < 1 || c->h_max > 32767) return pod_fail(POD_ERR_ARG, "h_max must be in [1, 32767]");
+    if (!(c->initial_capital > 0.0)) return pod_fail(POD_ERR_ARG, "initial_capital must be > 0");
+    if (!(c->cost_rate >= 0.0 && c->cost_rate < 1.0)) return pod_fail(POD_ERR_ARG, "cost_rate must be in [0, 1)");
+    if (!(c->gamma > 0.0 && c->gamma <= 1.0)) return pod_fail(POD_ERR_ARG, "gamma must be in (0, 1]");
+    if (!(c->reward_scale == c->reward_scale)) return pod_fail(POD_ERR_ARG, "reward_scale is NaN");
+    int od = 0, kp = 0, nop = 0;
+    return dims_of(c, &od, &kp, &nop);
+}
+
+extern "C" pod_status pod_env_workspace_size(const pod_env_config* cfg, size_t* bytes) {
+    pod_status st = check_config(cfg);
+    if (st) return st;
+    if (!bytes) return pod_fail(POD_ERR_ARG, "bytes is NULL");
+    *bytes = ws_layout(cfg).total;
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market* market, void* ws, size_t ws_bytes,
+                                     pod_env_t** out) {
+    pod_status st = check_config(cfg);
+    if (st) return st;
+    if (!market || !market->close || (cfg->n_feat > 0 && !market->feat) || !out)
+        return pod_fail(POD_ERR_ARG, "market tensors and out must be non-NULL");
+    if (market->T_data < 2 || market->T_data >= (1ll << 31)) return pod_fail(POD_ERR_SHAPE, "T_data must be in [2, 2^31)");
+    WsLayout w = ws_layout(cfg);
+    if (!ws || ws_bytes < w.total) return pod_fail(POD_ERR_WORKSPACE, "workspace needs %zu bytes", w.total);
+    if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return pod_fail(POD_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+    st = pod_require_sm100();
+    if (st) return st;
+    pod_env* e = new pod_env();
+    e->cfg = *cfg;
+    e->market = *market;
+    dims_of(cfg, &e->obs_dim, &e->k_pad, &e->n_out_pad);
+    e->n_tiles = (cfg->n_envs + POD_ENV_TILE - 1) / POD_ENV_TILE;
+    e->per_agent = cfg->n_envs / cfg->n_agents;
+    char* b = static_cast<char*>(ws);
+    e->hold = reinterpret_cast<int32_t*>(b + w.hold);
+    e->aint = reinterpret_cast<int16_t*>(b + w.aint);
+    e->cash = reinterpret_cast<double*>(b + w.cash);
+    e->asset = reinterpret_cast<double*>(b + w.asset);
+    e->disc = reinterpret_cast<double*>(b + w.disc);
+    e->ep_ret = reinterpret_cast<double*>(b + w.ep_ret);
+    e->tile_start = reinterpret_cast<int32_t*>(b + w.tile_start);
+    e->tile_k = reinterpret_cast<int32_t*>(b + w.tile_k);
+    e->tile_gpow = reinterpret_cast<double*>(b + w.tile_gpow);
+    e->step = reinterpret_cast<uint64_t*>(b + w.step);
+    e->err = reinterpret_cast<uint32_t*>(b + w.err);
+    e->use_clock = 0;
+    const char* ng = getenv("POD_NO_GRAPH");
+    e->use_graphs = !(ng && ng[0] == '1');
+    cudaError_t ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_starts), sizeof(int32_t) * e->n_tiles);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
+    if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(actor_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(gae_smem_bytes()));
+    if (ce != cudaSuccess) {
+        delete e;
+        return pod_fail(POD_ERR_CUDA, "pod_env_create: %s", cudaGetErrorString(ce));
+    }
+    *out = e;
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_destroy(pod_env_t* e) {
+    if (!e) return POD_OK;
+    for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    if (e->h_starts) cudaFreeHost(e->h_starts);
+    delete e;
+    return POD_OK;
+}
+
+static EnvArgs env_args(const pod_env* e, int mode) {
+    EnvArgs a{};
+    a.N = e->cfg.n_envs;
+    a.n = e->cfg.n_stocks;
+    a.f = e->cfg.n_feat;
+    a.k_pad = e->k_pad;
+    a.obs_dim = e->obs_dim;
+    a.horizon = e->cfg.horizon;
+    a.n_tiles = e->n_tiles;
+    a.mode = mode;
+    a.T_data = e->market.T_data;
+    a.C0 = e->cfg.initial_capital;
+    a.cost = e->cfg.cost_rate;
+    a.scale = e->cfg.reward_scale;
+    a.gamma = e->cfg.gamma;
+    a.close = e->market.close;
+    a.feat = e->market.feat;
+    a.hold = e->hold;
+    a.aint = e->aint;
+    a.cash = e->cash;
+    a.asset = e->asset;
+    a.disc = e->disc;
+    a.ep_ret = e->ep_ret;
+    a.tile_start = e->tile_start;
+    a.tile_k = e->tile_k;
+    a.tile_gpow = e->tile_gpow;
+    a.err = e->err;
+    return a;
+}
+
+static inline int env_blocks(const pod_env* e) { return (e->n_tiles + ENV_WARPS - 1) / ENV_WARPS; }
+
+static uint64_t splitmix64(uint64_t& x) {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_t* obs0, void* stream) {
+    if (!e) return pod_fail(POD_ERR_ARG, "env is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t max_start = e->market.T_data - 1 - e->cfg.horizon;
+    if (max_start < 0) return pod_fail(POD_ERR_RANGE, "horizon %d does not fit in T_data %lld", e->cfg.horizon,
+                                       static_cast<long long>(e->market.T_data));
+    uint64_t rs = e->cfg.seed ^ 0x5EED5EED5EEDull;
+    for (int i = 0; i < e->n_tiles; ++i) {
+        int64_t v = starts ? starts[i] : static_cast<int64_t>(splitmix64(rs) % static_cast<uint64_t>(max_start + 1));
+        if (v < 0 || v > max_start)
+            return pod_fail(POD_ERR_RANGE, "tile %d start row %lld outside [0, %lld] (start + H <= T_data - 1)", i,
+                            static_cast<long long>(v), static_cast<long long>(max_start));
+        e->h_starts[i] = static_cast<int32_t>(v);
+    }
+    POD_CUDA(cudaMemcpyAsync(e->tile_start, e->h_starts, sizeof(int32_t) * e->n_tiles, cudaMemcpyHostToDevice, s));
+    POD_CUDA(cudaMemsetAsync(e->step, 0, 8, s));
+    EnvArgs a = env_args(e, 2);
+    a.obs_out = obs0;
+    env_step_kernel<<<env_blocks(e), 32 * ENV_WARPS, 0, s>>>(a);
+    POD_CUDA(cudaGetLastError());
+    POD_CUDA(cudaStreamSynchronize(s));   // the pinned staging buffer is reused by the next reset
+    return POD_OK;
+}
+
+// ------------------------------------------------------------ rollout
+struct RolloutPlan {
+    bool injected;
+    ActorMaps maps;
+    ActorArgs aa;
+    size_t actor_smem;
+};
+
+static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj,
+                                  double* fitness_out, cudaStream_t s) {
+    const int N = e->cfg.n_envs, n = e->cfg.n_stocks;
+    // s_0 from the carried state
+    EnvArgs a0 = env_args(e, 1);
+    a0.obs_out = tr->obs;
+    env_step_kernel<<<env_blocks(e), 32 * ENV_WARPS, 0, s>>>(a0);
+    for (int t = 0; t < T; ++t) {
+        if (p.injected) {
+            const int64_t tot = static_cast<int64_t>(N) * n;
+            inject_map_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(
+                inj + static_cast<int64_t>(t) * N * n, N, n, e->cfg.h_max, e->aint,
+                tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr);
+        } else {
+            ActorArgs aa = p.aa;
+            aa.t = t;
+            aa.obs_row0 = t * N;
+            aa.act_out = tr->act + static_cast<int64_t>(t) * N * n;
+            aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
+            aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
+            aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
+            const unsigned grid = static_cast<unsigned>(e->cfg.n_agents * aa.tiles_per_agent);
+            actor_forward_kernel<<<grid, ACT_THREADS, p.actor_smem, s>>>(p.maps, aa);
+        }
+        EnvArgs a = env_args(e, 0);
+        a.rew = tr->rew + static_cast<int64_t>(t) * N;
+        a.done = tr->done + static_cast<int64_t>(t) * N;
+        a.obs_out = tr->obs + static_cast<int64_t>(t + 1) * N * e->k_pad;
+        a.dbg_hold = tr->dbg_hold ? tr->dbg_hold + static_cast<int64_t>(t) * N * n : nullptr;
+        a.dbg_cash = tr->dbg_cash ? tr->dbg_cash + static_cast<int64_t>(t) * N : nullptr;
+        env_step_kernel<<<env_blocks(e), 32 * ENV_WARPS, 0, s>>>(a);
+    }
+    if (!p.injected) bump_step_kernel<<<1, 1, 0, s>>>(e->step, static_cast<uint64_t>(T));
+    if (fitness_out) fitness_kernel<<<e->cfg.n_agents, 256, 0, s>>>(e->ep_ret, e->per_agent, fitness_out);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t T, const pod_traj* tr,
+                                  const float* injected_u, int32_t deterministic, double* fitness_out, void* stream) {
+    if (!e || !tr) return pod_fail(POD_ERR_ARG, "env and traj must be non-NULL");
+    if (T < 1) return pod_fail(POD_ERR_ARG, "T must be >= 1");
+    if (!tr->obs || !tr->rew || !tr->done) return pod_fail(POD_ERR_ARG, "traj.obs, traj.rew and traj.done are required");
+    if (reinterpret_cast<uintptr_t>(tr->obs) % 16 != 0) return pod_fail(POD_ERR_ARG, "traj.obs must be 16-byte aligned");
+    const int N = e->cfg.n_envs;
+    if (static_cast<int64_t>(T + 1) * N >= (1ll << 31)) return pod_fail(POD_ERR_SHAPE, "(T+1) * N must be < 2^31");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    RolloutPlan p{};
+    p.injected = injected_u != nullptr;
+    if (!p.injected) {
+        if (!actor || !actor->params) return pod_fail(POD_ERR_ARG, "actor (or injected_u) is required");
+        if (!tr->act || !tr->logp) return pod_fail(POD_ERR_ARG, "traj.act and traj.logp are required when sampling");
+        pod_actor_layout L;
+        pod_status st = pod_actor_layout_get(&e->cfg, actor->n_hidden, actor->hidden, &L);
+        if (st) return st;
+        if (actor->act != 0 && actor->act != 1) return pod_fail(POD_ERR_ARG, "actor.act must be 0 (ReLU) or 1 (tanh)");
+        if (actor->param_bytes < L.param_bytes || actor->param_bytes % 16 != 0)
+            return pod_fail(POD_ERR_SHAPE, "param_bytes %zu must be >= %zu and a multiple of 16", actor->param_bytes,
+                            L.param_bytes);
+        if (reinterpret_cast<uintptr_t>(actor->params) % 16 != 0)
+            return pod_fail(POD_ERR_ARG, "actor.params must be 16-byte aligned");
+        // TMA descriptors: obs [(T+1) N][k_pad], weights [agents][out][in]
+        {
+            const uint64_t dims[2] = {static_cast<uint64_t>(e->k_pad), static_cast<uint64_t>(T + 1) * N};
+            const uint64_t str[1] = {static_cast<uint64_t>(e->k_pad) * 2};
+            const uint32_t box[2] = {64, 128};
+            st = encode_bf16(&p.maps.obs, tr->obs, 2, dims, str, box);
+            if (st) return st;
+        }
+        int bn_max = 16;
+        for (int l = 0; l < L.n_layers; ++l) {
+            const int rows = L.w_rows[l];
+            const int bn = rows > 256 ? 256 : rows;
+            bn_max = bn > bn_max ? bn : bn_max;
+            const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
+                                      static_cast<uint64_t>(e->cfg.n_agents)};
+            const uint64_t str[2] = {static_cast<uint64_t>(L.w_cols[l]) * 2, actor->param_bytes};
+            const uint32_t box[3] = {64, static_cast<uint32_t>(bn), 1};
+            st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 3, dims, str, box);
+            if (st) return st;
+        }
+        ActorArgs& aa = p.aa;
+        aa.N = N;
+        aa.per_agent = e->per_agent;
+        aa.tiles_per_agent = (e->per_agent + 127) / 128;
+        aa.n = e->cfg.n_stocks;
+        aa.n_out_pad = L.n_out_pad;
+        aa.k_pad = L.k_pad;
+        aa.hidden = actor->hidden;
+        aa.n_layers = L.n_layers;
+        aa.act = actor->act;
+        aa.h_max = e->cfg.h_max;
+        aa.deterministic = deterministic ? 1 : 0;
+        aa.bn_max = bn_max;
+        aa.seed = e->cfg.seed;
+        aa.env_offset = e->cfg.env_offset;
+        aa.step_base = e->step;
+        aa.params = static_cast<const char*>(actor->params);
+        aa.param_bytes = actor->param_bytes;
+        for (int l = 0; l < L.n_layers; ++l) aa.b_off[l] = L.b_offset[l];
+        aa.log_std_off = L.log_std_offset;
+        aa.aint = e->aint;
+        aa.err = e->err;
+        const int ka = (L.k_pad > actor->hidden ? L.k_pad : actor->hidden) / 64;
+        p.actor_smem = 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * bn_max * 128 + 128;
+        if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
+    }
+    if (!e->use_graphs) return enqueue_rollout(e, p, T, tr, injected_u, fitness_out, s);
+
+    GraphKey key;
+    memset(&key, 0, sizeof(key));
+    key.T = T;
+    key.deterministic = deterministic ? 1 : 0;
+    if (!p.injected) {
+        key.n_hidden = actor->n_hidden;
+        key.hidden = actor->hidden;
+        key.act = actor->act;
+        key.param_bytes = actor->param_bytes;
+        key.ptrs[0] = actor->params;
+    }
+    const void* ptrs[] = {tr->obs, tr->act, tr->logp, tr->rew, tr->done, tr->mu, tr->dbg_aint,
+                          tr->dbg_hold, tr->dbg_cash, injected_u, fitness_out};
+    for (int i = 0; i < 11; ++i) key.ptrs[1 + i] = ptrs[i];
+    GraphEntry* hit = nullptr;
+    for (auto& g : e->graphs)
+        if (memcmp(&g.key, &key, sizeof(key)) == 0) hit = &g;
+    if (!hit) {
+        cudaGraph_t graph;
+        POD_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+        pod_status st = enqueue_rollout(e, p, T, tr, injected_u, fitness_out, e->cap_stream);
+        cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &graph);
+        if (st) return st;
+        if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+        cudaGraphExec_t exec;
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+        if (e->graphs.size() >= 8) {
+            size_t victim = 0;
+            for (size_t i = 1; i < e->graphs.size(); ++i)
+                if (e->graphs[i].last_use < e->graphs[victim].last_use) victim = i;
+            cudaGraphExecDestroy(e->graphs[victim].exec);
+            e->graphs.erase(e->graphs.begin() + static_cast<long>(victim));
+        }
+        e->graphs.push_back(GraphEntry{key, exec, 0});
+        hit = &e->graphs.back();
+    }
+    hit->last_use = ++e->use_clock;
+    POD_CUDA(cudaGraphLaunch(hit->exec, s));
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_fitness(pod_env_t* e, double* fitness_out, void* stream) {
+    if (!e || !fitness_out) return pod_fail(POD_ERR_ARG, "env and fitness_out must be non-NULL");
+    fitness_kernel<<<e->cfg.n_agents, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->ep_ret, e->per_agent, fitness_out);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_check(pod_env_t* e, void* stream) {
+    if (!e) return pod_fail(POD_ERR_ARG, "env is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t h = 0;
+    POD_CUDA(cudaStreamSynchronize(s));
+    POD_CUDA(cudaMemcpy(&h, e->err, 4, cudaMemcpyDeviceToHost));
+    if (h) {
+        POD_CUDA(cudaMemset(e->err, 0, 4));
+        return pod_fail(POD_ERR_NONFINITE, "device error word 0x%x (1 = non-finite actor mean, 2 = non-finite account value)", h);
+    }
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_read_state(pod_env_t* e, int32_t* hold, double* cash, double* asset, double* ep_ret,
+                                         void* stream) {
+    if (!e) return pod_fail(POD_ERR_ARG, "env is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int N = e->cfg.n_envs, n = e->cfg.n_stocks;
+    if (hold) {
+        const int64_t tot = static_cast<int64_t>(N) * n;
+        hold_transpose_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(e->hold, N, n, hold);
+        POD_CUDA(cudaGetLastError());
+    }
+    if (cash) POD_CUDA(cudaMemcpyAsync(cash, e->cash, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    if (asset) POD_CUDA(cudaMemcpyAsync(asset, e->asset, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    if (ep_ret) POD_CUDA(cudaMemcpyAsync(ep_ret, e->ep_ret, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    return pod_env_check(e, stream);
+}
+
+// ------------------------------------------------------------ GAE
+extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
+                              int32_t N, float gamma, float lambda, float* adv, float* ret, void* stream) {
+    if (!rew || !val || !done || !boot || !adv || !ret) return pod_fail(POD_ERR_ARG, "GAE pointers must be non-NULL");
+    if (T < 1 || N < 1) return pod_fail(POD_ERR_ARG, "T and N must be >= 1");
+    if (static_cast<int64_t>(T) * N >= (1ll << 40)) return pod_fail(POD_ERR_SHAPE, "T * N too large");
+    pod_status st = pod_require_sm100();
+    if (st) return st;
+    auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    const int use_bulk = (N % 32 == 0) && al(rew) && al(val) && al(done) ? 1 : 0;
+    const int groups = (N + 31) / 32;
+    const unsigned blocks = static_cast<unsigned>((groups + GAE_WARPS - 1) / GAE_WARPS);
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(gae_smem_bytes()));
+    });
+    POD_CUDA(attr_err);
+    gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), static_cast<cudaStream_t>(stream)>>>(
+        rew, val, done, boot, T, N, gamma, lambda, adv, ret, use_bulk);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}

@@ -1,0 +1,265 @@
+"""GPU parity: libpod's CUDA path vs the float64 oracle on the same seeded
+inputs.  Every call goes through the C ABI (paper_2111_05188_b200.api).
+
+Bars: integer holdings, dones and the float64 cash ledger bit-exact; rewards
+equal the float32 rounding of the oracle's float64 reward; observations within
+bf16 rounding; GAE within 1e-5 x the magnitude recurrence; actor means within
+2e-2 (north_star); Gaussian noise, log-probs and the action map checked
+against the oracle's Philox/Box–Muller and map.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2111_05188_b200 import PodError, api, synth
+from parity_helpers import Case, assert_env_exact, assert_obs_close, bf16_to_f64, gae_check, mu_check
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    api.load()
+    torch.cuda.set_device(0)
+
+
+def _actor(case, n_hidden, hidden, seed=3, n_agents=1, act=0):
+    aws = [synth.make_actor(case.obs_dim, n_hidden, hidden, case.n, seed + a) for a in range(n_agents)]
+    params = api.pack_actor_params(case.cfg, aws, n_hidden, hidden)
+    return aws, params, api.make_actor(n_hidden, hidden, params, act)
+
+
+# ----------------------------------------------------------------- injected
+@pytest.mark.parametrize("kind", ["uniform", "all_buy", "all_sell", "sparse", "buy_then_sell"])
+@pytest.mark.parametrize("N,H", [(16, 64), (100, 13)])
+def test_injected_actions_exact(kind, N, H):
+    c = Case(n=30, f=3, T_data=400, N=N, H=H)
+    T = 40
+    u = synth.injected_u(kind, T, N, c.n, 5)
+    tr = api.Trajectory.allocate(T, N, c.n, c.k_pad, debug=True, sampled=False)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, injected_u=torch.from_numpy(u).cuda())
+    c.env.check()
+    o = c.oracle_env()
+    out = o.rollout(T, "inject", u=u, want=("obs", "rew", "done", "hold", "cash", "a_int"))
+    np.testing.assert_array_equal(tr.dbg_aint.cpu().numpy(), out["a_int"])
+    assert_env_exact(tr, out, c.obs_dim)
+    hold, cash, asset, ep = c.env.read_state()
+    np.testing.assert_array_equal(hold.cpu().numpy(), o.hold)
+    np.testing.assert_array_equal(cash.cpu().numpy(), o.cash)
+    np.testing.assert_array_equal(asset.cpu().numpy(), o.asset)
+    np.testing.assert_array_equal(ep.cpu().numpy(), o.ep_ret)
+
+
+def test_injected_end_of_data_and_continuation():
+    # tiles starting near the end of the data end their episodes at t+1 == T_data-1;
+    # state carries across two rollout calls
+    c = Case(n=5, f=2, T_data=120, N=64, H=50, C0=2e4, cost=0.001)
+    c.starts[:] = [69, 10]            # 69 + 50 = 119 = T_data - 1 -> ends by data exhaustion
+    u = synth.injected_u("uniform", 70, 64, 5, 9)
+    o = c.oracle_env()
+    out = o.rollout(70, "inject", u=u, want=("obs", "rew", "done", "hold", "cash"))
+    c.env.reset(c.starts)
+    for lo, hi in ((0, 33), (33, 70)):
+        T = hi - lo
+        tr = api.Trajectory.allocate(T, 64, 5, c.k_pad, debug=True, sampled=False)
+        c.env.rollout(T, tr, injected_u=torch.from_numpy(np.ascontiguousarray(u[lo:hi])).cuda())
+        sub = {k: out[k][lo:hi] for k in ("rew", "done", "hold", "cash")}
+        sub["obs"] = out["obs"][lo : hi + 1]
+        assert_env_exact(tr, sub, c.obs_dim)
+
+
+# ----------------------------------------------------------------- sampled
+@pytest.mark.parametrize("shape", ["dow30_2x128", "nasdaq100_3x512"])
+def test_sampled_rollout_parity(shape):
+    if shape == "dow30_2x128":
+        c = Case(n=30, f=3, T_data=500, N=160, H=24, seed=21, env_offset=1000)
+        nh, hid, T = 2, 128, 30
+    else:
+        c = Case(n=100, f=3, T_data=3000, N=256, H=400, seed=22, dt=1 / (252 * 390))
+        nh, hid, T = 3, 512, 6
+    aws, params, actor = _actor(c, nh, hid)
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, debug=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    c.env.check()
+    obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
+    mu_g = tr.mu.cpu().numpy().astype(np.float64)
+    raw_g = tr.act.cpu().numpy().astype(np.float64)
+    logp_g = tr.logp.cpu().numpy().astype(np.float64)
+    a_g = tr.dbg_aint.cpu().numpy()
+    w = oracle.actor_flat(aws[0].W, aws[0].b, aws[0].log_std)
+    ls = aws[0].log_std.astype(np.float64)
+    sig = np.exp(ls)
+    worst = 0.0
+    for t in range(T):
+        # actor mean: oracle float64 MLP on the GPU's own (bf16) observation
+        mu_o = oracle.actor_mu(w, obs_g[t], nh, hid, c.n)
+        worst = max(worst, mu_check(mu_g[t], mu_o))
+        for e in range(c.N):
+            z_o = oracle.normals(c.cfg.seed, c.cfg.env_offset + e, t, c.n)
+            z_g = (raw_g[t, e] - mu_g[t, e]) / sig
+            assert np.all(np.abs(z_g - z_o) <= 2e-5 * np.abs(z_o) + 5e-4), (t, e)
+            lp_o = float(np.sum(-0.5 * z_o * z_o - ls - 0.5 * math.log(2 * math.pi)))
+            terms = float(np.sum(0.5 * z_o * z_o + np.abs(ls) + 0.5 * math.log(2 * math.pi)))
+            assert abs(logp_g[t, e] - lp_o) <= 1e-5 * terms + 1e-4, (t, e)
+            # integer action = map(tanh(raw)) (R#6), except exactly at a rounding boundary
+            u = np.tanh(raw_g[t, e])
+            a_o = np.array([oracle.map_action(x, 100) for x in u])
+            off = a_g[t, e] != a_o
+            if off.any():
+                frac = np.abs(np.abs(u[off]) * 100 - np.floor(np.abs(u[off]) * 100) - 0.5)
+                assert (frac < 1e-4).all() and (np.abs(a_g[t, e][off] - a_o[off]) == 1).all()
+    # the environment driven by the GPU's executed actions: exact replay
+    o = c.oracle_env()
+    out = o.rollout(T, "replay", a_rep=a_g, want=("obs", "rew", "done", "hold", "cash"))
+    assert_env_exact(tr, out, c.obs_dim)
+    print(f"{shape}: worst mu row rel err {worst:.3e}")
+
+
+def test_deterministic_mode():
+    c = Case(n=30, f=3, T_data=300, N=64, H=40)
+    aws, params, actor = _actor(c, 2, 128)
+    tr = api.Trajectory.allocate(5, 64, 30, c.k_pad, debug=True)
+    c.env.reset(c.starts)
+    c.env.rollout(5, tr, actor=actor, deterministic=True)
+    np.testing.assert_array_equal(tr.act.cpu().numpy(), tr.mu.cpu().numpy())
+    lp = float(np.float32(np.sum(-aws[0].log_std.astype(np.float64) - 0.5 * math.log(2 * math.pi))))
+    np.testing.assert_allclose(tr.logp.cpu().numpy(), lp, rtol=1e-5)
+
+
+def test_multi_agent_grouping_and_ragged_tiles():
+    # 3 agents x 100 envs: tiles straddle agents (100 % 128 != 0) and env tiles are ragged
+    c = Case(n=30, f=3, T_data=400, N=300, H=30, n_agents=3, seed=5)
+    aws, params, actor = _actor(c, 2, 128, n_agents=3)
+    tr = api.Trajectory.allocate(3, 300, 30, c.k_pad, debug=True)
+    c.env.reset(c.starts)
+    c.env.rollout(3, tr, actor=actor)
+    obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
+    mu_g = tr.mu.cpu().numpy().astype(np.float64)
+    for a in range(3):
+        w = oracle.actor_flat(aws[a].W, aws[a].b, aws[a].log_std)
+        for t in range(3):
+            mu_o = oracle.actor_mu(w, obs_g[t, a * 100 : (a + 1) * 100], 2, 128, 30)
+            mu_check(mu_g[t, a * 100 : (a + 1) * 100], mu_o)
+
+
+def test_rerun_bit_identical_and_env_offset_invariance():
+    # reading R#14: noise keyed on global env ids -> the same global envs give
+    # bit-identical outputs whatever the split across processes/GPUs
+    full = Case(n=30, f=3, T_data=400, N=64, H=20, seed=9, env_offset=0)
+    aws, params, actor = _actor(full, 2, 128)
+    tr1 = api.Trajectory.allocate(8, 64, 30, full.k_pad, debug=True)
+    full.env.reset(full.starts)
+    full.env.rollout(8, tr1, actor=actor)
+    tr2 = api.Trajectory.allocate(8, 64, 30, full.k_pad, debug=True)
+    full.env.reset(full.starts)
+    full.env.rollout(8, tr2, actor=actor)
+    for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash"):
+        assert torch.equal(getattr(tr1, name), getattr(tr2, name)), name
+    half = Case(n=30, f=3, T_data=400, N=32, H=20, seed=9, env_offset=32)
+    half.starts = full.starts[1:2].copy()
+    tr3 = api.Trajectory.allocate(8, 32, 30, half.k_pad, debug=True)
+    half.env.reset(half.starts)
+    half.env.rollout(8, tr3, actor=actor)
+    for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash"):
+        assert torch.equal(getattr(tr1, name)[:, 32:], getattr(tr3, name)), name
+
+
+def test_fitness_after_deterministic_episode():
+    c = Case(n=30, f=3, T_data=400, N=128, H=16, n_agents=2, gamma=0.99)
+    aws, params, actor = _actor(c, 2, 128, n_agents=2)
+    tr = api.Trajectory.allocate(16, 128, 30, c.k_pad, debug=True)
+    fit = torch.empty(2, dtype=torch.float64, device="cuda")
+    c.env.reset(c.starts)
+    c.env.rollout(16, tr, actor=actor, deterministic=True, fitness_out=fit)
+    assert tr.done[-1].all() and not tr.done[:-1].any()
+    o = c.oracle_env()
+    o.rollout(16, "replay", a_rep=tr.dbg_aint.cpu().numpy(), want=("rew",))
+    _, _, _, ep = c.env.read_state()
+    np.testing.assert_array_equal(ep.cpu().numpy(), o.ep_ret)
+    np.testing.assert_allclose(fit.cpu().numpy(), oracle.fitness(o.ep_ret, 2), rtol=1e-12)
+
+
+# ----------------------------------------------------------------- GAE
+@pytest.mark.parametrize("T,N", [(1, 32), (3, 1), (77, 100), (64, 4096), (256, 8192), (1000, 96)])
+def test_gae_parity(T, N):
+    r, v, d, boot = synth.gae_inputs(T, N, seed=T * 7 + N)
+    adv_o, ret_o, mag = oracle.gae(r, v, d, boot, 0.99, 0.95)
+    adv, ret = api.pod_gae(*(torch.from_numpy(x).cuda() for x in (r, v, d, boot)), 0.99, 0.95)
+    gae_check(adv, ret, adv_o, ret_o, mag)
+
+
+def test_gae_worked_example_on_gpu():
+    r = torch.tensor([[1.0], [0.0], [2.0]]).cuda()
+    v = torch.tensor([[0.5], [0.2], [0.1]]).cuda()
+    d = torch.zeros((3, 1), dtype=torch.uint8).cuda()
+    adv, ret = api.pod_gae(r, v, d, torch.zeros(1).cuda(), 0.99, 0.95)
+    np.testing.assert_allclose(adv[:, 0].cpu().numpy(), [2.283635975, 1.68595, 1.9], rtol=2e-7)
+    np.testing.assert_allclose(ret[:, 0].cpu().numpy(), [2.783635975, 1.88595, 2.0], rtol=2e-7)
+
+
+# ----------------------------------------------------------------- selection
+def test_select_elite_single_rank():
+    comm = api.Comm(1, 0, 8)
+    fit = torch.tensor([1.2, 3.4, 2.0, -1.0, 3.4, 0.0], dtype=torch.float64, device="cuda")
+    params = torch.arange(6, dtype=torch.uint8, device="cuda")[:, None].repeat(1, 4096).contiguous()
+    plan = comm.select_elite(fit, 2, params)
+    ref = oracle.select_elite(fit.cpu().numpy(), 2)
+    np.testing.assert_array_equal(plan, ref)
+    torch.cuda.synchronize()
+    got = params[:, 0].cpu().numpy()
+    np.testing.assert_array_equal(got, ref)   # each slot now holds its source agent's slab
+    assert (params == params[:, :1]).all()
+    comm.destroy()
+
+
+# ----------------------------------------------------------------- errors
+def test_error_paths():
+    c = Case(n=30, f=3, T_data=200, N=32, H=50)
+    with pytest.raises(PodError) as ei:
+        c.env.reset(np.array([150]))          # 150 + 50 > 199
+    assert ei.value.name == "POD_ERR_RANGE"
+    bad = api.make_config(32, 30, 3, 50, cost_rate=1.5)
+    with pytest.raises(PodError) as ei:
+        api.Env(bad, c.close_d, c.feat_d)
+    assert ei.value.name == "POD_ERR_ARG"
+    tr = api.Trajectory.allocate(2, 32, 30, c.k_pad, sampled=False)
+    with pytest.raises(PodError) as ei:
+        c.env.rollout(2, tr)                    # neither actor nor injected actions
+    assert ei.value.name == "POD_ERR_ARG"
+
+
+# ----------------------------------------------------------------- full size (bench launch config)
+def test_full_size_c3_sampled_rows():
+    """C3 launch configuration (8192 envs, n=100, 3x512, one agent) on sampled rows."""
+    c = Case(n=100, f=3, T_data=60_000, N=8192, H=2000, seed=5191, dt=1 / (252 * 390))
+    aws, params, actor = _actor(c, 3, 512)
+    T = 4
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, debug=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    c.env.check()
+    rows = np.unique(np.concatenate([np.arange(0, 8192, 257), [8191, 127, 128]]))
+    obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
+    mu_g = tr.mu.cpu().numpy().astype(np.float64)
+    w = oracle.actor_flat(aws[0].W, aws[0].b, aws[0].log_std)
+    for t in range(T):
+        mu_check(mu_g[t, rows], oracle.actor_mu(w, obs_g[t, rows], 3, 512, 100))
+    # env replay on the sampled envs (envs are independent: batch equivalence)
+    a_g = tr.dbg_aint.cpu().numpy()
+    starts = c.env_starts()[rows]
+    o = oracle.Env(c.market.close, c.market.feat, len(rows), **c.kw)
+    o.reset(starts)
+    out = o.rollout(T, "replay", a_rep=np.ascontiguousarray(a_g[:, rows]), want=("obs", "rew", "done", "hold", "cash"))
+    np.testing.assert_array_equal(tr.dbg_hold.cpu().numpy()[:, rows], out["hold"])
+    np.testing.assert_array_equal(tr.dbg_cash.cpu().numpy()[:, rows], out["cash"])
+    np.testing.assert_array_equal(tr.rew.cpu().numpy()[:, rows], out["rew"].astype(np.float32))
+    assert_obs_close(tr.obs[:, rows], out["obs"], c.obs_dim)
+    # properties over all rows
+    assert (tr.dbg_cash >= 0).all() and (tr.dbg_hold >= 0).all()
