@@ -200,6 +200,22 @@ pod_status pod_rollout(pod_env_t* env, const pod_actor* actor, int32_t T, const 
                        const float* injected_u, int32_t deterministic, double* fitness_out,
                        void* stream);
 
+/* Per-kernel device timing (measurement support, not part of the method).
+ * stride k > 0: subsequent pod_rollout calls record CUDA events on their
+ * stream around the actor launch and the env-step launch of every k-th step
+ * (inside the captured graph); 0 turns it off.  pod_env_profile_read
+ * synchronises `stream` and returns the summed device milliseconds and the
+ * number of bracketed launches of the most recent profiled rollout (zeros if
+ * none since the last read), then forgets it. */
+pod_status pod_env_profile(pod_env_t* env, int32_t stride);
+pod_status pod_env_profile_read(pod_env_t* env, double* actor_ms, int64_t* actor_launches, double* env_ms,
+                                int64_t* env_launches, void* stream);
+
+/* Diagnostics only: buf [dev] u64 [2 x tiles][32] receives clock64 stamps of the
+ * actor kernel's phases (obs loaded, per-layer MMA issue / epilogue, head) at every
+ * actor launch of subsequent rollouts; NULL turns it off.  Drops cached graphs. */
+pod_status pod_debug_actor_trace(pod_env_t* env, unsigned long long* buf);
+
 /* Fitness J of the current state (same definition as pod_rollout's). */
 pod_status pod_env_fitness(pod_env_t* env, double* fitness_out, void* stream);
 

@@ -161,6 +161,17 @@ class Env:
                                  _ptr(injected_u), 1 if deterministic else 0, _ptr(fitness_out), _stream(stream)),
               "pod_rollout")
 
+    def profile(self, stride: int):
+        """Bracket the actor and env-step launches of every `stride`-th step with CUDA events (0 = off)."""
+        check(load().pod_env_profile(self.h, int(stride)), "pod_env_profile")
+
+    def profile_read(self, stream=None):
+        am, em = C.c_double(0), C.c_double(0)
+        al, el = C.c_int64(0), C.c_int64(0)
+        check(load().pod_env_profile_read(self.h, C.byref(am), C.byref(al), C.byref(em), C.byref(el),
+                                          _stream(stream)), "pod_env_profile_read")
+        return am.value, al.value, em.value, el.value
+
     def fitness(self, out: torch.Tensor, stream=None):
         check(load().pod_env_fitness(self.h, _ptr(out), _stream(stream)), "pod_env_fitness")
 

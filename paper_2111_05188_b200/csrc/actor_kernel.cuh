@@ -8,17 +8,29 @@
 //   raw = mu + exp(log_std) z,  logp = sum_i(-z_i^2/2 - log_std_i - ln(2 pi)/2),
 //   u = tanh(raw),  a_i = sgn(u_i) floor(|u_i| h_max + 1/2).
 //
-// B200 design (one CTA per 128-row tile of envs, all layers fused on chip):
+// B200 design.  A CLUSTER OF 2 CTAs owns one 128-env M-tile and splits every
+// layer's output columns between its two CTAs (CTA r computes columns
+// [r N/2, (r+1) N/2)), so twice as many SMs work on the chain and each SM
+// streams only half of every weight matrix from L2.  Per CTA:
 //   * warp 0 (one lane): TMA producer — the obs tile [128 x k_pad] bf16 into the
-//     activation buffer, then every weight tile W_l[BN x 64] through a
-//     STAGES-deep ring (128B-swizzled, 3-D tensor map over [agent][out][in]);
-//   * warp 1 (one lane): tcgen05.mma issuer, M=128, N=BN<=256, K=16 steps,
-//     A = activations in smem, B = weight ring, D = fp32 accumulator in TMEM;
-//   * warps 2..5: epilogue — tcgen05.ld of their 32-lane TMEM quadrant, bias +
-//     activation, bf16 pack, swizzled st.shared back into the activation buffer
-//     (it becomes the A operand of the next layer: activations never leave the
-//     SM), and for the head the sampling epilogue writing act/logp/mu and the
-//     integer action a_t (ticker-major scratch for the env-step kernel).
+//     activation buffer (128B-swizzled K-major atoms), then this CTA's half of
+//     every weight matrix W_l[BN x 64] through a STAGES-deep ring;
+//   * warp 1 (one lane): tcgen05.mma issuer (M=128, N=BN, K=16 steps), A =
+//     activations in smem, B = weight ring, D = fp32 accumulator in TMEM;
+//     each layer's completion is committed to the accumulator barrier of BOTH
+//     CTAs (multicast commit), so each side knows when the pair is done reading
+//     the current activations;
+//   * warps 2..9: epilogue, 2 warps per 32-lane TMEM quadrant, each half of
+//     the columns — tcgen05.ld, bias + activation (biases staged in smem), bf16
+//     pack, swizzled st.shared into the local activation buffer, then ONE
+//     bulk copy (TMA engine, DSMEM) of this CTA's new activation atoms into the
+//     peer's buffer, completing on the peer's activation-ready barrier.  The
+//     activations never leave the cluster.
+//   * the next layer's MMAs start on the CTA's own half of K while the peer's
+//     half is still in flight (per-rank K order: own half first);
+//   * head: each CTA samples its half of the tickers with noise z that the
+//     previous env-step launch generated in its otherwise idle warps; the per-row
+//     log-prob partials are combined in CTA 0 through DSMEM after a cluster barrier.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -30,16 +42,19 @@
 
 namespace pod {
 
-constexpr int ACT_THREADS = 192;       // 6 warps
-constexpr int ACT_STAGES = 3;          // weight ring depth
+constexpr int ACT_THREADS = 320;       // 10 warps
+constexpr int ACT_STAGES = 5;          // weight ring depth
+constexpr int ACT_BN = 128;            // weight rows per ring stage (max)
 constexpr int ACT_MAX_LAYERS = 5;      // n_hidden <= 4
+constexpr int ACT_BIAS_FLOATS = 1792;  // per-CTA staged biases + log-std + sigma
+constexpr int ACT_MAX_HQ = 32;         // head tickers per epilogue thread (n_out_pad <= 128)
 
 struct ActorArgs {
     int32_t N;               // envs
     int32_t per_agent;       // envs per agent
     int32_t tiles_per_agent; // ceil(per_agent / 128)
     int32_t n;               // stocks
-    int32_t n_out_pad;       // head rows (n rounded to 16)
+    int32_t n_out_pad;       // head rows (n rounded to 32)
     int32_t k_pad;           // obs row width
     int32_t hidden;
     int32_t n_layers;        // n_hidden + 1
@@ -48,7 +63,7 @@ struct ActorArgs {
     int32_t deterministic;
     int32_t t;               // step within the rollout
     int32_t obs_row0;        // row of obs[t][0] in the obs tensor map = t * N
-    int32_t bn_max;          // ring stage rows
+    int32_t pad_;
     uint64_t seed;
     int64_t env_offset;
     const uint64_t* step_base;   // device step counter of the handle
@@ -61,7 +76,9 @@ struct ActorArgs {
     float* mu_out;       // [N][n] or null
     int16_t* aint;       // [n][N] scratch
     int16_t* dbg_aint;   // [N][n] or null
+    const float* znoise; // [n][N] N(0,1) noise for this step (written by the previous env-step launch)
     uint32_t* err;
+    unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
 };
 
 struct ActorMaps {
@@ -69,39 +86,59 @@ struct ActorMaps {
     CUtensorMap w[ACT_MAX_LAYERS];       // 3-D bf16 [agents][out][in], box {64, BN_l, 1}
 };
 
+// column split of layer l: this CTA's half (rows of W_l) and the ring tile height
+__host__ __device__ inline int actor_layer_out(int l, int n_layers, int hidden, int n_out_pad) {
+    return l == n_layers - 1 ? n_out_pad : hidden;
+}
+__host__ __device__ inline int actor_bn(int half) { return half < ACT_BN ? half : ACT_BN; }
+
+inline size_t actor_smem_bytes(int k_pad, int hidden) {
+    const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
+    return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_BN * 128 +
+           ACT_BIAS_FLOATS * 4 + 4 * 128 * 4 + 256;
+}
+
 __device__ __forceinline__ float act_fn(float x, int act) { return act == 0 ? fmaxf(x, 0.0f) : tanhf(x); }
 
 __global__ void __launch_bounds__(ACT_THREADS, 1)
     actor_forward_kernel(const __grid_constant__ ActorMaps maps, const ActorArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-B alignment for the swizzle atoms
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();            // 0 / 1 within the pair
+    const uint32_t peer = rank ^ 1u;
     const int ka = (a.k_pad > a.hidden ? a.k_pad : a.hidden) / 64;   // activation atoms
     const uint32_t act_s = base_u32;                                  // ka * 16 KB
     const uint32_t ring_s = act_s + ka * 16384u;
-    const uint32_t stage_bytes = static_cast<uint32_t>(a.bn_max) * 128u;
-    const uint32_t bar_s = ring_s + ACT_STAGES * stage_bytes;        // 8-byte barriers
+    const uint32_t stage_bytes = ACT_BN * 128u;
+    const uint32_t bias_off = ka * 16384u + ACT_STAGES * stage_bytes;
+    float* bias_s = reinterpret_cast<float*>(base + bias_off);                 // [ACT_BIAS_FLOATS]
+    float* logp_s = bias_s + ACT_BIAS_FLOATS;                                  // [4][128] (CTA 0)
+    const uint32_t bar_s = base_u32 + bias_off + ACT_BIAS_FLOATS * 4 + 4 * 128 * 4;
     const uint32_t full_b = bar_s;                                   // [STAGES]
     const uint32_t empty_b = bar_s + 8u * ACT_STAGES;                // [STAGES]
     const uint32_t obs_b = bar_s + 16u * ACT_STAGES;
     const uint32_t accum_b = obs_b + 8u;
-    const uint32_t actrdy_b = obs_b + 16u;
-    const uint32_t tslot_s = obs_b + 24u;
+    const uint32_t ownrdy_b = obs_b + 16u;     // this CTA's half of h_{l+1} written (256 arrivals)
+    const uint32_t peerrdy_b = obs_b + 24u;    // the peer's half of h_{l+1} landed (expect_tx)
+    const uint32_t tslot_s = obs_b + 32u;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
-    const int agent = blockIdx.x / a.tiles_per_agent;
-    const int tile_in_agent = blockIdx.x % a.tiles_per_agent;
+    const int mtile = blockIdx.x >> 1;
+    const int agent = mtile / a.tiles_per_agent;
+    const int tile_in_agent = mtile % a.tiles_per_agent;
     const int env0 = agent * a.per_agent + tile_in_agent * 128;
     int rows_valid = a.per_agent - tile_in_agent * 128;
     rows_valid = rows_valid > 128 ? 128 : rows_valid;
 
+    const int hid_half = a.hidden / 2;
+    const int head_half = a.n_out_pad / 2;
     uint32_t tcols = 32;
     {
-        const int need = a.hidden > a.n_out_pad ? a.hidden : a.n_out_pad;
+        const int need = hid_half > head_half ? hid_half : head_half;
         while (tcols < static_cast<uint32_t>(need)) tcols <<= 1;
     }
 
@@ -112,8 +149,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 mbar_init(empty_b + 8u * s, 1);
             }
             mbar_init(obs_b, 1);
-            mbar_init(accum_b, 1);
-            mbar_init(actrdy_b, 128);
+            mbar_init(accum_b, 2);        // one multicast commit from each CTA of the pair
+            mbar_init(ownrdy_b, 256);     // the 256 epilogue threads
+            mbar_init(peerrdy_b, 1);      // one expect_tx arrival + the peer's bulk-copy bytes
             fence_mbar_init();
             prefetch_tmap(&maps.obs);
             for (int l = 0; l < a.n_layers; ++l) prefetch_tmap(&maps.w[l]);
@@ -122,9 +160,11 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         tmem_alloc(tslot_s, tcols);
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();          // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 32 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = clock64();
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -137,15 +177,17 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             uint32_t phase = 0;
             for (int l = 0; l < a.n_layers; ++l) {
                 const int K = l == 0 ? a.k_pad : a.hidden;
-                const int Nl = l == a.n_layers - 1 ? a.n_out_pad : a.hidden;
-                const int bn = Nl > 256 ? 256 : Nl;
-                const int nchunks = Nl / bn;
-                for (int c = 0; c < nchunks; ++c) {
-                    for (int kb = 0; kb < K / 64; ++kb) {
+                const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
+                const int bn = actor_bn(half);
+                const int KB = K / 64;
+                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);   // own half of h_l first
+                for (int c = 0; c < half / bn; ++c) {
+                    for (int j = 0; j < KB; ++j) {
+                        const int kb = (j + kb0) % KB;
                         mbar_wait(empty_b + 8u * stage, phase ^ 1u);
                         mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * 128u);
-                        tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * 64, c * bn, agent,
-                                    full_b + 8u * stage);
+                        tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * 64,
+                                    static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage);
                         if (++stage == ACT_STAGES) {
                             stage = 0;
                             phase ^= 1u;
@@ -160,27 +202,37 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         if (lane == 0) {
             mbar_wait(obs_b, 0);
             tc_fence_after();
+            if (tr) tr[1] = clock64();
             int stage = 0;
             uint32_t phase = 0;
             for (int l = 0; l < a.n_layers; ++l) {
-                if (l > 0) {
-                    mbar_wait(actrdy_b, static_cast<uint32_t>(l - 1) & 1u);
+                if (l > 0) {   // own half of h_l is local: start on it, the peer's half may still be in flight
+                    mbar_wait(ownrdy_b, static_cast<uint32_t>(l - 1) & 1u);
                     tc_fence_after();
                 }
+                if (tr) tr[2 + 4 * l] = clock64();
                 const int K = l == 0 ? a.k_pad : a.hidden;
-                const int Nl = l == a.n_layers - 1 ? a.n_out_pad : a.hidden;
-                const int bn = Nl > 256 ? 256 : Nl;
-                const int nchunks = Nl / bn;
-                const uint32_t idesc = idesc_bf16_f32(128, bn);
-                for (int c = 0; c < nchunks; ++c) {
-                    for (int kb = 0; kb < K / 64; ++kb) {
+                const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
+                const int bn = actor_bn(half);
+                const uint32_t idesc = idesc_bf16_f32(128, static_cast<uint32_t>(bn));
+                const int KB = K / 64;
+                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);
+                bool peer_seen = l == 0;
+                for (int c = 0; c < half / bn; ++c) {
+                    for (int j = 0; j < KB; ++j) {
+                        const int kb = (j + kb0) % KB;
+                        if (!peer_seen && j == KB / 2) {
+                            mbar_wait(peerrdy_b, static_cast<uint32_t>(l - 1) & 1u);
+                            tc_fence_after();
+                            peer_seen = true;
+                        }
                         mbar_wait(full_b + 8u * stage, phase);
                         tc_fence_after();
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const uint64_t ad = sw128_desc(act_s + kb * 16384u + k * 32u);
                             const uint64_t bd = sw128_desc(ring_s + stage * stage_bytes + k * 32u);
-                            mma_bf16(tmem + static_cast<uint32_t>(c * bn), ad, bd, idesc, (kb | k) != 0);
+                            mma_bf16(tmem + static_cast<uint32_t>(c * bn), ad, bd, idesc, (j | k) != 0);
                         }
                         mma_commit(empty_b + 8u * stage);
                         if (++stage == ACT_STAGES) {
@@ -189,79 +241,132 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         }
                     }
                 }
-                mma_commit(accum_b);
+                if (tr) tr[3 + 4 * l] = clock64();
+                mma_commit_mc(accum_b, 0x3);
             }
         }
         __syncwarp();
     } else {
-        // ===================== epilogue (warps 2..5) =====================
+        // ===================== epilogue (warps 2..9) =====================
+        const int ew = warp - 2;                   // 0..7
+        const int etid = ew * 32 + lane;           // 0..255
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+        const int hh = ew >> 2;                    // which half of this CTA's columns
         const int r = quad * 32 + lane;            // row of the tile == TMEM lane
         const uint32_t trow = tmem + (static_cast<uint32_t>(quad * 32) << 16);
         const int e = env0 + r;
         const bool valid = r < rows_valid && e < a.N;
-        for (int l = 0; l < a.n_layers - 1; ++l) {
-            mbar_wait(accum_b, static_cast<uint32_t>(l) & 1u);
-            tc_fence_after();
-            const float* bias = reinterpret_cast<const float*>(a.params + agent * a.param_bytes + a.b_off[l]);
-            for (int cc = 0; cc < a.hidden / 32; ++cc) {
-                uint32_t v[32];
-                tmem_ld32(trow + static_cast<uint32_t>(cc * 32), v);
-                tmem_ld_wait();
-                uint32_t pk[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const float x0 = act_fn(__uint_as_float(v[2 * j]) + __ldg(bias + cc * 32 + 2 * j), a.act);
-                    const float x1 = act_fn(__uint_as_float(v[2 * j + 1]) + __ldg(bias + cc * 32 + 2 * j + 1), a.act);
-                    pk[j] = pack_bf16x2(x0, x1);
-                }
-                const uint32_t atom = act_s + static_cast<uint32_t>((cc * 32) / 64) * 16384u;
-                const uint32_t c0 = static_cast<uint32_t>(((cc * 32) % 64) / 8);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    st_shared_v4(atom + sw128_offset(static_cast<uint32_t>(r), c0 + q), pk[4 * q], pk[4 * q + 1],
-                                 pk[4 * q + 2], pk[4 * q + 3]);
+        const char* slab = a.params + agent * a.param_bytes;
+        // stage this CTA's halves of the biases and log-std in smem
+        {
+            int off = 0;
+            for (int l = 0; l < a.n_layers; ++l) {
+                const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
+                const float* b = reinterpret_cast<const float*>(slab + a.b_off[l]) + rank * half;
+                for (int j = etid; j < half; j += 256) bias_s[off + j] = b[j];
+                off += half;
             }
+            const float* ls = reinterpret_cast<const float*>(slab + a.log_std_off) + rank * head_half;
+            for (int j = etid; j < head_half; j += 256) {
+                bias_s[off + j] = ls[j];
+                bias_s[off + head_half + j] = expf(ls[j]);   // sigma
+            }
+        }
+        // prefetch this thread's head noise z (written by the previous env-step launch):
+        // one round of independent loads, long before the head needs them
+        const int hq = head_half / 2;                                    // tickers of this thread
+        float zr[ACT_MAX_HQ];
+#pragma unroll
+        for (int q = 0; q < ACT_MAX_HQ; ++q) {
+            const int i = static_cast<int>(rank) * head_half + hh * hq + q;
+            zr[q] = (q < hq && valid && i < a.n && !a.deterministic) ? a.znoise[static_cast<int64_t>(i) * a.N + e] : 0.0f;
+        }
+        named_bar_sync(1, 256);
+        int boff = 0;
+        for (int l = 0; l < a.n_layers - 1; ++l) {
+            mbar_wait(accum_b, static_cast<uint32_t>(l) & 1u);   // both CTAs done reading h_l
+            tc_fence_after();
+            if (tr && etid == 0) tr[4 + 4 * l] = clock64();
+            const int quarter = hid_half / 2;                     // columns of this warp
+            for (int cc = 0; cc < quarter / 32; cc += 2) {
+                const int npair = quarter / 32 - cc >= 2 ? 2 : 1;
+                uint32_t v[2][32];
+                tmem_ld32(trow + static_cast<uint32_t>(hh * quarter + cc * 32), v[0]);
+                if (npair == 2) tmem_ld32(trow + static_cast<uint32_t>(hh * quarter + cc * 32 + 32), v[1]);
+                tmem_ld_wait();
+#pragma unroll
+                for (int pp = 0; pp < 2; ++pp) {
+                    if (pp < npair) {
+                        const int tc = hh * quarter + (cc + pp) * 32;    // TMEM column (local)
+                        const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 b = b4[j];
+                            pk[2 * j] = pack_bf16x2(act_fn(__uint_as_float(v[pp][4 * j]) + b.x, a.act),
+                                                    act_fn(__uint_as_float(v[pp][4 * j + 1]) + b.y, a.act));
+                            pk[2 * j + 1] = pack_bf16x2(act_fn(__uint_as_float(v[pp][4 * j + 2]) + b.z, a.act),
+                                                        act_fn(__uint_as_float(v[pp][4 * j + 3]) + b.w, a.act));
+                        }
+                        const int col = static_cast<int>(rank) * hid_half + tc;   // global column of h_{l+1}
+                        const uint32_t atom = act_s + static_cast<uint32_t>(col / 64) * 16384u;
+                        const uint32_t c0 = static_cast<uint32_t>((col % 64) / 8);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            st_shared_v4(atom + sw128_offset(static_cast<uint32_t>(r), c0 + q), pk[4 * q],
+                                         pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    }
+                }
+            }
+            boff += hid_half;
             fence_proxy_async_smem();
             tc_fence_before();
-            mbar_arrive(actrdy_b);
+            named_bar_sync(1, 256);
+            const uint32_t bytes = static_cast<uint32_t>(hid_half / 64) * 16384u;
+            if (tr && etid == 0) tr[5 + 4 * l] = clock64();
+            if (etid == 0) {
+                // this CTA's new atoms -> the same offsets in the peer, completing on its barrier
+                const uint32_t src = act_s + rank * bytes;
+                bulk_s2peer(mapa_shared(src, peer), src, bytes, mapa_shared(peerrdy_b, peer));
+                mbar_arrive_expect_tx(peerrdy_b, bytes);       // the peer's half arriving here
+            }
+            mbar_arrive(ownrdy_b);
         }
-        // ----- head: mean, Gaussian sample, log-prob, squash, integer action
+        // ----- head: this CTA's tickers [rank*head_half, ...), this warp's quarter of them
         const int L = a.n_layers - 1;
         mbar_wait(accum_b, static_cast<uint32_t>(L) & 1u);
         tc_fence_after();
-        const char* slab = a.params + agent * a.param_bytes;
-        const float* bias = reinterpret_cast<const float*>(slab + a.b_off[L]);
-        const float* log_std = reinterpret_cast<const float*>(slab + a.log_std_off);
-        const uint64_t step = *a.step_base + static_cast<uint64_t>(a.t);
-        const uint32_t eg = static_cast<uint32_t>(a.env_offset + e);
+        if (tr && etid == 0) tr[24] = clock64();
+        const float* bias = bias_s + boff;
+        const float* log_std = bias_s + boff + head_half;
+        const float* sigma = bias_s + boff + 2 * head_half;
         float logp = 0.0f;
         bool bad = false;
         const float half_ln_2pi = 0.918938533204672742f;
-        for (int cc = 0; cc * 32 < a.n; ++cc) {
-            uint32_t v[32];
+        const bool vec = (a.n % 4) == 0;
+#pragma unroll
+        for (int cc = 0; cc < ACT_MAX_HQ / 8; ++cc) {
+            if (cc >= hq / 8) break;
+            const int tc = hh * hq + cc * 8;                         // TMEM column (local)
+            const int i0 = static_cast<int>(rank) * head_half + tc;  // global ticker
+            uint32_t v[8];
             __syncwarp();
-            tmem_ld32(trow + static_cast<uint32_t>(cc * 32), v);   // warp-collective
+            tmem_ld8(trow + static_cast<uint32_t>(tc), v);
             tmem_ld_wait();
-            if (valid) {
-            float raw[32];
+            if (valid && i0 < a.n) {
+                float raw[8], mu[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                const int i0 = cc * 32 + q * 4;
-                if (!a.deterministic && i0 < a.n) z = normals4(a.seed, eg, step, static_cast<uint32_t>(i0 / 4));
-                const float zz[4] = {z.x, z.y, z.z, z.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int i = i0 + j;
-                    const int jj = q * 4 + j;
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int i = i0 + jj;
+                    mu[jj] = __uint_as_float(v[jj]) + bias[tc + jj];
+                    raw[jj] = mu[jj];
                     if (i < a.n) {
-                        const float mu = __uint_as_float(v[jj]) + __ldg(bias + i);
-                        const float ls = __ldg(log_std + i);
-                        bad |= !isfinite(mu);
-                        raw[jj] = fmaf(expf(ls), zz[j], mu);
-                        logp += (-0.5f * zz[j] * zz[j] - ls) - half_ln_2pi;
-                        v[jj] = __float_as_uint(mu);
+                        // noise z ~ N(0,1) for (env, step, ticker), generated by the previous env-step launch
+                        const float z = zr[cc * 8 + jj];
+                        const float ls = log_std[tc + jj];
+                        bad |= !isfinite(mu[jj]);
+                        raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
+                        logp += (-0.5f * z * z - ls) - half_ln_2pi;
                         const float u = tanhf(raw[jj]);
                         const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
                         const int ai = u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m);
@@ -269,30 +374,47 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         if (a.dbg_aint) a.dbg_aint[static_cast<int64_t>(e) * a.n + i] = static_cast<int16_t>(ai);
                     }
                 }
-            }
-            float* arow = a.act_out + static_cast<int64_t>(e) * a.n + cc * 32;
-            float* mrow = a.mu_out ? a.mu_out + static_cast<int64_t>(e) * a.n + cc * 32 : nullptr;
+                float* arow = a.act_out + static_cast<int64_t>(e) * a.n + i0;
+                float* mrow = a.mu_out ? a.mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;
+                if (vec && i0 + 8 <= a.n) {
+                    reinterpret_cast<float4*>(arow)[0] = make_float4(raw[0], raw[1], raw[2], raw[3]);
+                    reinterpret_cast<float4*>(arow)[1] = make_float4(raw[4], raw[5], raw[6], raw[7]);
+                    if (mrow) {
+                        reinterpret_cast<float4*>(mrow)[0] = make_float4(mu[0], mu[1], mu[2], mu[3]);
+                        reinterpret_cast<float4*>(mrow)[1] = make_float4(mu[4], mu[5], mu[6], mu[7]);
+                    }
+                } else {
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-                if (cc * 32 + jj < a.n) {
-                    arow[jj] = raw[jj];
-                    if (mrow) mrow[jj] = __uint_as_float(v[jj]);
+                    for (int jj = 0; jj < 8; ++jj) {
+                        if (i0 + jj < a.n) {
+                            arow[jj] = raw[jj];
+                            if (mrow) mrow[jj] = mu[jj];
+                        }
+                    }
                 }
             }
-            }
         }
-        if (valid) {
-            a.logp_out[e] = logp;
-            if (bad) atomicOr(a.err, 1u);
-        }
+        if (bad && valid) atomicOr(a.err, 1u);
+        if (tr && etid == 0) tr[25] = clock64();
+        // log-prob partial of (rank, hh) for row r -> CTA 0's logp_s[rank*2 + hh][r]
+        st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), 0), logp);
     }
 
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();      // logp partials visible in CTA 0; all peer DSMEM traffic finished
+    if (warp >= 2 && rank == 0) {
+        const int ew = warp - 2;
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int e = env0 + r;
+        if ((ew >> 2) == 0 && r < rows_valid && e < a.N)
+            a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
+    }
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, tcols);
     }
+    if (tr && threadIdx.x == 0) tr[26] = clock64();
 }
 
 }  // namespace pod

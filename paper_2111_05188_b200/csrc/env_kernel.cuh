@@ -11,29 +11,33 @@
 //   on done: ep_ret = disc and auto-reset (b = C0, h = 0, k = 0, t = s);
 //   s_{t+1} = [b/C0, h_i p_i/C0, p_i/p0_i, feat[t][c][i], 0-pad]  (bf16).
 //
-// B200 mapping: one warp per env tile (32 envs that share an episode start
-// row, hence the same market rows); lane = env.  The ledger is float64 and
-// evaluated per lane in exactly the order written above (explicit __dmul_rn /
-// __dadd_rn / __ddiv_rn, no FMA contraction), so cash, account value, reward
-// and the integer holdings are bit-identical to a sequential float64
-// implementation — a warp-parallel prefix over tickers would reassociate the
-// cash sums and could flip a floor() at a near tie.  State is ticker-major
-// (hold[i][env], a[i][env]) so every per-ticker access of the warp is one
-// coalesced 128-B (64-B for int16) transaction.  The tile's market rows
-// (p_t, p_{t+1}, p_0, feat_{t+1}) are staged once per warp in shared memory;
-// the per-tile part of s_{t+1} (price ratios, indicators, zero pad) is built
-// once per warp and each env row of s_{t+1} is then written by the whole warp
-// with coalesced 16-byte stores (512 contiguous bytes per instruction).
+// B200 mapping: one 128-thread block per env tile (32 envs that share an
+// episode start row, hence the same market rows).  The tile's holdings and
+// actions ([n][32], ticker-major in HBM) arrive as two 2-D TMA boxes, the
+// market rows with one round of independent loads; warp 0 (lane = env) then
+// runs ONLY the sequential float64 ledger, in exactly the order written
+// above (explicit __dmul_rn / __dadd_rn / __ddiv_rn, no FMA contraction), so
+// cash, account value, reward and the integer holdings are bit-identical to a
+// sequential float64 implementation — a parallel prefix over tickers would
+// reassociate the cash sums and could flip a floor() at a near tie.  All four
+// warps then write the new holdings (coalesced 128-B rows), build the per-env
+// part of s_{t+1} and store the 32 observation rows with 16-B vector stores
+// (512 contiguous bytes per warp instruction).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <cstdint>
 
+#include "philox.cuh"
+#include "ptx.cuh"
+
 namespace pod {
 
-constexpr int ENV_WARPS = 4;          // tiles per block
 constexpr int ENV_MAX_STOCKS = 128;
 constexpr int ENV_MAX_KPAD = 512;
+constexpr int ENV_THREADS = 128;      // 4 warps per env tile
+constexpr int ENV_MAX_MARKET = 3 * ENV_MAX_STOCKS + ENV_MAX_KPAD;   // p_t, p_1, p_0, indicators
 
 struct EnvArgs {
     int32_t N;
@@ -44,6 +48,14 @@ struct EnvArgs {
     int32_t horizon;
     int32_t n_tiles;
     int32_t mode;             // 0 = step, 1 = write obs of the current state, 2 = reset + obs
+    int32_t tma_ok;           // hold / aint tiles may be fetched with the 2-D tensor maps
+    int32_t gen_noise;        // also draw the actor's N(0,1) noise for step *step_base + noise_t
+    int32_t noise_t;
+    int32_t pad_;
+    uint64_t seed;
+    int64_t env_offset;
+    const uint64_t* step_base;
+    float* znoise;            // [n][N] noise output
     int64_t T_data;
     double C0;
     double cost;
@@ -68,159 +80,266 @@ struct EnvArgs {
     uint32_t* err;
 };
 
-struct EnvSmem {
-    float p_t[ENV_MAX_STOCKS];
-    float p_1[ENV_MAX_STOCKS];
-    float p_0[ENV_MAX_STOCKS];
-    __align__(16) uint16_t tmpl[ENV_MAX_KPAD];                 // per-tile part of the obs row
-    __align__(16) uint16_t stg[32][((1 + ENV_MAX_STOCKS) + 7) / 8 * 8];  // per-env part
+struct EnvMaps {
+    CUtensorMap hold;   // 2-D int32 [n][N], box {32, n}
+    CUtensorMap aint;   // 2-D uint16 [n][N], box {32, n}
 };
+
+// shared memory of one block (one tile), TMA destinations 128-B aligned:
+//   [hold_s n*32 i32 | aint_s n*32 i16 (pad 128) | unit, p_t, p_1 n f64 each (pad 16) |
+//    p_t, p_1, p_0 n f32 (pad 16) | tmpl k_pad bf16 | stg 32 x e_pad bf16 | mbar]
+__host__ __device__ inline int env_e_pad(int n) { return (1 + n + 7) / 8 * 8; }
+struct EnvSmemLayout {
+    int aint, unit, p, tmpl, stg, bar, total;
+};
+__host__ __device__ inline EnvSmemLayout env_smem_layout(int n, int k_pad) {
+    EnvSmemLayout L;
+    L.aint = n * 128;
+    L.unit = L.aint + (n * 64 + 127) / 128 * 128;
+    L.p = L.unit + (3 * n * 8 + 15) / 16 * 16;
+    L.tmpl = L.p + (3 * n * 4 + 15) / 16 * 16;
+    L.stg = L.tmpl + k_pad * 2;
+    L.bar = L.stg + 32 * env_e_pad(n) * 2;
+    L.total = L.bar + 16;
+    return L;
+}
+__host__ __device__ inline int env_smem_bytes(int n, int k_pad) { return env_smem_layout(n, k_pad).total; }
 
 __device__ __forceinline__ uint16_t f2bf(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
-__global__ void __launch_bounds__(32 * ENV_WARPS) env_step_kernel(const EnvArgs a) {
-    __shared__ EnvSmem sm_all[ENV_WARPS];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * ENV_WARPS + warp;
-    if (tile >= a.n_tiles) return;   // warp-uniform
-    EnvSmem& sm = sm_all[warp];
+__global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_constant__ EnvMaps maps, const EnvArgs a) {
+    extern __shared__ __align__(128) uint8_t env_smem[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int tile = blockIdx.x;
     const int n = a.n;
-    const int e = tile * 32 + lane;
+    const int e_pad = env_e_pad(n);
+    const EnvSmemLayout SL = env_smem_layout(n, a.k_pad);
+    int32_t* hold_s = reinterpret_cast<int32_t*>(env_smem);                                     // [n][32]
+    int16_t* aint_s = reinterpret_cast<int16_t*>(env_smem + SL.aint);                           // [n][32]
+    double* unit_s = reinterpret_cast<double*>(env_smem + SL.unit);   // [n] p_t (1 + c)
+    double* p_t64 = unit_s + n;                                           // [n] p_t as float64
+    double* p_164 = unit_s + 2 * n;                                       // [n] p_{t+1} as float64
+    float* p_t = reinterpret_cast<float*>(env_smem + SL.p);
+    float* p_1 = p_t + n;
+    float* p_0 = p_1 + n;
+    uint16_t* tmpl = reinterpret_cast<uint16_t*>(env_smem + SL.tmpl);
+    uint16_t* stg = reinterpret_cast<uint16_t*>(env_smem + SL.stg);                           // [32][e_pad]
+    const uint32_t bar = smem_u32(env_smem + SL.bar);
+
+    const int e = tile * 32 + lane;                 // this lane's env (all four warps)
     const bool active = e < a.N;
     const int64_t N = a.N;
+    const bool full_tile = (tile + 1) * 32 <= a.N;
+    const bool stepping = a.mode == 0;
+    const bool need_hold = a.mode != 2;
+    const bool tma = need_hold && full_tile && a.tma_ok;
 
+    // ---- 1. fetch the tile's holdings h_t[n][32] and actions a_t[n][32]: two 2-D TMA boxes
+    if (tma && tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(n) * (stepping ? 192u : 128u));
+        tma_load_2d(smem_u32(hold_s), &maps.hold, tile * 32, 0, bar);
+        if (stepping) tma_load_2d(smem_u32(aint_s), &maps.aint, tile * 32, 0, bar);
+    }
+    // per-env ledger state (warp 0 owns the ledger)
+    double cash0 = 0.0, v0 = 0.0, disc0 = 0.0;
+    if (warp == 0 && active && a.mode != 2) {
+        cash0 = a.cash[e];
+        if (stepping) {
+            v0 = a.asset[e];
+            disc0 = a.disc[e];
+        }
+    }
     const int64_t s = a.tile_start[tile];
     const int k = a.mode == 2 ? 0 : a.tile_k[tile];
     const double gpow = a.mode == 2 ? 1.0 : a.tile_gpow[tile];
     const int64_t t = s + k;
-    const bool stepping = a.mode == 0;
     const bool done = stepping && ((k + 1 == a.horizon) || (t + 1 == a.T_data - 1));
-    // market row the next observation is taken at
-    const int64_t t_obs = stepping ? (done ? s : t + 1) : t;
+    const int64_t t_obs = stepping ? (done ? s : t + 1) : t;   // market row of the next observation
 
-    // ---- stage the tile's market rows (all lanes, coalesced)
-    for (int i = lane; i < n; i += 32) {
-        sm.p_t[i] = a.close[t * n + i];
-        sm.p_1[i] = stepping ? a.close[(t + 1) * n + i] : a.close[t * n + i];
-        sm.p_0[i] = a.close[s * n + i];
-    }
-    __syncwarp();
-    // ---- per-tile part of the observation: p/p0 at t_obs, indicators, zero pad
-    {
-        const int e_cols = 1 + n;
-        for (int c = lane; c < a.k_pad; c += 32) {
-            float v = 0.0f;
-            if (c >= e_cols && c < e_cols + n) {
-                const int i = c - e_cols;
-                const float p = t_obs == s ? sm.p_0[i] : (t_obs == t ? sm.p_t[i] : sm.p_1[i]);
-                v = p / sm.p_0[i];
-            } else if (c >= e_cols + n && c < a.obs_dim) {
-                const int j = c - e_cols - n;   // channel-major: j = ch * n + i
-                v = a.feat[t_obs * a.f * n + j];
-            }
-            sm.tmpl[c] = f2bf(v);
+    if (need_hold && !tma) {   // ragged tile: cooperative plain loads
+        for (int i = warp; i < n; i += 4) {
+            hold_s[i * 32 + lane] = active ? a.hold[i * N + e] : 0;
+            if (stepping) aint_s[i * 32 + lane] = active ? a.aint[i * N + e] : 0;
         }
     }
-    __syncwarp();
+    // ---- 2. market rows: every thread issues all of its loads before using any
+    {
+        const int total = 3 * n + a.f * n;
+        constexpr int PER = (ENV_MAX_MARKET + ENV_THREADS - 1) / ENV_THREADS;
+        float vals[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + ENV_THREADS * q;
+            float x = 0.0f;
+            if (idx < total) {
+                const float* src;
+                if (idx < n) src = a.close + t * n + idx;
+                else if (idx < 2 * n) src = a.close + (stepping ? t + 1 : t) * n + (idx - n);
+                else if (idx < 3 * n) src = a.close + s * n + (idx - 2 * n);
+                else src = a.feat + t_obs * a.f * n + (idx - 3 * n);
+                x = __ldg(src);
+            }
+            vals[q] = x;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + ENV_THREADS * q;
+            if (idx < 3 * n) p_t[idx] = vals[q];
+            else if (idx < total) tmpl[1 + 2 * n + (idx - 3 * n)] = f2bf(vals[q]);
+        }
+    }
+    __syncthreads();
+    // ---- 3. per-tile constants: unit price p_t (1 + c), p/p0 at t_obs, zero pad
+    const double opc = __dadd_rn(1.0, a.cost);
+    for (int i = tid; i < n; i += ENV_THREADS) {
+        unit_s[i] = __dmul_rn(static_cast<double>(p_t[i]), opc);
+        p_t64[i] = static_cast<double>(p_t[i]);
+        p_164[i] = static_cast<double>(p_1[i]);
+    }
+    for (int c = tid; c < a.k_pad; c += ENV_THREADS) {
+        if (c >= 1 + n && c < 1 + 2 * n) {
+            const int i = c - 1 - n;
+            const float p = t_obs == s ? p_0[i] : (t_obs == t ? p_t[i] : p_1[i]);
+            tmpl[c] = f2bf(p / p_0[i]);
+        } else if (c >= a.obs_dim || c < 1 + n) {
+            tmpl[c] = 0;
+        }
+    }
+    if (tma) mbar_wait(bar, 0);
+    __syncthreads();
 
-    if (active) {
-        double cash, v;
+    // ---- 4. the float64 ledger, warp 0, lane = env, in exactly the order of
+    //         Eqs. 3-4 under R#3/R#4 (sells, then greedy buys, tickers ascending)
+    double cash = cash0;
+    if (warp == 0 && active) {
         if (a.mode == 2) {
             cash = a.C0;
-            for (int i = 0; i < n; ++i) a.hold[i * N + e] = 0;
             a.cash[e] = a.C0;
             a.asset[e] = a.C0;
             a.disc[e] = 0.0;
             a.ep_ret[e] = 0.0;
-        } else {
-            cash = a.cash[e];
-        }
-        if (stepping) {
-            v = a.asset[e];
+        } else if (stepping) {
             const double omc = __dadd_rn(1.0, -a.cost);
-            const double opc = __dadd_rn(1.0, a.cost);
-            // selling set (Eq. 3 "+ (p^S)^T k^S")
+            // selling set (Eq. 3 "+ (p^S)^T k^S"), tickers ascending.  Branch-free: a
+            // non-sell adds +0.0, which leaves the (never negative-zero) cash unchanged.
+#pragma unroll 4
             for (int i = 0; i < n; ++i) {
-                const int ai = a.aint[i * N + e];
-                if (ai < 0) {
-                    const int h = a.hold[i * N + e];
-                    const int q = min(h, -ai);
-                    cash = __dadd_rn(cash, __dmul_rn(__dmul_rn(static_cast<double>(sm.p_t[i]), static_cast<double>(q)), omc));
-                }
+                const int ai = aint_s[i * 32 + lane];
+                const int h = hold_s[i * 32 + lane];
+                const int q = ai < 0 ? min(h, -ai) : 0;
+                hold_s[i * 32 + lane] = h - q;
+                cash = __dadd_rn(cash, __dmul_rn(__dmul_rn(p_t64[i], static_cast<double>(q)), omc));
             }
-            // buying set (Eq. 3 "- (p^B)^T k^B"), then revalue at p_{t+1} (Eq. 2)
+            // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending, then revalue at p_{t+1}.
+            // Exact shortcut: if fl(fl((a+1) unit) (1 + 2^-49)) <= b then the exact (a+1) unit < b,
+            // so floor(b / unit) >= a + 1 and the oracle's clipped quantity is a; the cost is
+            // then fl(a unit), which does not depend on b.  Only cash-limited buys divide.
             double ph = 0.0;
-            const float inv_c0 = static_cast<float>(1.0 / a.C0);
+#pragma unroll 4
             for (int i = 0; i < n; ++i) {
-                const int ai = a.aint[i * N + e];
-                int h = a.hold[i * N + e];
-                if (ai < 0) h -= min(h, -ai);
-                if (ai > 0) {
-                    const double unit = __dmul_rn(static_cast<double>(sm.p_t[i]), opc);
+                const int ai = aint_s[i * 32 + lane];
+                int h = hold_s[i * 32 + lane];
+                const double unit = unit_s[i];
+                const int ap = ai > 0 ? ai : 0;
+                const double need = ai > 0 ? __dmul_rn(__dmul_rn(static_cast<double>(ap + 1), unit), 1.0000000000000017763568394002504646778106689453125) : 0.0;
+                double cost = __dmul_rn(static_cast<double>(ap), unit);
+                int q = ap;
+                if (need > cash) {   // cash-limited: the oracle's floor + post-check
                     double qmax = floor(__ddiv_rn(cash, unit));
                     if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
-                    double q = static_cast<double>(ai) < qmax ? static_cast<double>(ai) : qmax;
-                    q = q < 0.0 ? 0.0 : q;
-                    h += static_cast<int>(q);
-                    cash = __dadd_rn(cash, -__dmul_rn(q, unit));
+                    double qd = static_cast<double>(ai) < qmax ? static_cast<double>(ai) : qmax;
+                    qd = qd < 0.0 ? 0.0 : qd;
+                    q = static_cast<int>(qd);
+                    cost = __dmul_rn(qd, unit);
                 }
-                ph = __dadd_rn(ph, __dmul_rn(static_cast<double>(sm.p_1[i]), static_cast<double>(h)));
-                a.hold[i * N + e] = done ? 0 : h;
-                if (a.dbg_hold) a.dbg_hold[static_cast<int64_t>(e) * n + i] = h;
-                sm.stg[lane][1 + i] = done ? f2bf(0.0f) : f2bf(static_cast<float>(h) * sm.p_1[i] * inv_c0);
+                h += q;
+                cash = __dadd_rn(cash, -cost);
+                hold_s[i * 32 + lane] = h;
+                ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
             }
             const double v1 = __dadd_rn(cash, ph);
-            const double r = __dmul_rn(a.scale, __dadd_rn(v1, -v));
-            double disc = __dadd_rn(a.disc[e], __dmul_rn(gpow, r));
+            const double r = __dmul_rn(a.scale, __dadd_rn(v1, -v0));
+            double disc = __dadd_rn(disc0, __dmul_rn(gpow, r));
             a.rew[e] = static_cast<float>(r);
             a.done[e] = done ? 1 : 0;
             if (a.dbg_cash) a.dbg_cash[e] = cash;
             if (!isfinite(v1)) atomicOr(a.err, 2u);
+            double v = v1;
             if (done) {
                 a.ep_ret[e] = disc;
                 cash = a.C0;
                 v = a.C0;
                 disc = 0.0;
-            } else {
-                v = v1;
             }
             a.cash[e] = cash;
             a.asset[e] = v;
             a.disc[e] = disc;
-        } else {
-            const float inv_c0 = static_cast<float>(1.0 / a.C0);
-            for (int i = 0; i < n; ++i) {
-                const int h = a.mode == 2 ? 0 : a.hold[i * N + e];
-                sm.stg[lane][1 + i] = f2bf(static_cast<float>(h) * sm.p_t[i] * inv_c0);
+        }
+        uint16_t* my = stg + lane * e_pad;
+        my[0] = f2bf(static_cast<float>(cash / a.C0));
+        for (int c = 1 + n; c < e_pad; ++c) my[c] = tmpl[c];
+    }
+    if (warp != 0 && a.gen_noise) {
+        // the actor's Gaussian noise for the next actor launch (R#14: Philox4x32-10 keyed on
+        // (global env, global step, ticker quad)), drawn while warp 0 runs the ledger
+        const uint64_t step = *a.step_base + static_cast<uint64_t>(a.noise_t);
+        const int nq = (n + 3) / 4;
+        for (int idx = tid - 32; idx < 32 * nq; idx += ENV_THREADS - 32) {
+            const int el = idx & 31;
+            const int qd = idx >> 5;
+            const int ee = tile * 32 + el;
+            if (ee < a.N) {
+                const float4 z = normals4(a.seed, static_cast<uint32_t>(a.env_offset + ee), step, static_cast<uint32_t>(qd));
+                const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (4 * qd + j < n) a.znoise[static_cast<int64_t>(4 * qd + j) * N + ee] = zz[j];
             }
         }
-        sm.stg[lane][0] = f2bf(static_cast<float>(cash / a.C0));
     }
-    const int e_pad = (1 + n + 7) / 8 * 8;   // per-env staging width, 16-B multiple
-    if (active) {
-        for (int c = 1 + n; c < e_pad; ++c) sm.stg[lane][c] = sm.tmpl[c];
-    }
-    if (lane == 0 && stepping) {
+    if (tid == 0 && stepping) {
         a.tile_k[tile] = done ? 0 : k + 1;
         a.tile_gpow[tile] = done ? 1.0 : __dmul_rn(gpow, a.gamma);
     }
-    if (lane == 0 && a.mode == 2) {
+    if (tid == 0 && a.mode == 2) {
         a.tile_k[tile] = 0;
         a.tile_gpow[tile] = 1.0;
     }
-    __syncwarp();
-    // ---- write s_{t+1}: each env row by the whole warp, 16-B chunks
+    __syncthreads();
+    // ---- 5. holdings out (coalesced rows) and the per-env part of s_{t+1}, 4 warps
+    {
+        const float inv_c0 = static_cast<float>(1.0 / a.C0);
+        const float* p_obs = stepping ? p_1 : p_t;
+        uint16_t* my = stg + lane * e_pad;
+        for (int i = warp; i < n; i += 4) {
+            const int h = a.mode == 2 ? 0 : hold_s[i * 32 + lane];
+            if (active) {
+                if (stepping) {
+                    a.hold[i * N + e] = done ? 0 : h;
+                    if (a.dbg_hold) a.dbg_hold[static_cast<int64_t>(e) * n + i] = h;
+                } else if (a.mode == 2) {
+                    a.hold[i * N + e] = 0;
+                }
+            }
+            my[1 + i] = (done || a.mode == 2) ? 0 : f2bf(static_cast<float>(h) * p_obs[i] * inv_c0);
+        }
+    }
+    __syncthreads();
+    // ---- 6. write s_{t+1}: env rows spread over the 4 warps, 16-B chunks (512 B per instruction)
     if (a.obs_out) {
         const int chunks = a.k_pad / 8;
         const int rows = min(32, a.N - tile * 32);
-        for (int row = 0; row < rows; ++row) {
+        for (int row = warp; row < rows; row += 4) {
             uint4* dst = reinterpret_cast<uint4*>(a.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
             for (int c = lane; c < chunks; c += 32) {
-                const uint4 val = c * 8 < e_pad ? *reinterpret_cast<const uint4*>(&sm.stg[row][c * 8])
-                                                : *reinterpret_cast<const uint4*>(&sm.tmpl[c * 8]);
+                const uint4 val = c * 8 < e_pad ? *reinterpret_cast<const uint4*>(stg + row * e_pad + c * 8)
+                                                : *reinterpret_cast<const uint4*>(tmpl + c * 8);
                 dst[c] = val;
             }
         }
@@ -241,19 +360,30 @@ __global__ void inject_map_kernel(const float* __restrict__ u, int N, int n, int
     if (dbg_aint) dbg_aint[idx] = static_cast<int16_t>(ai);
 }
 
-// J_a = (sum over agent a's envs of ep_ret) / per_agent, one block per agent
-__global__ void fitness_kernel(const double* __restrict__ ep_ret, int per_agent, double* __restrict__ out) {
-    __shared__ double red[256];
+// J_a = (sum over agent a's envs of ep_ret) / per_agent, one 1024-thread block per agent
+__global__ void __launch_bounds__(1024) fitness_kernel(const double* __restrict__ ep_ret, int per_agent,
+                                                       double* __restrict__ out) {
+    __shared__ double red[32];
     const int agent = blockIdx.x;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < per_agent; i += blockDim.x) acc += ep_ret[static_cast<int64_t>(agent) * per_agent + i];
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
+    const double* src = ep_ret + static_cast<int64_t>(agent) * per_agent;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int i = threadIdx.x;
+    for (; i + 3 * 1024 < per_agent; i += 4 * 1024) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += src[i + q * 1024];
     }
-    if (threadIdx.x == 0) out[agent] = red[0] / static_cast<double>(per_agent);
+    for (; i < per_agent; i += 1024) acc[0] += src[i];
+    double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = red[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) out[agent] = v / static_cast<double>(per_agent);
+    }
 }
 
 // hold [n][N] -> out [N][n]

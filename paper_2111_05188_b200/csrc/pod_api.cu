@@ -110,13 +110,26 @@ static pod_status encode_bf16(CUtensorMap* m, const void* base, int rank, const 
     return POD_OK;
 }
 
+// 2-D, no swizzle (state tiles for the env-step kernel)
+static pod_status encode_plain(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const uint64_t* dims,
+                               const uint64_t* strides_bytes, const uint32_t* box) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t d[2] = {dims[0], dims[1]}, s[1] = {strides_bytes[0]};
+    cuuint32_t b[2] = {box[0], box[1]}, es[2] = {1, 1};
+    CUresult r = enc(m, dt, 2, const_cast<void*>(base), d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled (state) failed (%d)", static_cast<int>(r));
+    return POD_OK;
+}
+
 // ------------------------------------------------------------ layout
 static pod_status dims_of(const pod_env_config* c, int* obs_dim, int* k_pad, int* n_out_pad) {
     if (!c) return pod_fail(POD_ERR_ARG, "config is NULL");
     if (c->n_stocks < 1 || c->n_feat < 0) return pod_fail(POD_ERR_ARG, "n_stocks >= 1 and n_feat >= 0 required");
     *obs_dim = 1 + 2 * c->n_stocks + c->n_stocks * c->n_feat;
     *k_pad = static_cast<int>(round_up(static_cast<size_t>(*obs_dim), 64));
-    *n_out_pad = static_cast<int>(round_up(static_cast<size_t>(c->n_stocks), 16));
+    *n_out_pad = static_cast<int>(round_up(static_cast<size_t>(c->n_stocks), 32));
     if (*k_pad > ENV_MAX_KPAD || c->n_stocks > ENV_MAX_STOCKS)
         return pod_fail(POD_ERR_UNSUPPORTED, "obs_dim %d exceeds the kernel limit (k_pad <= %d, n <= %d)", *obs_dim,
                         ENV_MAX_KPAD, ENV_MAX_STOCKS);
@@ -131,9 +144,9 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
     if (st) return st;
     if (n_hidden < 1 || n_hidden > POD_MAX_HIDDEN_LAYERS)
         return pod_fail(POD_ERR_UNSUPPORTED, "n_hidden must be in [1, %d]", POD_MAX_HIDDEN_LAYERS);
-    if (!(hidden == 64 || hidden == 128 || hidden == 192 || hidden == 256 || hidden == 512))
-        return pod_fail(POD_ERR_UNSUPPORTED, "hidden must be one of 64, 128, 192, 256, 512");
-    if (nop > 256) return pod_fail(POD_ERR_UNSUPPORTED, "n_stocks > 256");
+    if (!(hidden == 128 || hidden == 256 || hidden == 512))
+        return pod_fail(POD_ERR_UNSUPPORTED, "hidden must be one of 128, 256, 512");
+    if (nop > 128) return pod_fail(POD_ERR_UNSUPPORTED, "n_stocks > 128");
     memset(out, 0, sizeof(*out));
     out->obs_dim = od;
     out->k_pad = kp;
@@ -160,24 +173,52 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
 
 // ------------------------------------------------------------ env handle
 struct GraphKey {
-    int32_t T, deterministic, n_hidden, hidden, act, pad_;
+    int32_t T, deterministic, n_hidden, hidden, act, profile;
     const void* ptrs[12];
     size_t param_bytes;
+};
+
+// CUDA events recorded around every actor / env-step launch of one rollout
+// (profiling mode): ev[4t+0..1] bracket the actor at step t, ev[4t+2..3] the env step.
+struct ProfEvents {
+    std::vector<cudaEvent_t> ev;
+    int T = 0;
+    int stride = 1;
+    int n_marked = 0;
+    bool injected = false;
+    pod_status create(int T_, int stride_, bool inj) {
+        T = T_;
+        stride = stride_ < 1 ? 1 : stride_;
+        n_marked = (T_ + stride - 1) / stride;
+        injected = inj;
+        ev.resize(static_cast<size_t>(4) * n_marked);
+        for (auto& x : ev)
+            if (cudaEventCreate(&x) != cudaSuccess) return pod_fail(POD_ERR_CUDA, "cudaEventCreate failed");
+        return POD_OK;
+    }
+    void destroy() {
+        for (auto& x : ev)
+            if (x) cudaEventDestroy(x);
+        ev.clear();
+    }
 };
 
 struct GraphEntry {
     GraphKey key;
     cudaGraphExec_t exec;
     uint64_t last_use;
+    ProfEvents* prof;
 };
 
 struct pod_env {
     pod_env_config cfg;
     pod_market market;
-    int obs_dim, k_pad, n_out_pad, n_tiles, per_agent;
+    int obs_dim, k_pad, n_out_pad, n_tiles, per_agent, env_tma_ok;
+    EnvMaps env_maps;
     // workspace carve
     int32_t* hold;
     int16_t* aint;
+    float* znoise;
     double *cash, *asset, *disc, *ep_ret, *tile_gpow;
     int32_t *tile_start, *tile_k;
     uint64_t* step;
@@ -187,10 +228,14 @@ struct pod_env {
     std::vector<GraphEntry> graphs;
     uint64_t use_clock;
     bool use_graphs;
+    int profile;                // 0 = off, k = bracket every k-th step
+    unsigned long long* trace;  // diagnostics: actor clock64 stamps of the last launch
+    ProfEvents* last_prof;      // events of the most recent profiled rollout
+    ProfEvents direct_prof;     // events for non-graph profiled rollouts
 };
 
 struct WsLayout {
-    size_t hold, aint, cash, asset, disc, ep_ret, tile_start, tile_k, tile_gpow, step, err, total;
+    size_t hold, aint, znoise, cash, asset, disc, ep_ret, tile_start, tile_k, tile_gpow, step, err, total;
 };
 
 static WsLayout ws_layout(const pod_env_config* c) {
@@ -205,6 +250,7 @@ static WsLayout ws_layout(const pod_env_config* c) {
     };
     w.hold = take(n * N * 4);
     w.aint = take(n * N * 2);
+    w.znoise = take(n * N * 4);
     w.cash = take(N * 8);
     w.asset = take(N * 8);
     w.disc = take(N * 8);
@@ -262,6 +308,7 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     char* b = static_cast<char*>(ws);
     e->hold = reinterpret_cast<int32_t*>(b + w.hold);
     e->aint = reinterpret_cast<int16_t*>(b + w.aint);
+    e->znoise = reinterpret_cast<float*>(b + w.znoise);
     e->cash = reinterpret_cast<double*>(b + w.cash);
     e->asset = reinterpret_cast<double*>(b + w.asset);
     e->disc = reinterpret_cast<double*>(b + w.disc);
@@ -272,6 +319,9 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     e->step = reinterpret_cast<uint64_t*>(b + w.step);
     e->err = reinterpret_cast<uint32_t*>(b + w.err);
     e->use_clock = 0;
+    e->profile = 0;
+    e->last_prof = nullptr;
+    e->trace = nullptr;
     const char* ng = getenv("POD_NO_GRAPH");
     e->use_graphs = !(ng && ng[0] == '1');
     cudaError_t ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_starts), sizeof(int32_t) * e->n_tiles);
@@ -280,11 +330,30 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  env_smem_bytes(ENV_MAX_STOCKS, ENV_MAX_KPAD));
+    if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(gae_smem_bytes()));
     if (ce != cudaSuccess) {
         delete e;
         return pod_fail(POD_ERR_CUDA, "pod_env_create: %s", cudaGetErrorString(ce));
+    }
+    // 2-D tensor maps over the ticker-major state: one TMA box = one tile's [n][32]
+    e->env_tma_ok = (cfg->n_envs % 8 == 0) ? 1 : 0;
+    if (e->env_tma_ok) {
+        const uint64_t N = static_cast<uint64_t>(cfg->n_envs), n = static_cast<uint64_t>(cfg->n_stocks);
+        const uint64_t dh[2] = {N, n}, sh[1] = {N * 4};
+        const uint64_t da[2] = {N, n}, sa[1] = {N * 2};
+        const uint32_t box[2] = {32, static_cast<uint32_t>(n)};
+        st = encode_plain(&e->env_maps.hold, e->hold, CU_TENSOR_MAP_DATA_TYPE_INT32, dh, sh, box);
+        if (!st) st = encode_plain(&e->env_maps.aint, e->aint, CU_TENSOR_MAP_DATA_TYPE_UINT16, da, sa, box);
+        if (st) {
+            delete e;
+            return st;
+        }
+    } else {
+        memset(&e->env_maps, 0, sizeof(e->env_maps));
     }
     *out = e;
     return POD_OK;
@@ -292,7 +361,14 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
 
 extern "C" pod_status pod_env_destroy(pod_env_t* e) {
     if (!e) return POD_OK;
-    for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : e->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        if (g.prof) {
+            g.prof->destroy();
+            delete g.prof;
+        }
+    }
+    e->direct_prof.destroy();
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     if (e->h_starts) cudaFreeHost(e->h_starts);
     delete e;
@@ -326,10 +402,18 @@ static EnvArgs env_args(const pod_env* e, int mode) {
     a.tile_k = e->tile_k;
     a.tile_gpow = e->tile_gpow;
     a.err = e->err;
+    a.tma_ok = e->env_tma_ok;
+    a.seed = e->cfg.seed;
+    a.env_offset = e->cfg.env_offset;
+    a.step_base = e->step;
+    a.znoise = e->znoise;
     return a;
 }
 
-static inline int env_blocks(const pod_env* e) { return (e->n_tiles + ENV_WARPS - 1) / ENV_WARPS; }
+static inline int env_blocks(const pod_env* e) { return e->n_tiles; }
+static inline size_t env_smem(const pod_env* e) {
+    return static_cast<size_t>(env_smem_bytes(e->cfg.n_stocks, e->k_pad));
+}
 
 static uint64_t splitmix64(uint64_t& x) {
     uint64_t z = (x += 0x9E3779B97F4A7C15ull);
@@ -356,7 +440,7 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
     POD_CUDA(cudaMemsetAsync(e->step, 0, 8, s));
     EnvArgs a = env_args(e, 2);
     a.obs_out = obs0;
-    env_step_kernel<<<env_blocks(e), 32 * ENV_WARPS, 0, s>>>(a);
+    env_step_kernel<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
     POD_CUDA(cudaGetLastError());
     POD_CUDA(cudaStreamSynchronize(s));   // the pinned staging buffer is reused by the next reset
     return POD_OK;
@@ -371,13 +455,24 @@ struct RolloutPlan {
 };
 
 static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj,
-                                  double* fitness_out, cudaStream_t s) {
+                                  double* fitness_out, cudaStream_t s, ProfEvents* prof) {
+    auto mark = [&](int t, int k) {
+        // external event-record node when captured into the graph (timing-capable);
+        // only every `stride`-th step is bracketed, to keep the timing overhead small
+        if (prof && t % prof->stride == 0)
+            cudaEventRecordWithFlags(prof->ev[static_cast<size_t>(4 * (t / prof->stride) + k)], s,
+                                     cudaEventRecordExternal);
+    };
     const int N = e->cfg.n_envs, n = e->cfg.n_stocks;
     // s_0 from the carried state
     EnvArgs a0 = env_args(e, 1);
     a0.obs_out = tr->obs;
-    env_step_kernel<<<env_blocks(e), 32 * ENV_WARPS, 0, s>>>(a0);
+    const int sampling = (!p.injected && !p.aa.deterministic) ? 1 : 0;
+    a0.gen_noise = sampling;          // noise for the actor launch of step 0
+    a0.noise_t = 0;
+    env_step_kernel<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
     for (int t = 0; t < T; ++t) {
+        mark(t, 0);
         if (p.injected) {
             const int64_t tot = static_cast<int64_t>(N) * n;
             inject_map_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(
@@ -391,19 +486,36 @@ static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const
             aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
             aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
             aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
-            const unsigned grid = static_cast<unsigned>(e->cfg.n_agents * aa.tiles_per_agent);
-            actor_forward_kernel<<<grid, ACT_THREADS, p.actor_smem, s>>>(p.maps, aa);
+            // one 2-CTA cluster per 128-env tile (column split of every layer)
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(static_cast<unsigned>(2 * e->cfg.n_agents * aa.tiles_per_agent));
+            lc.blockDim = dim3(ACT_THREADS);
+            lc.dynamicSmemBytes = p.actor_smem;
+            lc.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
         }
+        mark(t, 1);
+        mark(t, 2);
         EnvArgs a = env_args(e, 0);
         a.rew = tr->rew + static_cast<int64_t>(t) * N;
         a.done = tr->done + static_cast<int64_t>(t) * N;
         a.obs_out = tr->obs + static_cast<int64_t>(t + 1) * N * e->k_pad;
         a.dbg_hold = tr->dbg_hold ? tr->dbg_hold + static_cast<int64_t>(t) * N * n : nullptr;
         a.dbg_cash = tr->dbg_cash ? tr->dbg_cash + static_cast<int64_t>(t) * N : nullptr;
-        env_step_kernel<<<env_blocks(e), 32 * ENV_WARPS, 0, s>>>(a);
+        a.gen_noise = (sampling && t + 1 < T) ? 1 : 0;   // noise for the actor launch of step t+1
+        a.noise_t = t + 1;
+        env_step_kernel<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+        mark(t, 3);
     }
     if (!p.injected) bump_step_kernel<<<1, 1, 0, s>>>(e->step, static_cast<uint64_t>(T));
-    if (fitness_out) fitness_kernel<<<e->cfg.n_agents, 256, 0, s>>>(e->ep_ret, e->per_agent, fitness_out);
+    if (fitness_out) fitness_kernel<<<e->cfg.n_agents, 1024, 0, s>>>(e->ep_ret, e->per_agent, fitness_out);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }
@@ -439,11 +551,9 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             st = encode_bf16(&p.maps.obs, tr->obs, 2, dims, str, box);
             if (st) return st;
         }
-        int bn_max = 16;
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
-            const int bn = rows > 256 ? 256 : rows;
-            bn_max = bn > bn_max ? bn : bn_max;
+            const int bn = actor_bn(rows / 2);
             const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
                                       static_cast<uint64_t>(e->cfg.n_agents)};
             const uint64_t str[2] = {static_cast<uint64_t>(L.w_cols[l]) * 2, actor->param_bytes};
@@ -463,7 +573,6 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         aa.act = actor->act;
         aa.h_max = e->cfg.h_max;
         aa.deterministic = deterministic ? 1 : 0;
-        aa.bn_max = bn_max;
         aa.seed = e->cfg.seed;
         aa.env_offset = e->cfg.env_offset;
         aa.step_base = e->step;
@@ -472,17 +581,29 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         for (int l = 0; l < L.n_layers; ++l) aa.b_off[l] = L.b_offset[l];
         aa.log_std_off = L.log_std_offset;
         aa.aint = e->aint;
+        aa.znoise = e->znoise;
         aa.err = e->err;
-        const int ka = (L.k_pad > actor->hidden ? L.k_pad : actor->hidden) / 64;
-        p.actor_smem = 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * bn_max * 128 + 128;
+        aa.trace = e->trace;
+        p.actor_smem = actor_smem_bytes(L.k_pad, actor->hidden);
         if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
     }
-    if (!e->use_graphs) return enqueue_rollout(e, p, T, tr, injected_u, fitness_out, s);
+    if (!e->use_graphs) {
+        ProfEvents* prof = nullptr;
+        if (e->profile) {
+            e->direct_prof.destroy();
+            pod_status st = e->direct_prof.create(T, e->profile, p.injected);
+            if (st) return st;
+            prof = &e->direct_prof;
+        }
+        e->last_prof = prof;
+        return enqueue_rollout(e, p, T, tr, injected_u, fitness_out, s, prof);
+    }
 
     GraphKey key;
     memset(&key, 0, sizeof(key));
     key.T = T;
     key.deterministic = deterministic ? 1 : 0;
+    key.profile = e->profile;
     if (!p.injected) {
         key.n_hidden = actor->n_hidden;
         key.hidden = actor->hidden;
@@ -498,8 +619,18 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         if (memcmp(&g.key, &key, sizeof(key)) == 0) hit = &g;
     if (!hit) {
         cudaGraph_t graph;
+        ProfEvents* prof = nullptr;
+        if (e->profile) {
+            prof = new ProfEvents();
+            pod_status pst = prof->create(T, e->profile, p.injected);
+            if (pst) {
+                prof->destroy();
+                delete prof;
+                return pst;
+            }
+        }
         POD_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
-        pod_status st = enqueue_rollout(e, p, T, tr, injected_u, fitness_out, e->cap_stream);
+        pod_status st = enqueue_rollout(e, p, T, tr, injected_u, fitness_out, e->cap_stream, prof);
         cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &graph);
         if (st) return st;
         if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
@@ -512,19 +643,64 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             for (size_t i = 1; i < e->graphs.size(); ++i)
                 if (e->graphs[i].last_use < e->graphs[victim].last_use) victim = i;
             cudaGraphExecDestroy(e->graphs[victim].exec);
+            if (e->graphs[victim].prof) {
+                e->graphs[victim].prof->destroy();
+                delete e->graphs[victim].prof;
+            }
             e->graphs.erase(e->graphs.begin() + static_cast<long>(victim));
         }
-        e->graphs.push_back(GraphEntry{key, exec, 0});
+        e->graphs.push_back(GraphEntry{key, exec, 0, prof});
         hit = &e->graphs.back();
     }
     hit->last_use = ++e->use_clock;
+    e->last_prof = hit->prof;
     POD_CUDA(cudaGraphLaunch(hit->exec, s));
+    return POD_OK;
+}
+
+extern "C" pod_status pod_debug_actor_trace(pod_env_t* e, unsigned long long* buf) {
+    if (!e) return pod_fail(POD_ERR_ARG, "env is NULL");
+    e->trace = buf;
+    for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
+    e->graphs.clear();
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_profile(pod_env_t* e, int32_t enable) {
+    if (!e) return pod_fail(POD_ERR_ARG, "env is NULL");
+    if (enable < 0) return pod_fail(POD_ERR_ARG, "profile stride must be >= 0");
+    e->profile = enable;
+    e->last_prof = nullptr;
+    return POD_OK;
+}
+
+extern "C" pod_status pod_env_profile_read(pod_env_t* e, double* actor_ms, int64_t* actor_launches, double* env_ms,
+                                           int64_t* env_launches, void* stream) {
+    if (!e || !actor_ms || !actor_launches || !env_ms || !env_launches) return pod_fail(POD_ERR_ARG, "NULL argument");
+    *actor_ms = *env_ms = 0.0;
+    *actor_launches = *env_launches = 0;
+    ProfEvents* p = e->last_prof;
+    if (!p) return POD_OK;
+    POD_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    double a = 0.0, v = 0.0;
+    for (int t = 0; t < p->n_marked; ++t) {
+        float ms = 0.f;
+        POD_CUDA(cudaEventElapsedTime(&ms, p->ev[static_cast<size_t>(4 * t)], p->ev[static_cast<size_t>(4 * t + 1)]));
+        a += ms;
+        POD_CUDA(cudaEventElapsedTime(&ms, p->ev[static_cast<size_t>(4 * t + 2)], p->ev[static_cast<size_t>(4 * t + 3)]));
+        v += ms;
+    }
+    *actor_ms = a;
+    *env_ms = v;
+    *actor_launches = p->n_marked;
+    *env_launches = p->n_marked;
+    e->last_prof = nullptr;
     return POD_OK;
 }
 
 extern "C" pod_status pod_env_fitness(pod_env_t* e, double* fitness_out, void* stream) {
     if (!e || !fitness_out) return pod_fail(POD_ERR_ARG, "env and fitness_out must be non-NULL");
-    fitness_kernel<<<e->cfg.n_agents, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->ep_ret, e->per_agent, fitness_out);
+    fitness_kernel<<<e->cfg.n_agents, 1024, 0, static_cast<cudaStream_t>(stream)>>>(e->ep_ret, e->per_agent, fitness_out);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }

@@ -30,60 +30,63 @@ ENV_TILE = 32  # envs per tile (one warp); tiles share a start row
 # Market data
 # ---------------------------------------------------------------------------
 def _ema(x: np.ndarray, period: int) -> np.ndarray:
-    """EMA along axis 0 seeded with the first value (S:L55–60 warm-up rule)."""
+    """EMA along the last axis (time), seeded with the first value."""
     a = 2.0 / (period + 1.0)
-    zi = ((1.0 - a) * x[0])[None, :]
-    y, _ = lfilter([a], [1.0, -(1.0 - a)], x, axis=0, zi=zi)
+    zi = ((1.0 - a) * x[:, :1])
+    y, _ = lfilter([a], [1.0, -(1.0 - a)], x, axis=-1, zi=zi)
     return y
 
 
 def _wilder(x: np.ndarray, period: int) -> np.ndarray:
     a = 1.0 / period
-    zi = ((1.0 - a) * x[0])[None, :]
-    y, _ = lfilter([a], [1.0, -(1.0 - a)], x, axis=0, zi=zi)
+    zi = ((1.0 - a) * x[:, :1])
+    y, _ = lfilter([a], [1.0, -(1.0 - a)], x, axis=-1, zi=zi)
     return y
 
 
 def _macd(close: np.ndarray) -> np.ndarray:
+    """close [n, T] -> MACD line EMA12 - EMA26 [n, T]."""
     return _ema(close, 12) - _ema(close, 26)
 
 
 def _rsi(close: np.ndarray, period: int = 14) -> np.ndarray:
-    d = np.diff(close, axis=0, prepend=close[:1])
+    """Wilder RSI [n, T]; flat series -> 50 (S:L90 convention)."""
+    d = np.diff(close, axis=-1, prepend=close[:, :1])
     g = _wilder(np.maximum(d, 0.0), period)
     l = _wilder(np.maximum(-d, 0.0), period)
     with np.errstate(divide="ignore", invalid="ignore"):
         rsi = 100.0 - 100.0 / (1.0 + g / l)
-    rsi = np.where(l == 0.0, np.where(g == 0.0, 50.0, 100.0), rsi)
-    return rsi
+    return np.where(l == 0.0, np.where(g == 0.0, 50.0, 100.0), rsi)
 
 
 def _cci(high: np.ndarray, low: np.ndarray, close: np.ndarray, period: int = 20) -> np.ndarray:
+    """CCI [n, T] = (tp - SMA(tp)) / (0.015 * mean |tp - SMA|) over the trailing window
+    (shorter during warm-up); zero deviation -> 0."""
     tp = (high + low + close) / 3.0
-    T, n = tp.shape
-    out = np.empty_like(tp)
-    cs = np.cumsum(tp, axis=0)
-    cs = np.concatenate([np.zeros((1, n)), cs], axis=0)
+    n, T = tp.shape
+    cs = np.concatenate([np.zeros((n, 1)), np.cumsum(tp, axis=-1)], axis=-1)
     idx = np.arange(T)
     lo = np.maximum(idx - period + 1, 0)
     cnt = (idx - lo + 1).astype(np.float64)
-    sma = (cs[idx + 1] - cs[lo]) / cnt[:, None]
-    # mean absolute deviation of the trailing window about the current SMA
-    pad = np.concatenate([np.repeat(tp[:1], period - 1, axis=0), tp], axis=0)
-    for i in range(n):
-        win = np.lib.stride_tricks.sliding_window_view(pad[:, i], period)  # [T, period]
-        dev = np.abs(win - sma[:, i : i + 1])
-        # warm-up windows only count the real rows
-        md = dev.sum(axis=1)
-        if period > 1:
-            head = min(period - 1, T)
-            for t in range(head):
-                md[t] = np.abs(tp[: t + 1, i] - sma[t, i]).sum()
-        md = md / cnt
-        with np.errstate(divide="ignore", invalid="ignore"):
-            c = (tp[:, i] - sma[:, i]) / (0.015 * md)
-        out[:, i] = np.where(md == 0.0, 0.0, c)
-    return out
+    sma = (cs[:, idx + 1] - cs[:, lo]) / cnt
+    # trailing-window sum of |tp_j - sma_t|; torch (multi-threaded CPU) over time blocks
+    import torch
+
+    tpt = torch.from_numpy(tp)
+    smat = torch.from_numpy(sma)
+    md_t = torch.zeros_like(tpt)
+    for t in range(min(period - 1, T)):  # warm-up: windows [0, t]
+        md_t[:, t] = (tpt[:, : t + 1] - smat[:, t : t + 1]).abs().sum(-1)
+    blk = 32768
+    for t0 in range(period - 1, T, blk):  # full windows [t - period + 1, t]
+        t1 = min(T, t0 + blk)
+        win = tpt[:, t0 - period + 1 : t1].unfold(1, period, 1)       # [n, t1 - t0, period]
+        md_t[:, t0:t1] = (win - smat[:, t0:t1, None]).abs().sum(-1)
+    md = md_t.numpy()
+    md /= cnt
+    with np.errstate(divide="ignore", invalid="ignore"):
+        c = (tp - sma) / (0.015 * md)
+    return np.where(md == 0.0, 0.0, c)
 
 
 @dataclass
@@ -135,22 +138,25 @@ def make_market(n: int, T_data: int, dt: float, seed: int, n_feat: int = 3,
     close64 = np.exp(logp)
     del logp
     close = close64.astype(np.float32)
-    close64 = close.astype(np.float64)  # indicators see exactly the stored prices
-    feats = []
-    if n_feat >= 1:
-        feats.append(_macd(close64))
-    if n_feat >= 2:
-        feats.append(_rsi(close64))
-    if n_feat >= 3:
-        spread = np.abs(rng.standard_normal((T_data, n))) * (0.25 * vol)
-        spread2 = np.abs(rng.standard_normal((T_data, n))) * (0.25 * vol)
-        feats.append(_cci(close64 * (1.0 + spread), close64 * (1.0 - spread2), close64))
-    for extra in range(3, n_feat):
-        feats.append(_ema(close64, 5 + 5 * extra) / close64 - 1.0)
+    del close64
+    cT = np.ascontiguousarray(close.T, dtype=np.float64)  # [n, T]: indicators see exactly the stored prices
     feat = np.empty((T_data, n_feat, n), dtype=np.float32)
-    for ch, x in enumerate(feats):
+
+    def put(ch, x):
         m, s = float(x.mean()), float(x.std())
-        feat[:, ch, :] = ((x - m) / (s if s > 0 else 1.0)).astype(np.float32)
+        feat[:, ch, :] = ((x - m) / (s if s > 0 else 1.0)).T.astype(np.float32)
+
+    if n_feat >= 1:
+        put(0, _macd(cT))
+    if n_feat >= 2:
+        put(1, _rsi(cT))
+    if n_feat >= 3:
+        spread = np.abs(rng.standard_normal((n, T_data))) * (0.25 * vol)[:, None]
+        spread2 = np.abs(rng.standard_normal((n, T_data))) * (0.25 * vol)[:, None]
+        put(2, _cci(cT * (1.0 + spread), cT * (1.0 - spread2), cT))
+        del spread, spread2
+    for extra in range(3, n_feat):
+        put(extra, _ema(cT, 5 + 5 * extra) / cT - 1.0)
     return Market(close=np.ascontiguousarray(close), feat=feat, dt=dt)
 
 

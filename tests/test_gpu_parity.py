@@ -263,3 +263,18 @@ def test_full_size_c3_sampled_rows():
     assert_obs_close(tr.obs[:, rows], out["obs"], c.obs_dim)
     # properties over all rows
     assert (tr.dbg_cash >= 0).all() and (tr.dbg_hold >= 0).all()
+
+
+def test_profile_events_in_graph():
+    c = Case(n=30, f=3, T_data=300, N=256, H=40)
+    aws, params, actor = _actor(c, 2, 128)
+    tr = api.Trajectory.allocate(6, 256, 30, c.k_pad)
+    c.env.reset(c.starts)
+    for stride, marked in ((1, 6), (4, 2)):
+        c.env.profile(stride)
+        for _ in range(2):   # capture, then replay
+            c.env.rollout(6, tr, actor=actor)
+            am, an, em, en = c.env.profile_read()
+            assert an == marked and en == marked and am > 0 and em > 0
+        assert c.env.profile_read() == (0.0, 0, 0.0, 0)
+    c.env.profile(0)

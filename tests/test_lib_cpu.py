@@ -36,11 +36,11 @@ def test_exports_match_header():
 def test_layout_and_workspace():
     cfg = api.make_config(8192, 100, 3, 8192)
     L = api.actor_layout(cfg, 3, 512)
-    assert (L.obs_dim, L.k_pad, L.n_out_pad, L.n_layers) == (501, 512, 112, 4)
-    assert [L.w_rows[i] for i in range(4)] == [512, 512, 512, 112]
+    assert (L.obs_dim, L.k_pad, L.n_out_pad, L.n_layers) == (501, 512, 128, 4)
+    assert [L.w_rows[i] for i in range(4)] == [512, 512, 512, 128]
     assert [L.w_cols[i] for i in range(4)] == [512, 512, 512, 512]
     assert L.param_bytes % 1024 == 0 and L.w_offset[0] == 0
-    assert L.b_offset[0] >= L.w_offset[3] + 112 * 512 * 2
+    assert L.b_offset[0] >= L.w_offset[3] + 128 * 512 * 2
     cfg30 = api.make_config(16, 30, 3, 64)
     L30 = api.actor_layout(cfg30, 2, 128)
     assert (L30.obs_dim, L30.k_pad, L30.n_out_pad) == (151, 192, 32)

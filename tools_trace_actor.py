@@ -1,0 +1,36 @@
+"""Diagnostics: per-phase clock64 timeline of the actor kernel at the C3 shape."""
+import sys
+import numpy as np
+import torch
+import ctypes as C
+sys.path.insert(0, ".")
+from paper_2111_05188_b200 import api, synth, configs, _lib
+
+w = configs.preset(sys.argv[1] if len(sys.argv) > 1 else "C3", T_data=20000)
+m = synth.make_market(w.n_stocks, w.T_data, w.dt, w.seed, n_feat=w.n_feat)
+cfg = api.config_from_workload(w)
+env = api.Env(cfg, torch.from_numpy(m.close).cuda(), torch.from_numpy(m.feat).cuda())
+aw = synth.make_actor(env.obs_dim, w.n_hidden, w.hidden, w.n_stocks, 1)
+params = api.pack_actor_params(cfg, [aw] * w.n_agents, w.n_hidden, w.hidden)
+actor = api.make_actor(w.n_hidden, w.hidden, params)
+T = 4
+tr = api.Trajectory.allocate(T, w.n_envs, w.n_stocks, env.k_pad)
+grid = 2 * ((w.n_envs // w.n_agents + 127) // 128) * w.n_agents
+buf = torch.zeros(grid * 32, dtype=torch.int64, device="cuda")
+_lib.load().pod_debug_actor_trace(env.h, C.c_void_p(buf.data_ptr()))
+env.reset(synth.tile_starts(env.n_tiles, w.T_data, min(w.horizon, w.T_data - 2), 1))
+for _ in range(3):
+    env.rollout(T, tr, actor=actor)
+torch.cuda.synchronize()
+b = buf.view(grid, 32).cpu().numpy().astype(np.int64)
+rel = b - b[:, :1]
+names = {1: "obs", 26: "end", 24: "head_acc", 25: "head_done"}
+for l in range(w.n_hidden + 1):
+    names[2 + 4 * l] = f"L{l}_mma_start"
+    names[3 + 4 * l] = f"L{l}_mma_issued"
+    if l < w.n_hidden:
+        names[4 + 4 * l] = f"L{l}_acc_ready"
+        names[5 + 4 * l] = f"L{l}_epi_done"
+for k in sorted(names):
+    col = rel[:, k]
+    print(f"{names[k]:16s} median {int(np.median(col)):8d}  min {int(col.min()):8d}  max {int(col.max()):8d}")
