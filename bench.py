@@ -388,20 +388,20 @@ def main():
             tf = flops / (a_ms / 1e3) / 1e12
             kern["actor_mlp"] = {"bound": "tensor", "achieved": tf, "peak": peaks["bf16_tflops_sustained"],
                                  "unit": "TFLOP/s", "frac": tf / peaks["bf16_tflops_sustained"],
-                                 "avg_launch_us": a_ms * 1e3, "launches_timed": acc["actor_n"],
+                                 "avg_launch_us_full_n": a_ms * 1e3, "launch_units_timed": acc["actor_n"],
                                  "share_of_step": a_ms * T * args.steps / ms}
         if acc["env_n"]:
             e_ms = acc["env_ms"] / acc["env_n"]
             by = N * env_bytes_per_env(n, w.n_feat, env.obs_dim)
             gbs = by / (e_ms / 1e3) / 1e9
             kern["env_step"] = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                "frac": gbs / peaks["hbm_gbs"], "avg_launch_us": e_ms * 1e3,
-                                "launches_timed": acc["env_n"], "share_of_step": e_ms * T * args.steps / ms}
+                                "frac": gbs / peaks["hbm_gbs"], "avg_launch_us_full_n": e_ms * 1e3,
+                                "launch_units_timed": acc["env_n"], "share_of_step": e_ms * T * args.steps / ms}
         if acc["gae_n"]:
             g_ms = acc["gae_ms"] / acc["gae_n"]
             gbs = gae_bytes(T, N) / (g_ms / 1e3) / 1e9
             kern["gae"] = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                           "frac": gbs / peaks["hbm_gbs"], "avg_launch_us": g_ms * 1e3, "launches_timed": acc["gae_n"],
+                           "frac": gbs / peaks["hbm_gbs"], "avg_launch_us_full_n": g_ms * 1e3, "launch_units_timed": acc["gae_n"],
                            "share_of_step": acc["gae_ms"] / ms}
         dom = max(kern, key=lambda k: kern[k]["share_of_step"]) if kern else None
         traffic = None

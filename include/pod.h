@@ -201,15 +201,19 @@ pod_status pod_rollout(pod_env_t* env, const pod_actor* actor, int32_t T, const 
                        void* stream);
 
 /* Per-kernel device timing (measurement support, not part of the method).
- * stride k > 0: subsequent pod_rollout calls record CUDA events on their
- * stream around the actor launch and the env-step launch of every k-th step
- * (inside the captured graph); 0 turns it off.  pod_env_profile_read
- * synchronises `stream` and returns the summed device milliseconds and the
- * number of bracketed launches of the most recent profiled rollout (zeros if
- * none since the last read), then forgets it. */
+ * stride k > 0: subsequent pod_rollout calls record CUDA events around the
+ * actor launches and the env-step launches of every k-th step, on the stream
+ * (graph branch) each launch runs on; 0 turns it off.  pod_env_profile_read
+ * synchronises `stream` and returns, for the most recent profiled rollout, the
+ * summed device milliseconds of the bracketed launches and their size in
+ * "units" (sum over bracketed launches of envs-in-launch / n_envs; a launch
+ * over all envs counts 1), then forgets it (zeros if none since the last read).
+ * Note: with env groups (pod_rollout runs 2 independent halves of the envs on
+ * separate graph branches so one half's env step overlaps the other's actor)
+ * the bracketed launches may overlap in time. */
 pod_status pod_env_profile(pod_env_t* env, int32_t stride);
-pod_status pod_env_profile_read(pod_env_t* env, double* actor_ms, int64_t* actor_launches, double* env_ms,
-                                int64_t* env_launches, void* stream);
+pod_status pod_env_profile_read(pod_env_t* env, double* actor_ms, double* actor_units, double* env_ms,
+                                double* env_units, void* stream);
 
 /* Diagnostics only: buf [dev] u64 [2 x tiles][32] receives clock64 stamps of the
  * actor kernel's phases (obs loaded, per-layer MMA issue / epilogue, head) at every

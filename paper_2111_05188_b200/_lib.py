@@ -83,7 +83,7 @@ def load():
         "pod_rollout": ([vp, P(Actor), i32, P(Traj), vp, i32, vp, vp], C.c_int),
         "pod_env_profile": ([vp, i32], C.c_int),
         "pod_debug_actor_trace": ([vp, vp], C.c_int),
-        "pod_env_profile_read": ([vp, P(d), P(i64), P(d), P(i64), vp], C.c_int),
+        "pod_env_profile_read": ([vp, P(d), P(d), P(d), P(d), vp], C.c_int),
         "pod_env_fitness": ([vp, vp, vp], C.c_int),
         "pod_env_read_state": ([vp, vp, vp, vp, vp, vp], C.c_int),
         "pod_env_check": ([vp, vp], C.c_int),

@@ -167,7 +167,7 @@ class Env:
 
     def profile_read(self, stream=None):
         am, em = C.c_double(0), C.c_double(0)
-        al, el = C.c_int64(0), C.c_int64(0)
+        al, el = C.c_double(0), C.c_double(0)
         check(load().pod_env_profile_read(self.h, C.byref(am), C.byref(al), C.byref(em), C.byref(el),
                                           _stream(stream)), "pod_env_profile_read")
         return am.value, al.value, em.value, el.value

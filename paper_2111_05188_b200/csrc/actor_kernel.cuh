@@ -63,7 +63,7 @@ struct ActorArgs {
     int32_t deterministic;
     int32_t t;               // step within the rollout
     int32_t obs_row0;        // row of obs[t][0] in the obs tensor map = t * N
-    int32_t pad_;
+    int32_t mtile0;          // first 128-env M-tile of this launch (env groups)
     uint64_t seed;
     int64_t env_offset;
     const uint64_t* step_base;   // device step counter of the handle
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t tslot_s = obs_b + 32u;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
-    const int mtile = blockIdx.x >> 1;
+    const int mtile = a.mtile0 + static_cast<int>(blockIdx.x >> 1);
     const int agent = mtile / a.tiles_per_agent;
     const int tile_in_agent = mtile % a.tiles_per_agent;
     const int env0 = agent * a.per_agent + tile_in_agent * 128;

@@ -51,7 +51,7 @@ struct EnvArgs {
     int32_t tma_ok;           // hold / aint tiles may be fetched with the 2-D tensor maps
     int32_t gen_noise;        // also draw the actor's N(0,1) noise for step *step_base + noise_t
     int32_t noise_t;
-    int32_t pad_;
+    int32_t tile0;            // first env tile of this launch (env groups)
     uint64_t seed;
     int64_t env_offset;
     const uint64_t* step_base;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    const int tile = blockIdx.x;
+    const int tile = a.tile0 + static_cast<int>(blockIdx.x);
     const int n = a.n;
     const int e_pad = env_e_pad(n);
     const EnvSmemLayout SL = env_smem_layout(n, a.k_pad);
@@ -348,9 +348,9 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
 
 // injected actions: a[i][e] = sgn(u) floor(|u| h_max + 1/2)  (R#6)
 __global__ void inject_map_kernel(const float* __restrict__ u, int N, int n, int h_max, int16_t* __restrict__ aint,
-                                  int16_t* __restrict__ dbg_aint) {
-    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= static_cast<int64_t>(N) * n) return;
+                                  int16_t* __restrict__ dbg_aint, int e0, int e1) {
+    const int64_t idx = static_cast<int64_t>(e0) * n + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<int64_t>(e1) * n) return;
     const int e = static_cast<int>(idx / n);
     const int i = static_cast<int>(idx % n);
     const float x = u[idx];

@@ -172,26 +172,33 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
 }
 
 // ------------------------------------------------------------ env handle
+#define POD_MAX_GROUPS 4
+
 struct GraphKey {
     int32_t T, deterministic, n_hidden, hidden, act, profile;
     const void* ptrs[12];
     size_t param_bytes;
 };
 
-// CUDA events recorded around every actor / env-step launch of one rollout
-// (profiling mode): ev[4t+0..1] bracket the actor at step t, ev[4t+2..3] the env step.
+// CUDA events recorded around the actor / env-step launches of every stride-th
+// step of one rollout (profiling mode): ev[4 (m G + g) + 0..1] bracket group g's
+// actor at marked step m, ev[4 (m G + g) + 2..3] its env step.
 struct ProfEvents {
     std::vector<cudaEvent_t> ev;
+    std::vector<double> frac;   // envs of group g / N
     int T = 0;
     int stride = 1;
     int n_marked = 0;
+    int groups = 1;
     bool injected = false;
-    pod_status create(int T_, int stride_, bool inj) {
+    pod_status create(int T_, int stride_, bool inj, int G, const std::vector<double>& fr) {
         T = T_;
         stride = stride_ < 1 ? 1 : stride_;
         n_marked = (T_ + stride - 1) / stride;
         injected = inj;
-        ev.resize(static_cast<size_t>(4) * n_marked);
+        groups = G;
+        frac = fr;
+        ev.resize(static_cast<size_t>(4) * n_marked * G);
         for (auto& x : ev)
             if (cudaEventCreate(&x) != cudaSuccess) return pod_fail(POD_ERR_CUDA, "cudaEventCreate failed");
         return POD_OK;
@@ -214,6 +221,12 @@ struct pod_env {
     pod_env_config cfg;
     pod_market market;
     int obs_dim, k_pad, n_out_pad, n_tiles, per_agent, env_tma_ok;
+    // env groups: independent slices of the envs whose actor / env-step chains run on
+    // separate graph branches, so one group's env step overlaps another's actor
+    int groups;
+    int g_m0[POD_MAX_GROUPS + 1];          // M-tile boundaries (128 envs)
+    cudaStream_t gstream[POD_MAX_GROUPS];
+    cudaEvent_t fork_ev, join_ev[POD_MAX_GROUPS];
     EnvMaps env_maps;
     // workspace carve
     int32_t* hold;
@@ -319,6 +332,17 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     e->step = reinterpret_cast<uint64_t*>(b + w.step);
     e->err = reinterpret_cast<uint32_t*>(b + w.err);
     e->use_clock = 0;
+    {
+        const int mt = (cfg->n_envs + 127) / 128;
+        int G = 1;   // per-CTA latency bound at C3: branches run in lockstep, so 1 by default
+        const char* gs = getenv("POD_GROUPS");
+        if (gs && atoi(gs) >= 1) G = atoi(gs);
+        if (G > POD_MAX_GROUPS) G = POD_MAX_GROUPS;
+        if (G > mt) G = mt;
+        if (e->per_agent % 128 != 0) G = 1;
+        e->groups = G;
+        for (int g = 0; g <= G; ++g) e->g_m0[g] = static_cast<int>(static_cast<int64_t>(g) * mt / G);
+    }
     e->profile = 0;
     e->last_prof = nullptr;
     e->trace = nullptr;
@@ -326,6 +350,11 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     e->use_graphs = !(ng && ng[0] == '1');
     cudaError_t ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_starts), sizeof(int32_t) * e->n_tiles);
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
+    for (int g = 0; g < POD_MAX_GROUPS && ce == cudaSuccess; ++g) {
+        ce = cudaStreamCreateWithFlags(&e->gstream[g], cudaStreamNonBlocking);
+        if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->join_ev[g], cudaEventDisableTiming);
+    }
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming);
     if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
@@ -370,6 +399,11 @@ extern "C" pod_status pod_env_destroy(pod_env_t* e) {
     }
     e->direct_prof.destroy();
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    for (int g = 0; g < POD_MAX_GROUPS; ++g) {
+        if (e->gstream[g]) cudaStreamDestroy(e->gstream[g]);
+        if (e->join_ev[g]) cudaEventDestroy(e->join_ev[g]);
+    }
+    if (e->fork_ev) cudaEventDestroy(e->fork_ev);
     if (e->h_starts) cudaFreeHost(e->h_starts);
     delete e;
     return POD_OK;
@@ -454,41 +488,48 @@ struct RolloutPlan {
     size_t actor_smem;
 };
 
-static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj,
-                                  double* fitness_out, cudaStream_t s, ProfEvents* prof) {
+// one group's chain: s_0, then T x {actor (or injected map), env step}
+static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj, cudaStream_t s,
+                          ProfEvents* prof, int g) {
+    const int N = e->cfg.n_envs, n = e->cfg.n_stocks;
+    const int m0 = e->g_m0[g], m1 = e->g_m0[g + 1];
+    const int e0 = e->groups == 1 ? 0 : m0 * 128;
+    const int e1 = e->groups == 1 ? N : (m1 * 128 < N ? m1 * 128 : N);
+    const int t0 = e0 / POD_ENV_TILE, t1 = (e1 + POD_ENV_TILE - 1) / POD_ENV_TILE;
     auto mark = [&](int t, int k) {
         // external event-record node when captured into the graph (timing-capable);
         // only every `stride`-th step is bracketed, to keep the timing overhead small
         if (prof && t % prof->stride == 0)
-            cudaEventRecordWithFlags(prof->ev[static_cast<size_t>(4 * (t / prof->stride) + k)], s,
+            cudaEventRecordWithFlags(prof->ev[static_cast<size_t>(4 * ((t / prof->stride) * prof->groups + g) + k)], s,
                                      cudaEventRecordExternal);
     };
-    const int N = e->cfg.n_envs, n = e->cfg.n_stocks;
-    // s_0 from the carried state
-    EnvArgs a0 = env_args(e, 1);
-    a0.obs_out = tr->obs;
     const int sampling = (!p.injected && !p.aa.deterministic) ? 1 : 0;
+    EnvArgs a0 = env_args(e, 1);
+    a0.tile0 = t0;
+    a0.obs_out = tr->obs;
     a0.gen_noise = sampling;          // noise for the actor launch of step 0
     a0.noise_t = 0;
-    env_step_kernel<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
+    env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
     for (int t = 0; t < T; ++t) {
         mark(t, 0);
         if (p.injected) {
-            const int64_t tot = static_cast<int64_t>(N) * n;
+            const int64_t tot = static_cast<int64_t>(e1 - e0) * n;
             inject_map_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(
                 inj + static_cast<int64_t>(t) * N * n, N, n, e->cfg.h_max, e->aint,
-                tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr);
+                tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr, e0, e1);
         } else {
             ActorArgs aa = p.aa;
             aa.t = t;
             aa.obs_row0 = t * N;
+            aa.mtile0 = m0;
             aa.act_out = tr->act + static_cast<int64_t>(t) * N * n;
             aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
             aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
             aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
             // one 2-CTA cluster per 128-env tile (column split of every layer)
             cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(static_cast<unsigned>(2 * e->cfg.n_agents * aa.tiles_per_agent));
+            const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
+            lc.gridDim = dim3(static_cast<unsigned>(2 * mtiles));
             lc.blockDim = dim3(ACT_THREADS);
             lc.dynamicSmemBytes = p.actor_smem;
             lc.stream = s;
@@ -504,6 +545,7 @@ static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const
         mark(t, 1);
         mark(t, 2);
         EnvArgs a = env_args(e, 0);
+        a.tile0 = t0;
         a.rew = tr->rew + static_cast<int64_t>(t) * N;
         a.done = tr->done + static_cast<int64_t>(t) * N;
         a.obs_out = tr->obs + static_cast<int64_t>(t + 1) * N * e->k_pad;
@@ -511,13 +553,44 @@ static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const
         a.dbg_cash = tr->dbg_cash ? tr->dbg_cash + static_cast<int64_t>(t) * N : nullptr;
         a.gen_noise = (sampling && t + 1 < T) ? 1 : 0;   // noise for the actor launch of step t+1
         a.noise_t = t + 1;
-        env_step_kernel<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+        env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
         mark(t, 3);
+    }
+}
+
+static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj,
+                                  double* fitness_out, cudaStream_t s, ProfEvents* prof) {
+    if (e->groups == 1) {
+        enqueue_group(e, p, T, tr, inj, s, prof, 0);
+    } else {
+        // fork: each env group's chain on its own stream (graph branch), then join
+        POD_CUDA(cudaEventRecord(e->fork_ev, s));
+        for (int g = 0; g < e->groups; ++g) {
+            POD_CUDA(cudaStreamWaitEvent(e->gstream[g], e->fork_ev, 0));
+            enqueue_group(e, p, T, tr, inj, e->gstream[g], prof, g);
+            POD_CUDA(cudaEventRecord(e->join_ev[g], e->gstream[g]));
+            POD_CUDA(cudaStreamWaitEvent(s, e->join_ev[g], 0));
+        }
     }
     if (!p.injected) bump_step_kernel<<<1, 1, 0, s>>>(e->step, static_cast<uint64_t>(T));
     if (fitness_out) fitness_kernel<<<e->cfg.n_agents, 1024, 0, s>>>(e->ep_ret, e->per_agent, fitness_out);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
+}
+
+static std::vector<double> group_fracs(const pod_env* e) {
+    std::vector<double> fr;
+    const int N = e->cfg.n_envs;
+    for (int g = 0; g < e->groups; ++g) {
+        if (e->groups == 1) {
+            fr.push_back(1.0);
+        } else {
+            const int e0 = e->g_m0[g] * 128;
+            const int e1 = e->g_m0[g + 1] * 128 < N ? e->g_m0[g + 1] * 128 : N;
+            fr.push_back(static_cast<double>(e1 - e0) / N);
+        }
+    }
+    return fr;
 }
 
 extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t T, const pod_traj* tr,
@@ -591,7 +664,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         ProfEvents* prof = nullptr;
         if (e->profile) {
             e->direct_prof.destroy();
-            pod_status st = e->direct_prof.create(T, e->profile, p.injected);
+            pod_status st = e->direct_prof.create(T, e->profile, p.injected, e->groups, group_fracs(e));
             if (st) return st;
             prof = &e->direct_prof;
         }
@@ -622,7 +695,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         ProfEvents* prof = nullptr;
         if (e->profile) {
             prof = new ProfEvents();
-            pod_status pst = prof->create(T, e->profile, p.injected);
+            pod_status pst = prof->create(T, e->profile, p.injected, e->groups, group_fracs(e));
             if (pst) {
                 prof->destroy();
                 delete prof;
@@ -674,26 +747,30 @@ extern "C" pod_status pod_env_profile(pod_env_t* e, int32_t enable) {
     return POD_OK;
 }
 
-extern "C" pod_status pod_env_profile_read(pod_env_t* e, double* actor_ms, int64_t* actor_launches, double* env_ms,
-                                           int64_t* env_launches, void* stream) {
-    if (!e || !actor_ms || !actor_launches || !env_ms || !env_launches) return pod_fail(POD_ERR_ARG, "NULL argument");
+extern "C" pod_status pod_env_profile_read(pod_env_t* e, double* actor_ms, double* actor_units, double* env_ms,
+                                           double* env_units, void* stream) {
+    if (!e || !actor_ms || !actor_units || !env_ms || !env_units) return pod_fail(POD_ERR_ARG, "NULL argument");
     *actor_ms = *env_ms = 0.0;
-    *actor_launches = *env_launches = 0;
+    *actor_units = *env_units = 0.0;
     ProfEvents* p = e->last_prof;
     if (!p) return POD_OK;
     POD_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
-    double a = 0.0, v = 0.0;
-    for (int t = 0; t < p->n_marked; ++t) {
-        float ms = 0.f;
-        POD_CUDA(cudaEventElapsedTime(&ms, p->ev[static_cast<size_t>(4 * t)], p->ev[static_cast<size_t>(4 * t + 1)]));
-        a += ms;
-        POD_CUDA(cudaEventElapsedTime(&ms, p->ev[static_cast<size_t>(4 * t + 2)], p->ev[static_cast<size_t>(4 * t + 3)]));
-        v += ms;
+    double a = 0.0, v = 0.0, u = 0.0;
+    for (int m = 0; m < p->n_marked; ++m) {
+        for (int g = 0; g < p->groups; ++g) {
+            const size_t b = static_cast<size_t>(4 * (m * p->groups + g));
+            float ms = 0.f;
+            POD_CUDA(cudaEventElapsedTime(&ms, p->ev[b], p->ev[b + 1]));
+            a += ms;
+            POD_CUDA(cudaEventElapsedTime(&ms, p->ev[b + 2], p->ev[b + 3]));
+            v += ms;
+            u += p->frac[static_cast<size_t>(g)];
+        }
     }
     *actor_ms = a;
     *env_ms = v;
-    *actor_launches = p->n_marked;
-    *env_launches = p->n_marked;
+    *actor_units = u;
+    *env_units = u;
     e->last_prof = nullptr;
     return POD_OK;
 }
