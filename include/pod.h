@@ -215,10 +215,12 @@ pod_status pod_env_profile(pod_env_t* env, int32_t stride);
 pod_status pod_env_profile_read(pod_env_t* env, double* actor_ms, double* actor_units, double* env_ms,
                                 double* env_units, void* stream);
 
-/* Diagnostics only: buf [dev] u64 [2 x tiles][32] receives clock64 stamps of the
- * actor kernel's phases (obs loaded, per-layer MMA issue / epilogue, head) at every
- * actor launch of subsequent rollouts; NULL turns it off.  Drops cached graphs. */
-pod_status pod_debug_actor_trace(pod_env_t* env, unsigned long long* buf);
+/* Diagnostics only: actor_buf [dev] u64 [2 x M-tiles][64] receives clock64 stamps of
+ * the actor kernel's phases (obs loaded, per-layer MMA issue / epilogue, head) and
+ * env_buf [dev] u64 [env tiles][8] those of the env-step kernel (start, inputs staged,
+ * sells done, buys done, ledger done, rows staged, end) at every launch of
+ * subsequent rollouts; NULL turns either off.  Drops cached graphs. */
+pod_status pod_debug_trace(pod_env_t* env, unsigned long long* actor_buf, unsigned long long* env_buf);
 
 /* Fitness J of the current state (same definition as pod_rollout's). */
 pod_status pod_env_fitness(pod_env_t* env, double* fitness_out, void* stream);

@@ -54,7 +54,7 @@ class Transfer(C.Structure):
 
 EXPORTS = ["pod_status_string", "pod_last_error", "pod_abi_version", "pod_actor_layout_get",
            "pod_env_workspace_size", "pod_env_create", "pod_env_destroy", "pod_env_reset", "pod_rollout",
-           "pod_env_profile", "pod_env_profile_read", "pod_debug_actor_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan",
+           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan",
            "pod_elite_transfers", "pod_comm_unique_id", "pod_comm_init", "pod_comm_destroy", "pod_select_elite"]
 
 _lib = None
@@ -82,7 +82,7 @@ def load():
         "pod_env_reset": ([vp, vp, vp, vp], C.c_int),
         "pod_rollout": ([vp, P(Actor), i32, P(Traj), vp, i32, vp, vp], C.c_int),
         "pod_env_profile": ([vp, i32], C.c_int),
-        "pod_debug_actor_trace": ([vp, vp], C.c_int),
+        "pod_debug_trace": ([vp, vp], C.c_int),
         "pod_env_profile_read": ([vp, P(d), P(d), P(d), P(d), vp], C.c_int),
         "pod_env_fitness": ([vp, vp, vp], C.c_int),
         "pod_env_read_state": ([vp, vp, vp, vp, vp, vp], C.c_int),

@@ -64,6 +64,7 @@ struct ActorArgs {
     int32_t t;               // step within the rollout
     int32_t obs_row0;        // row of obs[t][0] in the obs tensor map = t * N
     int32_t mtile0;          // first 128-env M-tile of this launch (env groups)
+    int32_t mc;              // 1: 4-CTA clusters (2 M-tiles) share weight tiles by TMA multicast
     uint64_t seed;
     int64_t env_offset;
     const uint64_t* step_base;   // device step counter of the handle
@@ -95,7 +96,7 @@ __host__ __device__ inline int actor_bn(int half) { return half < ACT_BN ? half 
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
     return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_BN * 128 +
-           ACT_BIAS_FLOATS * 4 + 4 * 128 * 4 + 256;
+           ACT_BIAS_FLOATS * 4 + 4 * 128 * 4 + 256;   // + barriers
 }
 
 __device__ __forceinline__ float act_fn(float x, int act) { return act == 0 ? fmaxf(x, 0.0f) : tanhf(x); }
@@ -108,8 +109,12 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();            // 0 / 1 within the pair
-    const uint32_t peer = rank ^ 1u;
+    const uint32_t cr = cluster_ctarank();              // rank in the cluster (2 or 4 CTAs)
+    const uint32_t rank = cr & 1u;                      // column half of this CTA
+    const uint32_t peer = cr ^ 1u;                      // same M-tile, other column half
+    const uint32_t partner = cr ^ 2u;                   // other M-tile, same column half (a.mc)
+    const uint16_t pair_mask = static_cast<uint16_t>((1u << cr) | (1u << peer));
+    const uint16_t share_mask = static_cast<uint16_t>((1u << cr) | (1u << partner));
     const int ka = (a.k_pad > a.hidden ? a.k_pad : a.hidden) / 64;   // activation atoms
     const uint32_t act_s = base_u32;                                  // ka * 16 KB
     const uint32_t ring_s = act_s + ka * 16384u;
@@ -122,9 +127,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t empty_b = bar_s + 8u * ACT_STAGES;                // [STAGES]
     const uint32_t obs_b = bar_s + 16u * ACT_STAGES;
     const uint32_t accum_b = obs_b + 8u;
-    const uint32_t ownrdy_b = obs_b + 16u;     // this CTA's half of h_{l+1} written (256 arrivals)
-    const uint32_t peerrdy_b = obs_b + 24u;    // the peer's half of h_{l+1} landed (expect_tx)
-    const uint32_t tslot_s = obs_b + 32u;
+    const uint32_t ownrdy_b = obs_b + 16u;     // [4] atom j of this CTA's half of h_{l+1} written (256 arrivals)
+    const uint32_t peerrdy_b = obs_b + 48u;    // [4] atom j of the peer's half landed (expect_tx)
+    const uint32_t tslot_s = obs_b + 80u;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
     const int mtile = a.mtile0 + static_cast<int>(blockIdx.x >> 1);
@@ -136,22 +141,24 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
 
     const int hid_half = a.hidden / 2;
     const int head_half = a.n_out_pad / 2;
+    // TMEM: two accumulator buffers (layer l uses buffer l & 1), so layer l+1's MMAs can
+    // start while the epilogue is still reading layer l's accumulator
+    const uint32_t tbuf = static_cast<uint32_t>(hid_half > head_half ? hid_half : head_half);
     uint32_t tcols = 32;
-    {
-        const int need = hid_half > head_half ? hid_half : head_half;
-        while (tcols < static_cast<uint32_t>(need)) tcols <<= 1;
-    }
+    while (tcols < 2 * tbuf) tcols <<= 1;
 
     if (warp == 0) {
         if (lane == 0) {
             for (int s = 0; s < ACT_STAGES; ++s) {
                 mbar_init(full_b + 8u * s, 1);
-                mbar_init(empty_b + 8u * s, 1);
+                mbar_init(empty_b + 8u * s, a.mc ? 2 : 1);   // both consumers of a shared tile
             }
             mbar_init(obs_b, 1);
             mbar_init(accum_b, 2);        // one multicast commit from each CTA of the pair
-            mbar_init(ownrdy_b, 256);     // the 256 epilogue threads
-            mbar_init(peerrdy_b, 1);      // one expect_tx arrival + the peer's bulk-copy bytes
+            for (int j = 0; j < 4; ++j) {
+                mbar_init(ownrdy_b + 8u * j, 256);   // the 256 epilogue threads
+                mbar_init(peerrdy_b + 8u * j, 1);    // the MMA thread's expect_tx + the peer's bytes
+            }
             fence_mbar_init();
             prefetch_tmap(&maps.obs);
             for (int l = 0; l < a.n_layers; ++l) prefetch_tmap(&maps.w[l]);
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     cluster_sync_all();          // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 32 : nullptr;
+    unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 64 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = clock64();
 
     if (warp == 0) {
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
             for (int kb = 0; kb < kb0; ++kb)
                 tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, a.obs_row0 + env0, obs_b);
-            int stage = 0;
+            int stage = 0, seq = 0;
             uint32_t phase = 0;
             for (int l = 0; l < a.n_layers; ++l) {
                 const int K = l == 0 ? a.k_pad : a.hidden;
@@ -186,8 +193,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         const int kb = (j + kb0) % KB;
                         mbar_wait(empty_b + 8u * stage, phase ^ 1u);
                         mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * 128u);
-                        tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * 64,
-                                    static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage);
+                        if (!a.mc) {
+                            tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * 64,
+                                        static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage);
+                        } else if ((seq & 1) == static_cast<int>(cr >> 1)) {
+                            // alternate tiles: this CTA fetches it for itself and its partner
+                            tma_load_3d_mc(ring_s + stage * stage_bytes, &maps.w[l], kb * 64,
+                                           static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage, share_mask);
+                        }
+                        if (tr && seq < 16) tr[48 + seq] = clock64();
+                        ++seq;
                         if (++stage == ACT_STAGES) {
                             stage = 0;
                             phase ^= 1u;
@@ -205,36 +220,42 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             if (tr) tr[1] = clock64();
             int stage = 0;
             uint32_t phase = 0;
+            const int na = a.hidden / 128;           // activation atoms (64 cols) per CTA half
             for (int l = 0; l < a.n_layers; ++l) {
-                if (l > 0) {   // own half of h_l is local: start on it, the peer's half may still be in flight
-                    mbar_wait(ownrdy_b, static_cast<uint32_t>(l - 1) & 1u);
-                    tc_fence_after();
-                }
                 if (tr) tr[2 + 4 * l] = clock64();
                 const int K = l == 0 ? a.k_pad : a.hidden;
                 const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
                 const int bn = actor_bn(half);
                 const uint32_t idesc = idesc_bf16_f32(128, static_cast<uint32_t>(bn));
                 const int KB = K / 64;
-                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);
-                bool peer_seen = l == 0;
+                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * na;   // own atoms of h_l first
+                const uint32_t par = static_cast<uint32_t>(l - 1) & 1u;
                 for (int c = 0; c < half / bn; ++c) {
                     for (int j = 0; j < KB; ++j) {
                         const int kb = (j + kb0) % KB;
-                        if (!peer_seen && j == KB / 2) {
-                            mbar_wait(peerrdy_b, static_cast<uint32_t>(l - 1) & 1u);
+                        if (l > 0 && c == 0) {
+                            // h_l atom by atom: own atoms as the epilogue finishes them, then the
+                            // peer's atoms as its bulk copies land
+                            if (j < na) {
+                                mbar_wait(ownrdy_b + 8u * j, par);
+                            } else {
+                                mbar_arrive_expect_tx(peerrdy_b + 8u * (j - na), 16384u);
+                                mbar_wait(peerrdy_b + 8u * (j - na), par);
+                            }
                             tc_fence_after();
-                            peer_seen = true;
                         }
                         mbar_wait(full_b + 8u * stage, phase);
                         tc_fence_after();
+                        if (tr && l == 0 && c * KB + j < 16) tr[32 + c * KB + j] = clock64();
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const uint64_t ad = sw128_desc(act_s + kb * 16384u + k * 32u);
                             const uint64_t bd = sw128_desc(ring_s + stage * stage_bytes + k * 32u);
-                            mma_bf16(tmem + static_cast<uint32_t>(c * bn), ad, bd, idesc, (j | k) != 0);
+                            mma_bf16(tmem + (static_cast<uint32_t>(l) & 1u) * tbuf + static_cast<uint32_t>(c * bn), ad, bd,
+                                     idesc, (j | k) != 0);
                         }
-                        mma_commit(empty_b + 8u * stage);
+                        if (a.mc) mma_commit_mc(empty_b + 8u * stage, share_mask);   // free it in both CTAs
+                        else mma_commit(empty_b + 8u * stage);
                         if (++stage == ACT_STAGES) {
                             stage = 0;
                             phase ^= 1u;
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     }
                 }
                 if (tr) tr[3 + 4 * l] = clock64();
-                mma_commit_mc(accum_b, 0x3);
+                mma_commit_mc(accum_b, pair_mask);
             }
         }
         __syncwarp();
@@ -287,50 +308,41 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             mbar_wait(accum_b, static_cast<uint32_t>(l) & 1u);   // both CTAs done reading h_l
             tc_fence_after();
             if (tr && etid == 0) tr[4 + 4 * l] = clock64();
-            const int quarter = hid_half / 2;                     // columns of this warp
-            for (int cc = 0; cc < quarter / 32; cc += 2) {
-                const int npair = quarter / 32 - cc >= 2 ? 2 : 1;
-                uint32_t v[2][32];
-                tmem_ld32(trow + static_cast<uint32_t>(hh * quarter + cc * 32), v[0]);
-                if (npair == 2) tmem_ld32(trow + static_cast<uint32_t>(hh * quarter + cc * 32 + 32), v[1]);
+            // h_{l+1} atom by atom (64 columns = 8 warps x 32 columns x 128 rows), so the next
+            // layer's MMAs and the DSMEM copy of each atom start as soon as it is written
+            const int na = hid_half / 64;
+            for (int j = 0; j < na; ++j) {
+                const int tc = j * 64 + hh * 32;                      // TMEM column (local)
+                uint32_t v[32];
+                tmem_ld32(trow + (static_cast<uint32_t>(l) & 1u) * tbuf + static_cast<uint32_t>(tc), v);
                 tmem_ld_wait();
+                const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
+                uint32_t pk[16];
 #pragma unroll
-                for (int pp = 0; pp < 2; ++pp) {
-                    if (pp < npair) {
-                        const int tc = hh * quarter + (cc + pp) * 32;    // TMEM column (local)
-                        const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
-                        uint32_t pk[16];
+                for (int q = 0; q < 8; ++q) {
+                    const float4 b = b4[q];
+                    pk[2 * q] = pack_bf16x2(act_fn(__uint_as_float(v[4 * q]) + b.x, a.act),
+                                            act_fn(__uint_as_float(v[4 * q + 1]) + b.y, a.act));
+                    pk[2 * q + 1] = pack_bf16x2(act_fn(__uint_as_float(v[4 * q + 2]) + b.z, a.act),
+                                                act_fn(__uint_as_float(v[4 * q + 3]) + b.w, a.act));
+                }
+                const int atom_g = static_cast<int>(rank) * na + j;           // global atom of h_{l+1}
+                const uint32_t atom = act_s + static_cast<uint32_t>(atom_g) * 16384u;
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 b = b4[j];
-                            pk[2 * j] = pack_bf16x2(act_fn(__uint_as_float(v[pp][4 * j]) + b.x, a.act),
-                                                    act_fn(__uint_as_float(v[pp][4 * j + 1]) + b.y, a.act));
-                            pk[2 * j + 1] = pack_bf16x2(act_fn(__uint_as_float(v[pp][4 * j + 2]) + b.z, a.act),
-                                                        act_fn(__uint_as_float(v[pp][4 * j + 3]) + b.w, a.act));
-                        }
-                        const int col = static_cast<int>(rank) * hid_half + tc;   // global column of h_{l+1}
-                        const uint32_t atom = act_s + static_cast<uint32_t>(col / 64) * 16384u;
-                        const uint32_t c0 = static_cast<uint32_t>((col % 64) / 8);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            st_shared_v4(atom + sw128_offset(static_cast<uint32_t>(r), c0 + q), pk[4 * q],
-                                         pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                    }
+                for (int q = 0; q < 4; ++q)
+                    st_shared_v4(atom + sw128_offset(static_cast<uint32_t>(r), static_cast<uint32_t>(hh * 4 + q)),
+                                 pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(ownrdy_b + 8u * j);
+                if (etid == 0) {
+                    // the whole atom is written: ship it to the same offset in the peer
+                    mbar_wait(ownrdy_b + 8u * j, static_cast<uint32_t>(l) & 1u);
+                    bulk_s2peer(mapa_shared(atom, peer), atom, 16384u, mapa_shared(peerrdy_b + 8u * j, peer));
                 }
             }
             boff += hid_half;
-            fence_proxy_async_smem();
-            tc_fence_before();
-            named_bar_sync(1, 256);
-            const uint32_t bytes = static_cast<uint32_t>(hid_half / 64) * 16384u;
             if (tr && etid == 0) tr[5 + 4 * l] = clock64();
-            if (etid == 0) {
-                // this CTA's new atoms -> the same offsets in the peer, completing on its barrier
-                const uint32_t src = act_s + rank * bytes;
-                bulk_s2peer(mapa_shared(src, peer), src, bytes, mapa_shared(peerrdy_b, peer));
-                mbar_arrive_expect_tx(peerrdy_b, bytes);       // the peer's half arriving here
-            }
-            mbar_arrive(ownrdy_b);
         }
         // ----- head: this CTA's tickers [rank*head_half, ...), this warp's quarter of them
         const int L = a.n_layers - 1;
@@ -351,7 +363,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             const int i0 = static_cast<int>(rank) * head_half + tc;  // global ticker
             uint32_t v[8];
             __syncwarp();
-            tmem_ld8(trow + static_cast<uint32_t>(tc), v);
+            tmem_ld8(trow + (static_cast<uint32_t>(L) & 1u) * tbuf + static_cast<uint32_t>(tc), v);
             tmem_ld_wait();
             if (valid && i0 < a.n) {
                 float raw[8], mu[8];
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         if (bad && valid) atomicOr(a.err, 1u);
         if (tr && etid == 0) tr[25] = clock64();
         // log-prob partial of (rank, hh) for row r -> CTA 0's logp_s[rank*2 + hh][r]
-        st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), 0), logp);
+        st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), cr & ~1u), logp);
     }
 
     tc_fence_before();

@@ -56,6 +56,7 @@ struct EnvArgs {
     int64_t env_offset;
     const uint64_t* step_base;
     float* znoise;            // [n][N] noise output
+    unsigned long long* trace;   // diagnostics: [n_tiles][8] clock64 stamps, or null
     int64_t T_data;
     double C0;
     double cost;
@@ -86,7 +87,7 @@ struct EnvMaps {
 };
 
 // shared memory of one block (one tile), TMA destinations 128-B aligned:
-//   [hold_s n*32 i32 | aint_s n*32 i16 (pad 128) | unit, p_t, p_1 n f64 each (pad 16) |
+//   [hold_s n*32 i32 | aint_s n*32 i16 (pad 128) | unit, p_t, p_1, 1/unit, unit_lo n f64 each (pad 16) |
 //    p_t, p_1, p_0 n f32 (pad 16) | tmpl k_pad bf16 | stg 32 x e_pad bf16 | mbar]
 __host__ __device__ inline int env_e_pad(int n) { return (1 + n + 7) / 8 * 8; }
 struct EnvSmemLayout {
@@ -96,7 +97,7 @@ __host__ __device__ inline EnvSmemLayout env_smem_layout(int n, int k_pad) {
     EnvSmemLayout L;
     L.aint = n * 128;
     L.unit = L.aint + (n * 64 + 127) / 128 * 128;
-    L.p = L.unit + (3 * n * 8 + 15) / 16 * 16;
+    L.p = L.unit + (5 * n * 8 + 15) / 16 * 16;
     L.tmpl = L.p + (3 * n * 4 + 15) / 16 * 16;
     L.stg = L.tmpl + k_pad * 2;
     L.bar = L.stg + 32 * env_e_pad(n) * 2;
@@ -115,6 +116,8 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const int tile = a.tile0 + static_cast<int>(blockIdx.x);
+    unsigned long long* trc = (a.trace && a.mode == 0) ? a.trace + tile * 8 : nullptr;
+    if (trc && threadIdx.x == 0) trc[0] = clock64();
     const int n = a.n;
     const int e_pad = env_e_pad(n);
     const EnvSmemLayout SL = env_smem_layout(n, a.k_pad);
@@ -123,6 +126,8 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     double* unit_s = reinterpret_cast<double*>(env_smem + SL.unit);   // [n] p_t (1 + c)
     double* p_t64 = unit_s + n;                                           // [n] p_t as float64
     double* p_164 = unit_s + 2 * n;                                       // [n] p_{t+1} as float64
+    double* rcp_s = unit_s + 3 * n;                                       // [n] fl(1 / unit)
+    double* unit_lo = unit_s + 4 * n;                                     // [n] fl(unit (1 - 2^-50))
     float* p_t = reinterpret_cast<float*>(env_smem + SL.p);
     float* p_1 = p_t + n;
     float* p_0 = p_1 + n;
@@ -199,6 +204,8 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     const double opc = __dadd_rn(1.0, a.cost);
     for (int i = tid; i < n; i += ENV_THREADS) {
         unit_s[i] = __dmul_rn(static_cast<double>(p_t[i]), opc);
+        rcp_s[i] = __ddiv_rn(1.0, unit_s[i]);
+        unit_lo[i] = __dmul_rn(unit_s[i], 0.99999999999999911182158029987);   // 1 - 2^-50
         p_t64[i] = static_cast<double>(p_t[i]);
         p_164[i] = static_cast<double>(p_1[i]);
     }
@@ -213,6 +220,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     }
     if (tma) mbar_wait(bar, 0);
     __syncthreads();
+    if (trc && threadIdx.x == 0) trc[1] = clock64();
 
     // ---- 4. the float64 ledger, warp 0, lane = env, in exactly the order of
     //         Eqs. 3-4 under R#3/R#4 (sells, then greedy buys, tickers ascending)
@@ -228,41 +236,55 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             const double omc = __dadd_rn(1.0, -a.cost);
             // selling set (Eq. 3 "+ (p^S)^T k^S"), tickers ascending.  Branch-free: a
             // non-sell adds +0.0, which leaves the (never negative-zero) cash unchanged.
-#pragma unroll 4
+            // Only cash is carried: the post-sell holdings are recomputed in the buy pass.
+#pragma unroll 8
             for (int i = 0; i < n; ++i) {
                 const int ai = aint_s[i * 32 + lane];
                 const int h = hold_s[i * 32 + lane];
                 const int q = ai < 0 ? min(h, -ai) : 0;
-                hold_s[i * 32 + lane] = h - q;
                 cash = __dadd_rn(cash, __dmul_rn(__dmul_rn(p_t64[i], static_cast<double>(q)), omc));
             }
+            if (trc && lane == 0) trc[2] = clock64();
             // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending, then revalue at p_{t+1}.
-            // Exact shortcut: if fl(fl((a+1) unit) (1 + 2^-49)) <= b then the exact (a+1) unit < b,
-            // so floor(b / unit) >= a + 1 and the oracle's clipped quantity is a; the cost is
-            // then fl(a unit), which does not depend on b.  Only cash-limited buys divide.
+            // The oracle computes qmax = floor(fl(b / unit)) (minus one if fl(qmax unit) > b) and
+            // q = max(0, min(a, qmax)).  Exact shortcuts keep the IEEE division off the chain:
+            //  (i)  fl(fl((a+1) unit)(1 + 2^-49)) <= b  =>  exact b/unit > a+1, so q = a;
+            //  (ii) b < fl(unit (1 - 2^-50))            =>  exact b/unit < 1 - 2^-52, so q = 0;
+            //  (iii) y = fl(b fl(1/unit)) is within b/unit (1 +- 2^-51); if y is at least
+            //       y 2^-49 away from both neighbouring integers, floor(fl(b/unit)) = floor(y).
+            // Otherwise (b/unit within ~2^-49 of an integer) the IEEE quotient is used (rare).
+            // Every candidate is computed and selected, so the loop has no divergent branch
+            // except that rare fallback.
             double ph = 0.0;
 #pragma unroll 4
             for (int i = 0; i < n; ++i) {
                 const int ai = aint_s[i * 32 + lane];
                 int h = hold_s[i * 32 + lane];
+                if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
                 const double unit = unit_s[i];
                 const int ap = ai > 0 ? ai : 0;
-                const double need = ai > 0 ? __dmul_rn(__dmul_rn(static_cast<double>(ap + 1), unit), 1.0000000000000017763568394002504646778106689453125) : 0.0;
-                double cost = __dmul_rn(static_cast<double>(ap), unit);
-                int q = ap;
-                if (need > cash) {   // cash-limited: the oracle's floor + post-check
-                    double qmax = floor(__ddiv_rn(cash, unit));
-                    if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
-                    double qd = static_cast<double>(ai) < qmax ? static_cast<double>(ai) : qmax;
-                    qd = qd < 0.0 ? 0.0 : qd;
-                    q = static_cast<int>(qd);
-                    cost = __dmul_rn(qd, unit);
-                }
+                const double need = __dmul_rn(__dmul_rn(static_cast<double>(ap + 1), unit),
+                                              1.0000000000000017763568394002504646778106689453125);
+                const double cost_a = __dmul_rn(static_cast<double>(ap), unit);
+                const bool fast = ai <= 0 || need <= cash;         // (i), or nothing to buy
+                const bool unaff = cash < unit_lo[i];              // (ii)
+                const double y = __dmul_rn(cash, rcp_s[i]);
+                double qmax = floor(y);
+                const double fr = __dadd_rn(y, -qmax);
+                const double tol = __dmul_rn(y, 1.7763568394002504646778106689453125e-15);   // 2^-49
+                if (!fast && !unaff && !(fr >= tol && __dadd_rn(1.0, -fr) >= tol))
+                    qmax = floor(__ddiv_rn(cash, unit));           // (iii) failed: IEEE quotient
+                if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
+                double qd = static_cast<double>(ai) < qmax ? static_cast<double>(ai) : qmax;
+                qd = qd < 0.0 ? 0.0 : qd;
+                const int q = fast ? ap : (unaff ? 0 : static_cast<int>(qd));
+                const double cost = fast ? cost_a : (unaff ? 0.0 : __dmul_rn(qd, unit));
                 h += q;
                 cash = __dadd_rn(cash, -cost);
                 hold_s[i * 32 + lane] = h;
                 ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
             }
+            if (trc && lane == 0) trc[3] = clock64();
             const double v1 = __dadd_rn(cash, ph);
             const double r = __dmul_rn(a.scale, __dadd_rn(v1, -v0));
             double disc = __dadd_rn(disc0, __dmul_rn(gpow, r));
@@ -312,11 +334,13 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
         a.tile_gpow[tile] = 1.0;
     }
     __syncthreads();
+    if (trc && threadIdx.x == 0) trc[4] = clock64();
     // ---- 5. holdings out (coalesced rows) and the per-env part of s_{t+1}, 4 warps
     {
         const float inv_c0 = static_cast<float>(1.0 / a.C0);
         const float* p_obs = stepping ? p_1 : p_t;
         uint16_t* my = stg + lane * e_pad;
+#pragma unroll 5
         for (int i = warp; i < n; i += 4) {
             const int h = a.mode == 2 ? 0 : hold_s[i * 32 + lane];
             if (active) {
@@ -331,10 +355,12 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
         }
     }
     __syncthreads();
+    if (trc && threadIdx.x == 0) trc[5] = clock64();
     // ---- 6. write s_{t+1}: env rows spread over the 4 warps, 16-B chunks (512 B per instruction)
     if (a.obs_out) {
         const int chunks = a.k_pad / 8;
         const int rows = min(32, a.N - tile * 32);
+#pragma unroll 4
         for (int row = warp; row < rows; row += 4) {
             uint4* dst = reinterpret_cast<uint4*>(a.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
             for (int c = lane; c < chunks; c += 32) {
@@ -344,6 +370,8 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             }
         }
     }
+    __syncthreads();
+    if (trc && threadIdx.x == 0) trc[6] = clock64();
 }
 
 // injected actions: a[i][e] = sgn(u) floor(|u| h_max + 1/2)  (R#6)

@@ -12,10 +12,14 @@
 // lane with cp.async.bulk (TMA engine, completion on an mbarrier with
 // expect_tx), so STAGES x L x 288 B per warp are in flight while the lanes
 // run the recurrence out of shared memory.  Outputs are written with
-// coalesced 128-B row stores.  Ragged or misaligned column groups use the
-// plain-load path (same arithmetic, same order).
+// coalesced 128-B row stores.  Each chunk arrives as three 2-D TMA boxes
+// ({32 envs x 32 steps} of r, V, d) issued by one lane (rows before t = 0 and
+// columns past N are zero-filled by the TMA unit); misaligned inputs
+// (N % 16 != 0) use the plain-load path (same arithmetic, same order).
 #pragma once
 #include <cstdint>
+
+#include <cuda.h>
 
 #include "ptx.cuh"
 
@@ -25,7 +29,7 @@ constexpr int GAE_L = 32;        // time rows per chunk
 constexpr int GAE_STAGES = 4;    // chunks in flight per warp
 constexpr int GAE_WARPS = 2;     // warps per block
 
-struct GaeStage {
+struct __align__(128) GaeStage {
     float r[GAE_L][32];
     float v[GAE_L][32];
     uint8_t d[GAE_L][32];
@@ -42,10 +46,14 @@ __device__ __forceinline__ void gae_row(float r, float v, uint8_t d, float gamma
     v_next = v;
 }
 
+struct GaeMaps {
+    CUtensorMap r, v, d;   // 2-D [T][N], box {32, 32}
+};
+
 __global__ void __launch_bounds__(32 * GAE_WARPS)
-    gae_kernel(const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
-               const float* __restrict__ boot, int T, int N, float gamma, float lambda, float* __restrict__ adv,
-               float* __restrict__ ret, int use_bulk) {
+    gae_kernel(const __grid_constant__ GaeMaps maps, const float* __restrict__ rew, const float* __restrict__ val,
+               const uint8_t* __restrict__ done, const float* __restrict__ boot, int T, int N, float gamma,
+               float lambda, float* __restrict__ adv, float* __restrict__ ret, int use_bulk) {
     extern __shared__ __align__(128) uint8_t gsm[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -59,7 +67,7 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
     float a_next = 0.0f;
     const int nchunks = (T + GAE_L - 1) / GAE_L;
 
-    const bool bulk = use_bulk && (e0 + 32 <= N);
+    const bool bulk = use_bulk != 0;
     if (!bulk) {
         for (int t = T - 1; t >= 0; --t) {
             if (active) {
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
         return;
     }
 
-    GaeStage* st = reinterpret_cast<GaeStage*>(gsm + warp * (GAE_STAGES * sizeof(GaeStage) + 64));
+    GaeStage* st = reinterpret_cast<GaeStage*>(gsm + warp * (GAE_STAGES * sizeof(GaeStage) + 128));
     const uint32_t bars = smem_u32(reinterpret_cast<uint8_t*>(st) + GAE_STAGES * sizeof(GaeStage));
     if (lane == 0) {
         for (int s = 0; s < GAE_STAGES; ++s) mbar_init(bars + 8u * s, 1);
@@ -78,22 +86,16 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
     }
     __syncwarp();
 
-    // chunk j covers t in [T - (j+1) L, T - j L) clipped at 0 (processed newest first)
+    // chunk j covers rows [T - (j+1) L, T - j L) (rows < 0 arrive zero-filled; processed newest first)
     auto issue = [&](int j) {
         const int s = j % GAE_STAGES;
         const int t_hi = T - j * GAE_L;            // exclusive
-        const int t_lo = t_hi - GAE_L > 0 ? t_hi - GAE_L : 0;
-        const int rows = t_hi - t_lo;
         const uint32_t bar = bars + 8u * s;
-        if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows) * (128u + 128u + 32u));
-        __syncwarp();
-        if (lane < rows) {
-            const int t = t_lo + lane;
-            const int row = GAE_L - rows + lane;   // chunk rows are bottom-aligned
-            const int64_t off = static_cast<int64_t>(t) * N + e0;
-            bulk_g2s(smem_u32(&st[s].r[row][0]), rew + off, 128u, bar);
-            bulk_g2s(smem_u32(&st[s].v[row][0]), val + off, 128u, bar);
-            bulk_g2s(smem_u32(&st[s].d[row][0]), done + off, 32u, bar);
+        if (lane == 0) {
+            mbar_arrive_expect_tx(bar, GAE_L * (128u + 128u + 32u));
+            tma_load_2d(smem_u32(&st[s].r[0][0]), &maps.r, e0, t_hi - GAE_L, bar);
+            tma_load_2d(smem_u32(&st[s].v[0][0]), &maps.v, e0, t_hi - GAE_L, bar);
+            tma_load_2d(smem_u32(&st[s].d[0][0]), &maps.d, e0, t_hi - GAE_L, bar);
         }
     };
 
@@ -108,7 +110,12 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
         for (int q = GAE_L - 1; q >= GAE_L - rows; --q) {
             const int t = t_lo + (q - (GAE_L - rows));
             const int64_t i = static_cast<int64_t>(t) * N + e;
-            gae_row(st[s].r[q][lane], st[s].v[q][lane], st[s].d[q][lane], gamma, gl, v_next, a_next, adv + i, ret + i);
+            float A = 0.f, R = 0.f;
+            gae_row(st[s].r[q][lane], st[s].v[q][lane], st[s].d[q][lane], gamma, gl, v_next, a_next, &A, &R);
+            if (active) {
+                adv[i] = A;
+                ret[i] = R;
+            }
         }
         __syncwarp();
         fence_proxy_async_smem();   // order this stage's generic reads before the async refill
@@ -116,6 +123,6 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
     }
 }
 
-inline size_t gae_smem_bytes() { return GAE_WARPS * (GAE_STAGES * sizeof(GaeStage) + 64); }
+inline size_t gae_smem_bytes() { return GAE_WARPS * (GAE_STAGES * sizeof(GaeStage) + 128); }
 
 }  // namespace pod

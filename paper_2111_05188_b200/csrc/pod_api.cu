@@ -220,7 +220,7 @@ struct GraphEntry {
 struct pod_env {
     pod_env_config cfg;
     pod_market market;
-    int obs_dim, k_pad, n_out_pad, n_tiles, per_agent, env_tma_ok;
+    int obs_dim, k_pad, n_out_pad, n_tiles, per_agent, env_tma_ok, mc_ok;
     // env groups: independent slices of the envs whose actor / env-step chains run on
     // separate graph branches, so one group's env step overlaps another's actor
     int groups;
@@ -243,6 +243,7 @@ struct pod_env {
     bool use_graphs;
     int profile;                // 0 = off, k = bracket every k-th step
     unsigned long long* trace;  // diagnostics: actor clock64 stamps of the last launch
+    unsigned long long* env_trace;
     ProfEvents* last_prof;      // events of the most recent profiled rollout
     ProfEvents direct_prof;     // events for non-graph profiled rollouts
 };
@@ -341,11 +342,16 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         if (G > mt) G = mt;
         if (e->per_agent % 128 != 0) G = 1;
         e->groups = G;
+        // weight-tile multicast across 2 M-tiles: measured no faster (the fills are limited by
+        // shared-memory bandwidth under SS-mode MMAs, not by L2), so opt-in only
+        const char* mcs = getenv("POD_MULTICAST");
+        e->mc_ok = (e->per_agent % 256 == 0 && mcs && mcs[0] == '1') ? 1 : 0;
         for (int g = 0; g <= G; ++g) e->g_m0[g] = static_cast<int>(static_cast<int64_t>(g) * mt / G);
     }
     e->profile = 0;
     e->last_prof = nullptr;
     e->trace = nullptr;
+    e->env_trace = nullptr;
     const char* ng = getenv("POD_NO_GRAPH");
     e->use_graphs = !(ng && ng[0] == '1');
     cudaError_t ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_starts), sizeof(int32_t) * e->n_tiles);
@@ -441,6 +447,7 @@ static EnvArgs env_args(const pod_env* e, int mode) {
     a.env_offset = e->cfg.env_offset;
     a.step_base = e->step;
     a.znoise = e->znoise;
+    a.trace = e->env_trace;
     return a;
 }
 
@@ -529,13 +536,16 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             // one 2-CTA cluster per 128-env tile (column split of every layer)
             cudaLaunchConfig_t lc{};
             const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
+            // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
+            // every agent has an even number of full M-tiles and so does this launch
+            aa.mc = (e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
             lc.gridDim = dim3(static_cast<unsigned>(2 * mtiles));
             lc.blockDim = dim3(ACT_THREADS);
             lc.dynamicSmemBytes = p.actor_smem;
             lc.stream = s;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.x = aa.mc ? 4 : 2;
             at[0].val.clusterDim.y = 1;
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
@@ -731,9 +741,10 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
     return POD_OK;
 }
 
-extern "C" pod_status pod_debug_actor_trace(pod_env_t* e, unsigned long long* buf) {
+extern "C" pod_status pod_debug_trace(pod_env_t* e, unsigned long long* actor_buf, unsigned long long* env_buf) {
     if (!e) return pod_fail(POD_ERR_ARG, "env is NULL");
-    e->trace = buf;
+    e->trace = actor_buf;
+    e->env_trace = env_buf;
     for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
     e->graphs.clear();
     return POD_OK;
@@ -820,7 +831,18 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
     pod_status st = pod_require_sm100();
     if (st) return st;
     auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-    const int use_bulk = (N % 32 == 0) && al(rew) && al(val) && al(done) ? 1 : 0;
+    GaeMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    int use_bulk = (N % 16 == 0) && al(rew) && al(val) && al(done) ? 1 : 0;
+    if (use_bulk) {
+        const uint64_t dims[2] = {static_cast<uint64_t>(N), static_cast<uint64_t>(T)};
+        const uint64_t s4[1] = {static_cast<uint64_t>(N) * 4}, s1[1] = {static_cast<uint64_t>(N)};
+        const uint32_t box[2] = {32, GAE_L};
+        if (encode_plain(&maps.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dims, s4, box) ||
+            encode_plain(&maps.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dims, s4, box) ||
+            encode_plain(&maps.d, done, CU_TENSOR_MAP_DATA_TYPE_UINT8, dims, s1, box))
+            use_bulk = 0;
+    }
     const int groups = (N + 31) / 32;
     const unsigned blocks = static_cast<unsigned>((groups + GAE_WARPS - 1) / GAE_WARPS);
     static std::once_flag once;
@@ -831,7 +853,7 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
     });
     POD_CUDA(attr_err);
     gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), static_cast<cudaStream_t>(stream)>>>(
-        rew, val, done, boot, T, N, gamma, lambda, adv, ret, use_bulk);
+        maps, rew, val, done, boot, T, N, gamma, lambda, adv, ret, use_bulk);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }

@@ -187,7 +187,7 @@ def test_fitness_after_deterministic_episode():
 
 
 # ----------------------------------------------------------------- GAE
-@pytest.mark.parametrize("T,N", [(1, 32), (3, 1), (77, 100), (64, 4096), (256, 8192), (1000, 96)])
+@pytest.mark.parametrize("T,N", [(1, 32), (3, 1), (77, 100), (50, 48), (64, 4096), (256, 8192), (1000, 96), (33, 65536)])
 def test_gae_parity(T, N):
     r, v, d, boot = synth.gae_inputs(T, N, seed=T * 7 + N)
     adv_o, ret_o, mag = oracle.gae(r, v, d, boot, 0.99, 0.95)
@@ -295,3 +295,41 @@ def test_env_groups_bit_identical(monkeypatch):
     for other in outs[1:]:
         for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash", "dbg_aint"):
             assert torch.equal(getattr(outs[0], name), getattr(other, name)), name
+
+
+@pytest.mark.parametrize("cost", [0.0, 0.25, 0.002])
+@pytest.mark.parametrize("kind", ["all_buy", "uniform", "buy_then_sell"])
+def test_exact_quotient_ties(kind, cost):
+    """Integer prices and capital make b/unit land exactly on integers: exercises the
+    ledger's division fallback, the post-check and both exact shortcuts."""
+    rng = np.random.default_rng(17)
+    n, T_data, N, H, T = 8, 60, 64, 40, 40
+    prices = rng.choice([1.0, 2.0, 4.0, 5.0, 8.0, 10.0, 20.0, 25.0, 50.0], size=(T_data, n))
+    m = synth.make_flat_market(n, T_data, prices, n_feat=1)
+    cfg = api.make_config(N, n, 1, H, 1, 100, 0, 1000.0, cost, 1.0, 0.99, 3)
+    env = api.Env(cfg, torch.from_numpy(m.close).cuda(), torch.from_numpy(m.feat).cuda())
+    starts = np.array([0, 7], np.int64)
+    u = synth.injected_u(kind, T, N, n, 4)
+    tr = api.Trajectory.allocate(T, N, n, env.k_pad, debug=True, sampled=False)
+    env.reset(starts)
+    env.rollout(T, tr, injected_u=torch.from_numpy(u).cuda())
+    o = oracle.Env(m.close, m.feat, N, horizon=H, C0=1000.0, cost=cost, seed=3)
+    o.reset(np.repeat(starts, 32)[:N])
+    out = o.rollout(T, "inject", u=u, want=("obs", "rew", "done", "hold", "cash"))
+    assert_env_exact(tr, out, env.obs_dim)
+
+
+def test_weight_multicast_bit_identical(monkeypatch):
+    """Opt-in 4-CTA clusters sharing weight tiles by TMA multicast give identical results."""
+    outs = []
+    for mc in ("0", "1"):
+        monkeypatch.setenv("POD_MULTICAST", mc)
+        c = Case(n=100, f=3, T_data=2000, N=512, H=300, seed=13, dt=1 / (252 * 390))
+        aws, params, actor = _actor(c, 3, 512)
+        tr = api.Trajectory.allocate(4, 512, 100, c.k_pad, debug=True)
+        c.env.reset(c.starts)
+        c.env.rollout(4, tr, actor=actor)
+        c.env.check()
+        outs.append(tr)
+    for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash", "mu"):
+        assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name

@@ -16,13 +16,14 @@ actor = api.make_actor(w.n_hidden, w.hidden, params)
 T = 4
 tr = api.Trajectory.allocate(T, w.n_envs, w.n_stocks, env.k_pad)
 grid = 2 * ((w.n_envs // w.n_agents + 127) // 128) * w.n_agents
-buf = torch.zeros(grid * 32, dtype=torch.int64, device="cuda")
-_lib.load().pod_debug_actor_trace(env.h, C.c_void_p(buf.data_ptr()))
+buf = torch.zeros(grid * 64, dtype=torch.int64, device="cuda")
+ebuf = torch.zeros(env.n_tiles * 8, dtype=torch.int64, device="cuda")
+_lib.load().pod_debug_trace(env.h, C.c_void_p(buf.data_ptr()), C.c_void_p(ebuf.data_ptr()))
 env.reset(synth.tile_starts(env.n_tiles, w.T_data, min(w.horizon, w.T_data - 2), 1))
 for _ in range(3):
     env.rollout(T, tr, actor=actor)
 torch.cuda.synchronize()
-b = buf.view(grid, 32).cpu().numpy().astype(np.int64)
+b = buf.view(grid, 64).cpu().numpy().astype(np.int64)
 rel = b - b[:, :1]
 names = {1: "obs", 26: "end", 24: "head_acc", 25: "head_done"}
 for l in range(w.n_hidden + 1):
@@ -34,3 +35,12 @@ for l in range(w.n_hidden + 1):
 for k in sorted(names):
     col = rel[:, k]
     print(f"{names[k]:16s} median {int(np.median(col)):8d}  min {int(col.min()):8d}  max {int(col.max()):8d}")
+
+eb = ebuf.view(env.n_tiles, 8).cpu().numpy().astype(np.int64)
+erel = eb - eb[:, :1]
+for k, nm in enumerate(["start", "staged", "sells_done", "buys_done", "ledger_done", "rows_staged", "end"]):
+    col = erel[:, k]
+    print(f"env {nm:14s} median {int(np.median(col)):8d}  min {int(col.min()):8d}  max {int(col.max()):8d}")
+
+print("L0 stage ready (MMA side):", [int(np.median(rel[:, 32 + q])) for q in range(16)])
+print("producer issue times      :", [int(np.median(rel[:, 48 + q])) for q in range(16)])
