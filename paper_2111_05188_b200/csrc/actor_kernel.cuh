@@ -44,10 +44,12 @@ namespace pod {
 
 constexpr int ACT_THREADS = 320;       // 10 warps
 constexpr int ACT_STAGES = 5;          // weight ring depth
-constexpr int ACT_BN = 128;            // weight rows per ring stage (max)
+constexpr int ACT_BN = 256;            // weight rows per ring stage (max): one N = 256 MMA
+constexpr int ACT_BK = 32;             // K per ring stage (64-byte swizzled rows)
 constexpr int ACT_MAX_LAYERS = 5;      // n_hidden <= 4
 constexpr int ACT_BIAS_FLOATS = 1792;  // per-CTA staged biases + log-std + sigma
 constexpr int ACT_MAX_HQ = 32;         // head tickers per epilogue thread (n_out_pad <= 128)
+constexpr int ACT_MAX_NA = 4;          // activation atoms per CTA half (hidden <= 512)
 
 struct ActorArgs {
     int32_t N;               // envs
@@ -92,10 +94,11 @@ __host__ __device__ inline int actor_layer_out(int l, int n_layers, int hidden, 
     return l == n_layers - 1 ? n_out_pad : hidden;
 }
 __host__ __device__ inline int actor_bn(int half) { return half < ACT_BN ? half : ACT_BN; }
+constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
 
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
-    return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_BN * 128 +
+    return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_STAGE_BYTES +
            ACT_BIAS_FLOATS * 4 + 4 * 128 * 4 + 256;   // + barriers
 }
 
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const int ka = (a.k_pad > a.hidden ? a.k_pad : a.hidden) / 64;   // activation atoms
     const uint32_t act_s = base_u32;                                  // ka * 16 KB
     const uint32_t ring_s = act_s + ka * 16384u;
-    const uint32_t stage_bytes = ACT_BN * 128u;
+    const uint32_t stage_bytes = ACT_STAGE_BYTES;
     const uint32_t bias_off = ka * 16384u + ACT_STAGES * stage_bytes;
     float* bias_s = reinterpret_cast<float*>(base + bias_off);                 // [ACT_BIAS_FLOATS]
     float* logp_s = bias_s + ACT_BIAS_FLOATS;                                  // [4][128] (CTA 0)
@@ -186,19 +189,19 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 const int K = l == 0 ? a.k_pad : a.hidden;
                 const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
                 const int bn = actor_bn(half);
-                const int KB = K / 64;
+                const int KB = K / ACT_BK;                                          // 32-wide K blocks
                 const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);   // own half of h_l first
                 for (int c = 0; c < half / bn; ++c) {
                     for (int j = 0; j < KB; ++j) {
                         const int kb = (j + kb0) % KB;
                         mbar_wait(empty_b + 8u * stage, phase ^ 1u);
-                        mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * 128u);
+                        mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * (ACT_BK * 2));
                         if (!a.mc) {
-                            tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * 64,
+                            tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
                                         static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage);
                         } else if ((seq & 1) == static_cast<int>(cr >> 1)) {
                             // alternate tiles: this CTA fetches it for itself and its partner
-                            tma_load_3d_mc(ring_s + stage * stage_bytes, &maps.w[l], kb * 64,
+                            tma_load_3d_mc(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
                                            static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage, share_mask);
                         }
                         if (tr && seq < 16) tr[48 + seq] = clock64();
@@ -218,6 +221,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             mbar_wait(obs_b, 0);
             tc_fence_after();
             if (tr) tr[1] = clock64();
+            const uint64_t adesc0 = sw128_desc(act_s);
+            const uint64_t bdesc0 = sw64_desc(ring_s);
             int stage = 0;
             uint32_t phase = 0;
             const int na = a.hidden / 128;           // activation atoms (64 cols) per CTA half
@@ -227,33 +232,33 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
                 const int bn = actor_bn(half);
                 const uint32_t idesc = idesc_bf16_f32(128, static_cast<uint32_t>(bn));
-                const int KB = K / 64;
-                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * na;   // own atoms of h_l first
+                const int KB = K / ACT_BK;                 // 32-wide K blocks (two per activation atom)
+                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * na * 2;   // own atoms of h_l first
                 const uint32_t par = static_cast<uint32_t>(l - 1) & 1u;
                 for (int c = 0; c < half / bn; ++c) {
                     for (int j = 0; j < KB; ++j) {
-                        const int kb = (j + kb0) % KB;
-                        if (l > 0 && c == 0) {
+                        const int kb = j + kb0 < KB ? j + kb0 : j + kb0 - KB;
+                        if (l > 0 && c == 0 && (j & 1) == 0) {
                             // h_l atom by atom: own atoms as the epilogue finishes them, then the
                             // peer's atoms as its bulk copies land
-                            if (j < na) {
-                                mbar_wait(ownrdy_b + 8u * j, par);
+                            const int ja = j >> 1;
+                            if (ja < na) {
+                                mbar_wait(ownrdy_b + 8u * ja, par);
                             } else {
-                                mbar_arrive_expect_tx(peerrdy_b + 8u * (j - na), 16384u);
-                                mbar_wait(peerrdy_b + 8u * (j - na), par);
+                                mbar_arrive_expect_tx(peerrdy_b + 8u * (ja - na), 16384u);
+                                mbar_wait(peerrdy_b + 8u * (ja - na), par);
                             }
                             tc_fence_after();
                         }
                         mbar_wait(full_b + 8u * stage, phase);
                         tc_fence_after();
                         if (tr && l == 0 && c * KB + j < 16) tr[32 + c * KB + j] = clock64();
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint64_t ad = sw128_desc(act_s + kb * 16384u + k * 32u);
-                            const uint64_t bd = sw128_desc(ring_s + stage * stage_bytes + k * 32u);
-                            mma_bf16(tmem + (static_cast<uint32_t>(l) & 1u) * tbuf + static_cast<uint32_t>(c * bn), ad, bd,
-                                     idesc, (j | k) != 0);
-                        }
+                        // descriptors: precomputed bases + the start-address field (16-B units)
+                        const uint64_t ad = adesc0 + (((kb >> 1) * 16384u + (kb & 1) * 64u) >> 4);
+                        const uint64_t bd = bdesc0 + ((stage * stage_bytes) >> 4);
+                        const uint32_t dt = tmem + (static_cast<uint32_t>(l) & 1u) * tbuf + static_cast<uint32_t>(c * bn);
+                        mma_bf16(dt, ad, bd, idesc, j != 0);
+                        mma_bf16(dt, ad + 2, bd + 2, idesc, 1u);
                         if (a.mc) mma_commit_mc(empty_b + 8u * stage, share_mask);   // free it in both CTAs
                         else mma_commit(empty_b + 8u * stage);
                         if (++stage == ACT_STAGES) {
@@ -361,16 +366,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             if (cc >= hq / 8) break;
             const int tc = hh * hq + cc * 8;                         // TMEM column (local)
             const int i0 = static_cast<int>(rank) * head_half + tc;  // global ticker
-            uint32_t v[8];
+            uint32_t hv[8];
             __syncwarp();
-            tmem_ld8(trow + (static_cast<uint32_t>(L) & 1u) * tbuf + static_cast<uint32_t>(tc), v);
+            tmem_ld8(trow + (static_cast<uint32_t>(L) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
             tmem_ld_wait();
             if (valid && i0 < a.n) {
                 float raw[8], mu[8];
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     const int i = i0 + jj;
-                    mu[jj] = __uint_as_float(v[jj]) + bias[tc + jj];
+                    mu[jj] = __uint_as_float(hv[jj]) + bias[tc + jj];
                     raw[jj] = mu[jj];
                     if (i < a.n) {
                         // noise z ~ N(0,1) for (env, step, ticker), generated by the previous env-step launch

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "actor_kernel.cuh"
+#include "actor_pair_kernel.cuh"
 #include "env_kernel.cuh"
 #include "gae_kernel.cuh"
 #include "pod.h"
@@ -91,9 +92,10 @@ static EncodeTiledFn get_encode() {
     return fn;
 }
 
-// bf16 tensor, rank 2 or 3, 128B swizzle, box inner 64 elements (128 B)
+// bf16 tensor, rank 2 or 3, 128B swizzle (box inner 64 elements) or 64B swizzle (32 elements)
 static pod_status encode_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                              const uint64_t* strides_bytes, const uint32_t* box) {
+                              const uint64_t* strides_bytes, const uint32_t* box,
+                              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     cuuint64_t d[3], s[2];
@@ -104,7 +106,7 @@ static pod_status encode_bf16(CUtensorMap* m, const void* base, int rank, const 
     }
     for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank), const_cast<void*>(base), d, s, b,
-                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
     return POD_OK;
@@ -341,12 +343,19 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         if (G > POD_MAX_GROUPS) G = POD_MAX_GROUPS;
         if (G > mt) G = mt;
         if (e->per_agent % 128 != 0) G = 1;
-        e->groups = G;
         // weight-tile multicast across 2 M-tiles: measured no faster (the fills are limited by
         // shared-memory bandwidth under SS-mode MMAs, not by L2), so opt-in only
         const char* mcs = getenv("POD_MULTICAST");
         e->mc_ok = (e->per_agent % 256 == 0 && mcs && mcs[0] == '1') ? 1 : 0;
-        for (int g = 0; g <= G; ++g) e->g_m0[g] = static_cast<int>(static_cast<int64_t>(g) * mt / G);
+        // boundaries in units of M-tile pairs when agents fill pairs (the 2-SM actor needs them)
+        const int unit = (e->per_agent % 256 == 0) ? 2 : 1;
+        const int units = (mt + unit - 1) / unit;
+        if (G > units) G = units;
+        for (int g = 0; g <= G; ++g) {
+            const int m = static_cast<int>(static_cast<int64_t>(g) * units / G) * unit;
+            e->g_m0[g] = m < mt ? m : mt;
+        }
+        e->groups = G;
     }
     e->profile = 0;
     e->last_prof = nullptr;
@@ -364,6 +373,8 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(actor_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   env_smem_bytes(ENV_MAX_STOCKS, ENV_MAX_KPAD));
@@ -490,6 +501,7 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
 // ------------------------------------------------------------ rollout
 struct RolloutPlan {
     bool injected;
+    bool pair;          // 4-CTA clusters with the 2-SM MMA (per-agent env count a multiple of 256)
     ActorMaps maps;
     ActorArgs aa;
     size_t actor_smem;
@@ -538,19 +550,22 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
             // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
             // every agent has an even number of full M-tiles and so does this launch
-            aa.mc = (e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
+            aa.mc = (!p.pair && e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
             lc.gridDim = dim3(static_cast<unsigned>(2 * mtiles));
             lc.blockDim = dim3(ACT_THREADS);
             lc.dynamicSmemBytes = p.actor_smem;
             lc.stream = s;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = aa.mc ? 4 : 2;
+            at[0].val.clusterDim.x = (aa.mc || p.pair) ? 4 : 2;
             at[0].val.clusterDim.y = 1;
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
+            if (p.pair)
+                cudaLaunchKernelEx(&lc, actor_pair_kernel, p.maps, aa);
+            else
+                cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
         }
         mark(t, 1);
         mark(t, 2);
@@ -634,14 +649,21 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             st = encode_bf16(&p.maps.obs, tr->obs, 2, dims, str, box);
             if (st) return st;
         }
+        {
+            // the 2-SM (cta_group::2) variant: opt-in — its MMA phase is faster but its
+            // epilogue/synchronisation currently costs more than it saves (measured)
+            const char* pp = getenv("POD_PAIR");
+            p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1';
+        }
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
-            const int bn = actor_bn(rows / 2);
+            const int bn = p.pair ? rows / 4 : actor_bn(rows / 2);   // pair: each CTA stages half of its column half
             const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
                                       static_cast<uint64_t>(e->cfg.n_agents)};
             const uint64_t str[2] = {static_cast<uint64_t>(L.w_cols[l]) * 2, actor->param_bytes};
-            const uint32_t box[3] = {64, static_cast<uint32_t>(bn), 1};
-            st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 3, dims, str, box);
+            const uint32_t box[3] = {ACT_BK, static_cast<uint32_t>(bn), 1};
+            st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 3, dims, str, box,
+                             CU_TENSOR_MAP_SWIZZLE_64B);
             if (st) return st;
         }
         ActorArgs& aa = p.aa;
@@ -667,7 +689,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         aa.znoise = e->znoise;
         aa.err = e->err;
         aa.trace = e->trace;
-        p.actor_smem = actor_smem_bytes(L.k_pad, actor->hidden);
+        p.actor_smem = p.pair ? actor_pair_smem_bytes(L.k_pad, actor->hidden) : actor_smem_bytes(L.k_pad, actor->hidden);
         if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
     }
     if (!e->use_graphs) {

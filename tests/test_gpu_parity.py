@@ -333,3 +333,20 @@ def test_weight_multicast_bit_identical(monkeypatch):
         outs.append(tr)
     for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash", "mu"):
         assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
+
+
+def test_pair_kernel_matches_single_cta_kernel(monkeypatch):
+    """The 2-SM (cta_group::2) actor and the 2-CTA column-split actor agree (same K order)."""
+    outs = []
+    for pp in ("0", "1"):
+        monkeypatch.setenv("POD_PAIR", pp)
+        c = Case(n=100, f=3, T_data=2000, N=512, H=300, seed=14, dt=1 / (252 * 390))
+        aws, params, actor = _actor(c, 3, 512)
+        tr = api.Trajectory.allocate(3, 512, 100, c.k_pad, debug=True)
+        c.env.reset(c.starts)
+        c.env.rollout(3, tr, actor=actor)
+        c.env.check()
+        outs.append(tr)
+    mu0 = outs[0].mu.cpu().numpy().astype(np.float64)
+    mu1 = outs[1].mu.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(mu1, mu0, rtol=1e-5, atol=1e-5)

@@ -42,5 +42,6 @@ for k, nm in enumerate(["start", "staged", "sells_done", "buys_done", "ledger_do
     col = erel[:, k]
     print(f"env {nm:14s} median {int(np.median(col)):8d}  min {int(col.min()):8d}  max {int(col.max()):8d}")
 
-print("L0 stage ready (MMA side):", [int(np.median(rel[:, 32 + q])) for q in range(16)])
+lead = rel[0::2] if rel[1::2, 1].max() == 0 and rel[0::2, 1].max() > 0 else rel
+print("L0 stage ready (MMA side):", [int(np.median(lead[:, 32 + q])) for q in range(16)])
 print("producer issue times      :", [int(np.median(rel[:, 48 + q])) for q in range(16)])
