@@ -54,7 +54,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--profile-stride", type=int, default=8,
+    p.add_argument("--profile-stride", type=int, default=32,
                    help="bracket every k-th step's kernels with CUDA events (0 = off)")
     p.add_argument("--elite-k", type=int, default=None)
     p.add_argument("--tdata", type=int, default=None, help="truncate the market (profiling runs only)")

@@ -1,0 +1,20 @@
+#!/bin/bash
+# One GPU call: benches (C3 default with cpu_baseline + e2e, C2, C5), the ncu launch
+# list of a short C3 run, and one `ncu --set full` capture per hot kernel.
+# Outputs under gpurun_out/$1/ (scratch; summaries are copied to profiles/ by hand).
+OUT=gpurun_out/${1:-prof}
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
+timeout 900 python bench.py > $OUT/bench_c3.json 2> $OUT/bench_c3.err; echo "C3 exit $?"
+timeout 600 python bench.py --config C2 > $OUT/bench_c2.json 2> $OUT/bench_c2.err; echo "C2 exit $?"
+timeout 900 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "C5 exit $?"
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "REF exit $?"
+CMD="python bench.py --T 8 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --profile-stride 0 --tdata 100000"
+$CMD > $OUT/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $OUT/launches_c3.csv $CMD > $OUT/ncu_list.log 2>&1; echo "list exit $?"
+for K in actor_forward env_step gae; do
+  SKIP=12; [ "$K" = gae ] && SKIP=3
+  ncu --set full --clock-control none --import-source on -k regex:$K -s $SKIP -c 1 -o $OUT/prof_$K $CMD > $OUT/ncu_$K.log 2>&1
+  echo "ncu $K exit $?"
+done
