@@ -87,7 +87,7 @@ struct EnvMaps {
 };
 
 // shared memory of one block (one tile), TMA destinations 128-B aligned:
-//   [hold_s n*32 i32 | aint_s n*32 i16 (pad 128) | unit, p_t, p_1, 1/unit, unit_lo n f64 each (pad 16) |
+//   [hold_s n*32 i32 | aint_s n*32 i16 (pad 128) | unit, p_t, p_1, 1/unit n f64 each (pad 16) |
 //    p_t, p_1, p_0 n f32 (pad 16) | tmpl k_pad bf16 | stg 32 x e_pad bf16 | mbar]
 __host__ __device__ inline int env_e_pad(int n) { return (1 + n + 7) / 8 * 8; }
 struct EnvSmemLayout {
@@ -97,7 +97,7 @@ __host__ __device__ inline EnvSmemLayout env_smem_layout(int n, int k_pad) {
     EnvSmemLayout L;
     L.aint = n * 128;
     L.unit = L.aint + (n * 64 + 127) / 128 * 128;
-    L.p = L.unit + (5 * n * 8 + 15) / 16 * 16;
+    L.p = L.unit + (4 * n * 8 + 15) / 16 * 16;
     L.tmpl = L.p + (3 * n * 4 + 15) / 16 * 16;
     L.stg = L.tmpl + k_pad * 2;
     L.bar = L.stg + 32 * env_e_pad(n) * 2;
@@ -127,7 +127,6 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     double* p_t64 = unit_s + n;                                           // [n] p_t as float64
     double* p_164 = unit_s + 2 * n;                                       // [n] p_{t+1} as float64
     double* rcp_s = unit_s + 3 * n;                                       // [n] fl(1 / unit)
-    double* unit_lo = unit_s + 4 * n;                                     // [n] fl(unit (1 - 2^-50))
     float* p_t = reinterpret_cast<float*>(env_smem + SL.p);
     float* p_1 = p_t + n;
     float* p_0 = p_1 + n;
@@ -205,7 +204,6 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     for (int i = tid; i < n; i += ENV_THREADS) {
         unit_s[i] = __dmul_rn(static_cast<double>(p_t[i]), opc);
         rcp_s[i] = __ddiv_rn(1.0, unit_s[i]);
-        unit_lo[i] = __dmul_rn(unit_s[i], 0.99999999999999911182158029987);   // 1 - 2^-50
         p_t64[i] = static_cast<double>(p_t[i]);
         p_164[i] = static_cast<double>(p_1[i]);
     }
@@ -246,15 +244,16 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             }
             if (trc && lane == 0) trc[2] = clock64();
             // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending, then revalue at p_{t+1}.
-            // The oracle computes qmax = floor(fl(b / unit)) (minus one if fl(qmax unit) > b) and
-            // q = max(0, min(a, qmax)).  Exact shortcuts keep the IEEE division off the chain:
-            //  (i)  fl(fl((a+1) unit)(1 + 2^-49)) <= b  =>  exact b/unit > a+1, so q = a;
-            //  (ii) b < fl(unit (1 - 2^-50))            =>  exact b/unit < 1 - 2^-52, so q = 0;
-            //  (iii) y = fl(b fl(1/unit)) is within b/unit (1 +- 2^-51); if y is at least
-            //       y 2^-49 away from both neighbouring integers, floor(fl(b/unit)) = floor(y).
-            // Otherwise (b/unit within ~2^-49 of an integer) the IEEE quotient is used (rare).
-            // Every candidate is computed and selected, so the loop has no divergent branch
-            // except that rare fallback.
+            // The oracle computes qmax = floor(fl(b / unit)) (minus one if fl(qmax unit) > b),
+            // q = max(0, min(a, qmax)), b -= fl(q unit).  Here, with y = fl(b fl(1/unit)):
+            //   q = min(floor(y), a+) and cost = fl(q unit)       (5 dependent float64 ops)
+            // equals the oracle whenever
+            //   (i)  fl(fl((a+1) unit)(1 + 2^-49)) <= b: exact b/unit > a+1, both give q = a; or
+            //   (ii) y is at least y 2^-49 from both neighbouring integers: y = b/unit (1 +- 2^-51)
+            //        and fl(b/unit) = b/unit (1 +- 2^-53) then have the same floor m, and
+            //        m unit < b (1 - 2^-51), so the oracle's post-check cannot fire.
+            // Otherwise (b/unit within ~2^-49 of an integer) the oracle's own expressions are
+            // evaluated (IEEE quotient + post-check): rare, and only then does the warp branch.
             double ph = 0.0;
 #pragma unroll 4
             for (int i = 0; i < n; ++i) {
@@ -262,24 +261,24 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 int h = hold_s[i * 32 + lane];
                 if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
                 const double unit = unit_s[i];
-                const int ap = ai > 0 ? ai : 0;
-                const double need = __dmul_rn(__dmul_rn(static_cast<double>(ap + 1), unit),
+                const double ad = static_cast<double>(ai > 0 ? ai : 0);
+                const double need = __dmul_rn(__dmul_rn(__dadd_rn(ad, 1.0), unit),
                                               1.0000000000000017763568394002504646778106689453125);
-                const double cost_a = __dmul_rn(static_cast<double>(ap), unit);
-                const bool fast = ai <= 0 || need <= cash;         // (i), or nothing to buy
-                const bool unaff = cash < unit_lo[i];              // (ii)
                 const double y = __dmul_rn(cash, rcp_s[i]);
-                double qmax = floor(y);
-                const double fr = __dadd_rn(y, -qmax);
+                const double fl = floor(y);
+                double qd = fl < ad ? fl : ad;
+                double cost = __dmul_rn(qd, unit);
+                const double fr = __dadd_rn(y, -fl);
                 const double tol = __dmul_rn(y, 1.7763568394002504646778106689453125e-15);   // 2^-49
-                if (!fast && !unaff && !(fr >= tol && __dadd_rn(1.0, -fr) >= tol))
-                    qmax = floor(__ddiv_rn(cash, unit));           // (iii) failed: IEEE quotient
-                if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
-                double qd = static_cast<double>(ai) < qmax ? static_cast<double>(ai) : qmax;
-                qd = qd < 0.0 ? 0.0 : qd;
-                const int q = fast ? ap : (unaff ? 0 : static_cast<int>(qd));
-                const double cost = fast ? cost_a : (unaff ? 0.0 : __dmul_rn(qd, unit));
-                h += q;
+                const bool safe = ai <= 0 || need <= cash || (fr >= tol && __dadd_rn(1.0, -fr) >= tol);
+                if (!safe) {                                       // the oracle's expressions
+                    double qmax = floor(__ddiv_rn(cash, unit));
+                    if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
+                    qd = ad < qmax ? ad : qmax;
+                    qd = qd < 0.0 ? 0.0 : qd;
+                    cost = __dmul_rn(qd, unit);
+                }
+                h += static_cast<int>(qd);
                 cash = __dadd_rn(cash, -cost);
                 hold_s[i * 32 + lane] = h;
                 ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
