@@ -853,19 +853,82 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
     pod_status st = pod_require_sm100();
     if (st) return st;
     auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    // Tensor-map encoding costs several microseconds of host time per map; a rollout loop calls pod_gae on the
+    // same trajectory buffers every iteration, so the last few encodings are cached by (pointers, T, N).
+    struct GaeCacheEntry {
+        const void *r, *v, *d;
+        int32_t T, N, use_bulk;
+        GaeMaps maps;
+    };
+    static std::mutex cache_mu;
+    static GaeCacheEntry cache[4];
+    static int cache_next = 0;
     GaeMaps maps;
     memset(&maps, 0, sizeof(maps));
     int use_bulk = (N % 16 == 0) && al(rew) && al(val) && al(done) ? 1 : 0;
     if (use_bulk) {
-        const uint64_t dims[2] = {static_cast<uint64_t>(N), static_cast<uint64_t>(T)};
-        const uint64_t s4[1] = {static_cast<uint64_t>(N) * 4}, s1[1] = {static_cast<uint64_t>(N)};
-        const uint32_t box[2] = {32, GAE_L};
-        if (encode_plain(&maps.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dims, s4, box) ||
-            encode_plain(&maps.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dims, s4, box) ||
-            encode_plain(&maps.d, done, CU_TENSOR_MAP_DATA_TYPE_UINT8, dims, s1, box))
-            use_bulk = 0;
+        std::lock_guard<std::mutex> lk(cache_mu);
+        bool hit = false;
+        for (const GaeCacheEntry& c : cache)
+            if (c.r == rew && c.v == val && c.d == done && c.T == T && c.N == N) {
+                maps = c.maps;
+                use_bulk = c.use_bulk;
+                hit = true;
+                break;
+            }
+        if (!hit) {
+            const uint64_t dims[2] = {static_cast<uint64_t>(N), static_cast<uint64_t>(T)};
+            const uint64_t s4[1] = {static_cast<uint64_t>(N) * 4}, s1[1] = {static_cast<uint64_t>(N)};
+            const uint32_t box[2] = {32, GAE_L};
+            if (encode_plain(&maps.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dims, s4, box) ||
+                encode_plain(&maps.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dims, s4, box) ||
+                encode_plain(&maps.d, done, CU_TENSOR_MAP_DATA_TYPE_UINT8, dims, s1, box))
+                use_bulk = 0;
+            cache[cache_next] = GaeCacheEntry{rew, val, done, T, N, use_bulk, maps};
+            cache_next = (cache_next + 1) % 4;
+        }
     }
     const int groups = (N + 31) / 32;
+    // Few column groups (under four per SM): split time across the warps of a block (gae_seg_kernel), as long
+    // as the [T x 32] slab fits in shared memory.  POD_GAE_PATH=seq|seg forces a path (tests compare both).
+    const int nchunks = (T + GAE_L - 1) / GAE_L;
+    bool seg_ok = use_bulk && nchunks <= 20;
+    bool use_seg = seg_ok && groups < 4 * 148;
+    if (const char* f = getenv("POD_GAE_PATH")) {
+        if (!strcmp(f, "seq")) use_seg = false;
+        if (!strcmp(f, "seg")) use_seg = seg_ok;
+    }
+    if (use_seg) {
+        const int cpw = nchunks <= GAE_SEG_MAX ? 1 : GAE_CPW_MAX;
+        const int seg = (nchunks + cpw - 1) / cpw;
+        const int want = static_cast<int>(gae_seg_smem_bytes(seg, cpw));
+        static std::mutex seg_mu;
+        static int seg_attr = 0;   // dynamic shared memory granted so far
+        {
+            std::lock_guard<std::mutex> lk(seg_mu);
+            if (seg_attr < want) {
+                cudaError_t ce = cudaFuncSetAttribute(gae_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
+                if (ce != cudaSuccess) {
+                    cudaFuncAttributes fa;
+                    memset(&fa, 0, sizeof(fa));
+                    cudaError_t ce2 = cudaFuncGetAttributes(&fa, gae_seg_kernel);
+                    int dev = 0, optin = 0;
+                    cudaGetDevice(&dev);
+                    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+                    return pod_fail(POD_ERR_CUDA,
+                                    "gae_seg_kernel smem attribute %d B: %s (getattr %s: static %zu B, max dyn %d B, "
+                                    "max threads %d, regs %d; device opt-in %d B)",
+                                    want, cudaGetErrorString(ce), cudaGetErrorString(ce2), fa.sharedSizeBytes,
+                                    fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock, fa.numRegs, optin);
+                }
+                seg_attr = want;
+            }
+        }
+        gae_seg_kernel<<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw),
+                         static_cast<cudaStream_t>(stream)>>>(maps, boot, T, N, gamma, lambda, adv, ret, cpw);
+        POD_CUDA(cudaGetLastError());
+        return POD_OK;
+    }
     const unsigned blocks = static_cast<unsigned>((groups + GAE_WARPS - 1) / GAE_WARPS);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;

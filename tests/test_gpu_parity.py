@@ -187,8 +187,13 @@ def test_fitness_after_deterministic_episode():
 
 
 # ----------------------------------------------------------------- GAE
-@pytest.mark.parametrize("T,N", [(1, 32), (3, 1), (77, 100), (50, 48), (64, 4096), (256, 8192), (1000, 96), (33, 65536)])
-def test_gae_parity(T, N):
+@pytest.mark.parametrize("path", ["auto", "seq", "seg"])
+@pytest.mark.parametrize("T,N", [(1, 32), (3, 1), (77, 100), (50, 48), (64, 4096), (256, 8192), (1000, 96), (33, 65536),
+                                 (31, 16), (512, 32), (544, 64), (640, 256)])
+def test_gae_parity(T, N, path, monkeypatch):
+    """Both GAE kernels (single-warp sequential scan; time-segmented block scan) against the oracle."""
+    if path != "auto":
+        monkeypatch.setenv("POD_GAE_PATH", path)
     r, v, d, boot = synth.gae_inputs(T, N, seed=T * 7 + N)
     adv_o, ret_o, mag = oracle.gae(r, v, d, boot, 0.99, 0.95)
     adv, ret = api.pod_gae(*(torch.from_numpy(x).cuda() for x in (r, v, d, boot)), 0.99, 0.95)
