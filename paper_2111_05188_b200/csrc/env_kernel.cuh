@@ -245,16 +245,24 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             if (trc && lane == 0) trc[2] = clock64();
             // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending, then revalue at p_{t+1}.
             // The oracle computes qmax = floor(fl(b / unit)) (minus one if fl(qmax unit) > b),
-            // q = max(0, min(a, qmax)), b -= fl(q unit).  Here, with y = fl(b fl(1/unit)):
-            //   q = min(floor(y), a+) and cost = fl(q unit)       (5 dependent float64 ops)
+            // q = max(0, min(a, qmax)), b -= fl(q unit).  Here, with y = fl(b fl(1/unit)) and
+            // m = floor(y) (y = b/unit (1 +- 2^-51), fl(b/unit) = b/unit (1 +- 2^-53)):
+            //   q = min(m, a+), cost = fl(q unit)         (5 dependent float64 ops)
             // equals the oracle whenever
-            //   (i)  fl(fl((a+1) unit)(1 + 2^-49)) <= b: exact b/unit > a+1, both give q = a; or
-            //   (ii) y is at least y 2^-49 from both neighbouring integers: y = b/unit (1 +- 2^-51)
-            //        and fl(b/unit) = b/unit (1 +- 2^-53) then have the same floor m, and
-            //        m unit < b (1 - 2^-51), so the oracle's post-check cannot fire.
-            // Otherwise (b/unit within ~2^-49 of an integer) the oracle's own expressions are
-            // evaluated (IEEE quotient + post-check): rare, and only then does the warp branch.
+            //   (i)  m > a+: b/unit >= (a+1)(1 - 2^-51) > a, so the oracle's qmax >= a too; or
+            //   (ii) fr = y - m (exact) lies in [2^-34, 1 - 2^-34]: y < 2^15 here (else (i)),
+            //        so |y - fl(b/unit)| <= y 2^-51 < 2^-36 while y is at least 2^-34 from both
+            //        neighbouring integers: fl(b/unit) has the same floor m, and
+            //        m unit < b - 2^-35 unit: the post-check cannot fire.
+            // fr and m are non-negative doubles, compared through their bit patterns (integer
+            // compares).  The test is kept off the carried chain: a ticker that fails it (b/unit
+            // within ~2^-34 of an integer: rare) only sets a flag, and if any lane of the warp
+            // raised it the whole buy pass is redone below with the oracle's own expressions.
+            constexpr long long FR_LO = 0x3DD0000000000000ll;   // 2^-34
+            constexpr long long FR_HI = 0x3FEFFFFFFFF80000ll;   // 1 - 2^-34
+            const double cash_sold = cash;
             double ph = 0.0;
+            bool unsure = false;
 #pragma unroll 4
             for (int i = 0; i < n; ++i) {
                 const int ai = aint_s[i * 32 + lane];
@@ -262,26 +270,43 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
                 const double unit = unit_s[i];
                 const double ad = static_cast<double>(ai > 0 ? ai : 0);
-                const double need = __dmul_rn(__dmul_rn(__dadd_rn(ad, 1.0), unit),
-                                              1.0000000000000017763568394002504646778106689453125);
                 const double y = __dmul_rn(cash, rcp_s[i]);
                 const double fl = floor(y);
-                double qd = fl < ad ? fl : ad;
-                double cost = __dmul_rn(qd, unit);
-                const double fr = __dadd_rn(y, -fl);
-                const double tol = __dmul_rn(y, 1.7763568394002504646778106689453125e-15);   // 2^-49
-                const bool safe = ai <= 0 || need <= cash || (fr >= tol && __dadd_rn(1.0, -fr) >= tol);
-                if (!safe) {                                       // the oracle's expressions
-                    double qmax = floor(__ddiv_rn(cash, unit));
-                    if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
-                    qd = ad < qmax ? ad : qmax;
-                    qd = qd < 0.0 ? 0.0 : qd;
-                    cost = __dmul_rn(qd, unit);
-                }
+                const double qd = fl < ad ? fl : ad;
+                const double cost = __dmul_rn(qd, unit);
+                const long long frb = __double_as_longlong(__dadd_rn(y, -fl));
+                unsure |= !(ai <= 0 || __double_as_longlong(fl) > __double_as_longlong(ad) ||
+                            (frb >= FR_LO && frb <= FR_HI));
                 h += static_cast<int>(qd);
                 cash = __dadd_rn(cash, -cost);
                 hold_s[i * 32 + lane] = h;
                 ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
+            }
+            if (__any_sync(__activemask(), unsure)) {
+                // redo: replay the pass above to recover each ticker's post-sell holdings, and run
+                // the oracle's expressions, qmax = floor(fl(b / unit)) (minus one if
+                // fl(qmax unit) > b), q = max(0, min(a+, qmax)), b -= fl(q unit), alongside
+                double bf = cash_sold;
+                cash = cash_sold;
+                ph = 0.0;
+                for (int i = 0; i < n; ++i) {
+                    const int ai = aint_s[i * 32 + lane];
+                    const double unit = unit_s[i];
+                    const double ad = static_cast<double>(ai > 0 ? ai : 0);
+                    const double yf = __dmul_rn(bf, rcp_s[i]);
+                    const double flf = floor(yf);
+                    const double qf = flf < ad ? flf : ad;
+                    bf = __dadd_rn(bf, -__dmul_rn(qf, unit));
+                    const int h_sold = hold_s[i * 32 + lane] - static_cast<int>(qf);
+                    double qmax = floor(__ddiv_rn(cash, unit));
+                    if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
+                    double qd = ad < qmax ? ad : qmax;
+                    qd = qd < 0.0 ? 0.0 : qd;
+                    cash = __dadd_rn(cash, -__dmul_rn(qd, unit));
+                    const int h = h_sold + static_cast<int>(qd);
+                    hold_s[i * 32 + lane] = h;
+                    ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
+                }
             }
             if (trc && lane == 0) trc[3] = clock64();
             const double v1 = __dadd_rn(cash, ph);

@@ -26,6 +26,12 @@ torch.cuda.synchronize()
 b = buf.view(grid, 64).cpu().numpy().astype(np.int64)
 rel = b - b[:, :1]
 names = {1: "obs", 26: "end", 24: "head_acc", 25: "head_done"}
+for j in range(4):
+    names[16 + 2 * j] = f"L1 atom{j} tmem"
+    names[17 + 2 * j] = f"L1 atom{j} sent"
+for j in range(2):
+    names[27 + 2 * j] = f"L1 atom{j} stored"
+    names[28 + 2 * j] = f"L1 atom{j} all arrived"
 for l in range(w.n_hidden + 1):
     names[2 + 4 * l] = f"L{l}_mma_start"
     names[3 + 4 * l] = f"L{l}_mma_issued"
@@ -41,6 +47,7 @@ erel = eb - eb[:, :1]
 for k, nm in enumerate(["start", "staged", "sells_done", "buys_done", "ledger_done", "rows_staged", "end"]):
     col = erel[:, k]
     print(f"env {nm:14s} median {int(np.median(col)):8d}  min {int(col.min()):8d}  max {int(col.max()):8d}")
+print("env slow-buy tickers per warp: median", int(np.median(eb[:, 7])), "max", int(eb[:, 7].max()))
 
 lead = rel[0::2] if rel[1::2, 1].max() == 0 and rel[0::2, 1].max() > 0 else rel
 print("L0 stage ready (MMA side):", [int(np.median(lead[:, 32 + q])) for q in range(16)])
