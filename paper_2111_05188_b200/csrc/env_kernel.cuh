@@ -37,6 +37,7 @@ namespace pod {
 constexpr int ENV_MAX_STOCKS = 128;
 constexpr int ENV_MAX_KPAD = 512;
 constexpr int ENV_THREADS = 128;      // 4 warps per env tile
+constexpr int ENV_BUY_CHUNKS = 7;     // buy-pass chunks released to the trailing warps (one mbarrier each)
 constexpr int ENV_MAX_MARKET = 3 * ENV_MAX_STOCKS + ENV_MAX_KPAD;   // p_t, p_1, p_0, indicators
 
 struct EnvArgs {
@@ -91,7 +92,7 @@ struct EnvMaps {
 //    p_t, p_1, p_0 n f32 (pad 16) | tmpl k_pad bf16 | stg 32 x e_pad bf16 | mbar]
 __host__ __device__ inline int env_e_pad(int n) { return (1 + n + 7) / 8 * 8; }
 struct EnvSmemLayout {
-    int aint, unit, p, tmpl, stg, bar, total;
+    int aint, unit, p, tmpl, stg, ph, bar, total;
 };
 __host__ __device__ inline EnvSmemLayout env_smem_layout(int n, int k_pad) {
     EnvSmemLayout L;
@@ -100,8 +101,9 @@ __host__ __device__ inline EnvSmemLayout env_smem_layout(int n, int k_pad) {
     L.p = L.unit + (4 * n * 8 + 15) / 16 * 16;
     L.tmpl = L.p + (3 * n * 4 + 15) / 16 * 16;
     L.stg = L.tmpl + k_pad * 2;
-    L.bar = L.stg + 32 * env_e_pad(n) * 2;
-    L.total = L.bar + 16;
+    L.ph = (L.stg + 32 * env_e_pad(n) * 2 + 7) / 8 * 8;
+    L.bar = L.ph + 32 * 8;
+    L.total = L.bar + 8 + 8 * ENV_BUY_CHUNKS;   // TMA barrier, then one per buy chunk
     return L;
 }
 __host__ __device__ inline int env_smem_bytes(int n, int k_pad) { return env_smem_layout(n, k_pad).total; }
@@ -132,6 +134,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     float* p_0 = p_1 + n;
     uint16_t* tmpl = reinterpret_cast<uint16_t*>(env_smem + SL.tmpl);
     uint16_t* stg = reinterpret_cast<uint16_t*>(env_smem + SL.stg);                           // [32][e_pad]
+    double* ph_s = reinterpret_cast<double*>(env_smem + SL.ph);                               // [32]
     const uint32_t bar = smem_u32(env_smem + SL.bar);
 
     const int e = tile * 32 + lane;                 // this lane's env (all four warps)
@@ -143,6 +146,11 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     const bool tma = need_hold && full_tile && a.tma_ok;
 
     // ---- 1. fetch the tile's holdings h_t[n][32] and actions a_t[n][32]: two 2-D TMA boxes
+    const uint32_t chunk_bar = bar + 8u;   // [ENV_BUY_CHUNKS] buy chunk c released by warp 0 (32 arrivals)
+    if (tid == 0 && stepping) {
+        for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(chunk_bar + 8u * c, 32);
+        if (!tma) fence_mbar_init();
+    }
     if (tma && tid == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -223,13 +231,22 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     // ---- 4. the float64 ledger, warp 0, lane = env, in exactly the order of
     //         Eqs. 3-4 under R#3/R#4 (sells, then greedy buys, tickers ascending)
     double cash = cash0;
-    if (warp == 0 && active) {
+    // buy pass in chunks of CH tickers: after each chunk warp 0 releases mbarrier c,
+    // and warps 1-3 (done with the noise) trail it: warp 1 carries the revaluation sum
+    // sum_i p_{t+1,i} h_i (tickers ascending, as the oracle), warps 2-3 write the holdings out
+    // and their part of s_{t+1}, so only the ledger's own chain is left on warp 0
+    const int CH = ((n + ENV_BUY_CHUNKS - 1) / ENV_BUY_CHUNKS + 3) & ~3;   // multiple of the 4-way unroll
+    const int nch = (n + CH - 1) / CH;
+    const float inv_c0 = static_cast<float>(1.0 / a.C0);
+    if (warp == 0) {
         if (a.mode == 2) {
             cash = a.C0;
-            a.cash[e] = a.C0;
-            a.asset[e] = a.C0;
-            a.disc[e] = 0.0;
-            a.ep_ret[e] = 0.0;
+            if (active) {
+                a.cash[e] = a.C0;
+                a.asset[e] = a.C0;
+                a.disc[e] = 0.0;
+                a.ep_ret[e] = 0.0;
+            }
         } else if (stepping) {
             const double omc = __dadd_rn(1.0, -a.cost);
             // selling set (Eq. 3 "+ (p^S)^T k^S"), tickers ascending.  Branch-free: a
@@ -243,7 +260,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 cash = __dadd_rn(cash, __dmul_rn(__dmul_rn(p_t64[i], static_cast<double>(q)), omc));
             }
             if (trc && lane == 0) trc[2] = clock64();
-            // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending, then revalue at p_{t+1}.
+            // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending.
             // The oracle computes qmax = floor(fl(b / unit)) (minus one if fl(qmax unit) > b),
             // q = max(0, min(a, qmax)), b -= fl(q unit).  Here, with y = fl(b fl(1/unit)) and
             // m = floor(y) (y = b/unit (1 +- 2^-51), fl(b/unit) = b/unit (1 +- 2^-53)):
@@ -257,96 +274,103 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             // fr and m are non-negative doubles, compared through their bit patterns (integer
             // compares).  The test is kept off the carried chain: a ticker that fails it (b/unit
             // within ~2^-34 of an integer: rare) only sets a flag, and if any lane of the warp
-            // raised it the whole buy pass is redone below with the oracle's own expressions.
+            // raised it the chunk is redone with the oracle's own expressions before its release.
             constexpr long long FR_LO = 0x3DD0000000000000ll;   // 2^-34
             constexpr long long FR_HI = 0x3FEFFFFFFFF80000ll;   // 1 - 2^-34
-            const double cash_sold = cash;
-            double ph = 0.0;
-            bool unsure = false;
+            for (int c = 0; c < nch; ++c) {
+                const int i0 = c * CH;
+                const int i1 = i0 + CH < n ? i0 + CH : n;
+                const double cash_c0 = cash;
+                bool unsure = false;
 #pragma unroll 4
-            for (int i = 0; i < n; ++i) {
-                const int ai = aint_s[i * 32 + lane];
-                int h = hold_s[i * 32 + lane];
-                if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
-                const double unit = unit_s[i];
-                const double ad = static_cast<double>(ai > 0 ? ai : 0);
-                const double y = __dmul_rn(cash, rcp_s[i]);
-                const double fl = floor(y);
-                const double qd = fl < ad ? fl : ad;
-                const double cost = __dmul_rn(qd, unit);
-                const long long frb = __double_as_longlong(__dadd_rn(y, -fl));
-                unsure |= !(ai <= 0 || __double_as_longlong(fl) > __double_as_longlong(ad) ||
-                            (frb >= FR_LO && frb <= FR_HI));
-                h += static_cast<int>(qd);
-                cash = __dadd_rn(cash, -cost);
-                hold_s[i * 32 + lane] = h;
-                ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
-            }
-            if (__any_sync(__activemask(), unsure)) {
-                // redo: replay the pass above to recover each ticker's post-sell holdings, and run
-                // the oracle's expressions, qmax = floor(fl(b / unit)) (minus one if
-                // fl(qmax unit) > b), q = max(0, min(a+, qmax)), b -= fl(q unit), alongside
-                double bf = cash_sold;
-                cash = cash_sold;
-                ph = 0.0;
-                for (int i = 0; i < n; ++i) {
+                for (int i = i0; i < i1; ++i) {
                     const int ai = aint_s[i * 32 + lane];
+                    int h = hold_s[i * 32 + lane];
+                    if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
                     const double unit = unit_s[i];
                     const double ad = static_cast<double>(ai > 0 ? ai : 0);
-                    const double yf = __dmul_rn(bf, rcp_s[i]);
-                    const double flf = floor(yf);
-                    const double qf = flf < ad ? flf : ad;
-                    bf = __dadd_rn(bf, -__dmul_rn(qf, unit));
-                    const int h_sold = hold_s[i * 32 + lane] - static_cast<int>(qf);
-                    double qmax = floor(__ddiv_rn(cash, unit));
-                    if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
-                    double qd = ad < qmax ? ad : qmax;
-                    qd = qd < 0.0 ? 0.0 : qd;
-                    cash = __dadd_rn(cash, -__dmul_rn(qd, unit));
-                    const int h = h_sold + static_cast<int>(qd);
+                    const double y = __dmul_rn(cash, rcp_s[i]);
+                    const double fl = floor(y);
+                    const double qd = fl < ad ? fl : ad;
+                    const double cost = __dmul_rn(qd, unit);
+                    const long long frb = __double_as_longlong(__dadd_rn(y, -fl));
+                    unsure |= !(ai <= 0 || __double_as_longlong(fl) > __double_as_longlong(ad) ||
+                                (frb >= FR_LO && frb <= FR_HI));
+                    h += static_cast<int>(qd);
+                    cash = __dadd_rn(cash, -cost);
                     hold_s[i * 32 + lane] = h;
-                    ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(h)));
                 }
+                if (__any_sync(0xffffffffu, unsure)) {
+                    // redo the chunk: replay the pass above to recover each ticker's post-sell
+                    // holdings, and run the oracle's expressions alongside
+                    double bf = cash_c0;
+                    cash = cash_c0;
+                    for (int i = i0; i < i1; ++i) {
+                        const int ai = aint_s[i * 32 + lane];
+                        const double unit = unit_s[i];
+                        const double ad = static_cast<double>(ai > 0 ? ai : 0);
+                        const double yf = __dmul_rn(bf, rcp_s[i]);
+                        const double flf = floor(yf);
+                        const double qf = flf < ad ? flf : ad;
+                        bf = __dadd_rn(bf, -__dmul_rn(qf, unit));
+                        const int h_sold = hold_s[i * 32 + lane] - static_cast<int>(qf);
+                        double qmax = floor(__ddiv_rn(cash, unit));
+                        if (__dmul_rn(qmax, unit) > cash) qmax = __dadd_rn(qmax, -1.0);
+                        double qd = ad < qmax ? ad : qmax;
+                        qd = qd < 0.0 ? 0.0 : qd;
+                        cash = __dadd_rn(cash, -__dmul_rn(qd, unit));
+                        hold_s[i * 32 + lane] = h_sold + static_cast<int>(qd);
+                    }
+                }
+                mbar_arrive(chunk_bar + 8u * c);   // release: this lane's holdings of the chunk
             }
             if (trc && lane == 0) trc[3] = clock64();
-            const double v1 = __dadd_rn(cash, ph);
-            const double r = __dmul_rn(a.scale, __dadd_rn(v1, -v0));
-            double disc = __dadd_rn(disc0, __dmul_rn(gpow, r));
-            a.rew[e] = static_cast<float>(r);
-            a.done[e] = done ? 1 : 0;
-            if (a.dbg_cash) a.dbg_cash[e] = cash;
-            if (!isfinite(v1)) atomicOr(a.err, 2u);
-            double v = v1;
-            if (done) {
-                a.ep_ret[e] = disc;
-                cash = a.C0;
-                v = a.C0;
-                disc = 0.0;
-            }
-            a.cash[e] = cash;
-            a.asset[e] = v;
-            a.disc[e] = disc;
         }
-        uint16_t* my = stg + lane * e_pad;
-        my[0] = f2bf(static_cast<float>(cash / a.C0));
-        for (int c = 1 + n; c < e_pad; ++c) my[c] = tmpl[c];
-    }
-    if (warp != 0 && a.gen_noise) {
-        // the actor's Gaussian noise for the next actor launch (R#14: Philox4x32-10 keyed on
-        // (global env, global step, ticker quad)), drawn while warp 0 runs the ledger
-        const uint64_t step = *a.step_base + static_cast<uint64_t>(a.noise_t);
-        const int nq = (n + 3) / 4;
-        for (int idx = tid - 32; idx < 32 * nq; idx += ENV_THREADS - 32) {
-            const int el = idx & 31;
-            const int qd = idx >> 5;
-            const int ee = tile * 32 + el;
-            if (ee < a.N) {
-                const float4 z = normals4(a.seed, static_cast<uint32_t>(a.env_offset + ee), step, static_cast<uint32_t>(qd));
-                const float zz[4] = {z.x, z.y, z.z, z.w};
+    } else {
+        if (a.gen_noise) {
+            // the actor's Gaussian noise for the next actor launch (R#14: Philox4x32-10 keyed on
+            // (global env, global step, ticker quad)), drawn while warp 0 runs the ledger
+            const uint64_t step = *a.step_base + static_cast<uint64_t>(a.noise_t);
+            const int nq = (n + 3) / 4;
+            for (int idx = tid - 32; idx < 32 * nq; idx += ENV_THREADS - 32) {
+                const int el = idx & 31;
+                const int qd = idx >> 5;
+                const int ee = tile * 32 + el;
+                if (ee < a.N) {
+                    const float4 z = normals4(a.seed, static_cast<uint32_t>(a.env_offset + ee), step, static_cast<uint32_t>(qd));
+                    const float zz[4] = {z.x, z.y, z.z, z.w};
+                    float* zp = a.znoise + static_cast<int64_t>(4 * qd) * N + ee;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (4 * qd + j < n) a.znoise[static_cast<int64_t>(4 * qd + j) * N + ee] = zz[j];
+                    for (int j = 0; j < 4; ++j)
+                        if (4 * qd + j < n) zp[static_cast<int64_t>(j) * N] = zz[j];
+                }
             }
+        }
+        if (stepping) {
+            uint16_t* my = stg + lane * e_pad;
+            if (warp == 1) {
+                for (int c = 1 + n; c < e_pad; ++c) my[c] = tmpl[c];
+            }
+            double ph = 0.0;
+            for (int c = 0; c < nch; ++c) {
+                mbar_wait(chunk_bar + 8u * c, 0u);
+                const int i0 = c * CH;
+                const int i1 = i0 + CH < n ? i0 + CH : n;
+                if (warp == 1) {
+                    for (int i = i0; i < i1; ++i)
+                        ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(hold_s[i * 32 + lane])));
+                } else {
+                    for (int i = i0 + (warp - 2); i < i1; i += 2) {
+                        const int h = hold_s[i * 32 + lane];
+                        if (active) {
+                            a.hold[i * N + e] = done ? 0 : h;
+                            if (a.dbg_hold) a.dbg_hold[static_cast<int64_t>(e) * n + i] = h;
+                        }
+                        my[1 + i] = done ? 0 : f2bf(static_cast<float>(h) * p_1[i] * inv_c0);
+                    }
+                }
+            }
+            if (warp == 1) ph_s[lane] = ph;
         }
     }
     if (tid == 0 && stepping) {
@@ -359,23 +383,45 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     }
     __syncthreads();
     if (trc && threadIdx.x == 0) trc[4] = clock64();
-    // ---- 5. holdings out (coalesced rows) and the per-env part of s_{t+1}, 4 warps
-    {
-        const float inv_c0 = static_cast<float>(1.0 / a.C0);
-        const float* p_obs = stepping ? p_1 : p_t;
+    if (stepping) {
+        // revalue at p_{t+1} (Eq. 2 reward), episode bookkeeping, and the cash entry of s_{t+1}
+        if (warp == 0) {
+            const double v1 = __dadd_rn(cash, ph_s[lane]);
+            const double r = __dmul_rn(a.scale, __dadd_rn(v1, -v0));
+            double disc = __dadd_rn(disc0, __dmul_rn(gpow, r));
+            double v = v1;
+            if (active) {
+                a.rew[e] = static_cast<float>(r);
+                a.done[e] = done ? 1 : 0;
+                if (a.dbg_cash) a.dbg_cash[e] = cash;
+                if (!isfinite(v1)) atomicOr(a.err, 2u);
+                if (done) a.ep_ret[e] = disc;
+            }
+            if (done) {
+                cash = a.C0;
+                v = a.C0;
+                disc = 0.0;
+            }
+            if (active) {
+                a.cash[e] = cash;
+                a.asset[e] = v;
+                a.disc[e] = disc;
+            }
+            stg[lane * e_pad] = f2bf(static_cast<float>(cash / a.C0));
+        }
+    } else {
+        // ---- 5. (reset / observe) holdings out and the per-env part of s_t, 4 warps
+        const float* p_obs = p_t;
         uint16_t* my = stg + lane * e_pad;
+        if (warp == 0) {
+            my[0] = f2bf(static_cast<float>(cash / a.C0));
+            for (int c = 1 + n; c < e_pad; ++c) my[c] = tmpl[c];
+        }
 #pragma unroll 5
         for (int i = warp; i < n; i += 4) {
             const int h = a.mode == 2 ? 0 : hold_s[i * 32 + lane];
-            if (active) {
-                if (stepping) {
-                    a.hold[i * N + e] = done ? 0 : h;
-                    if (a.dbg_hold) a.dbg_hold[static_cast<int64_t>(e) * n + i] = h;
-                } else if (a.mode == 2) {
-                    a.hold[i * N + e] = 0;
-                }
-            }
-            my[1 + i] = (done || a.mode == 2) ? 0 : f2bf(static_cast<float>(h) * p_obs[i] * inv_c0);
+            if (active && a.mode == 2) a.hold[i * N + e] = 0;
+            my[1 + i] = a.mode == 2 ? 0 : f2bf(static_cast<float>(h) * p_obs[i] * inv_c0);
         }
     }
     __syncthreads();
