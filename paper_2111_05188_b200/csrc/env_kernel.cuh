@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             }
             double ph = 0.0;
             for (int c = 0; c < nch; ++c) {
-                mbar_wait(chunk_bar + 8u * c, 0u);
+                mbar_wait_parked(chunk_bar + 8u * c, 0u);
                 const int i0 = c * CH;
                 const int i1 = i0 + CH < n ? i0 + CH : n;
                 if (warp == 1) {
