@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         bad |= !isfinite(mu[jj]);
                         raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
                         logp += (-0.5f * z * z - ls) - half_ln_2pi;
-                        const float u = tanhf(raw[jj]);
+                        const float u = tanh_sfu(raw[jj]);
                         const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
                         const int ai = u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m);
                         a.aint[static_cast<int64_t>(i) * a.N + e] = static_cast<int16_t>(ai);
