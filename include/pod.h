@@ -163,9 +163,11 @@ pod_status pod_env_workspace_size(const pod_env_config* cfg, size_t* bytes);
 
 /* Validate cfg (S:L139 invariants: C0 > 0, 0 <= c < 1, h_max >= 1,
  * 0 < gamma <= 1), check the device is sm_100, and bind market + workspace
- * (ws [dev], >= pod_env_workspace_size bytes, 256-byte aligned).  The env
+ * (ws [dev], >= pod_env_workspace_size bytes, 256-byte aligned).  The market
+ * is scanned once on the device (synchronously): every close price must be
+ * finite and > 0 and every indicator finite, else POD_ERR_NONFINITE.  The env
  * state is undefined until pod_env_reset.  Errors: ARG, SHAPE, WORKSPACE,
- * UNSUPPORTED, CUDA. */
+ * UNSUPPORTED, NONFINITE, CUDA. */
 pod_status pod_env_create(const pod_env_config* cfg, const pod_market* market, void* ws,
                           size_t ws_bytes, pod_env_t** out);
 pod_status pod_env_destroy(pod_env_t* env);

@@ -458,6 +458,22 @@ __global__ void inject_map_kernel(const float* __restrict__ u, int N, int n, int
     if (dbg_aint) dbg_aint[idx] = static_cast<int16_t>(ai);
 }
 
+// market validation at env creation: bit 0 = a close price that is not finite and > 0 (the unit
+// price p (1 + c) and its reciprocal must be positive and finite), bit 1 = a non-finite indicator
+__global__ void market_check_kernel(const float* __restrict__ close, int64_t n_close, const float* __restrict__ feat,
+                                    int64_t n_feat, uint32_t* __restrict__ flags) {
+    uint32_t f = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_close; i += stride) {
+        const float p = close[i];
+        if (!(p > 0.0f && p < INFINITY)) f |= 1u;
+    }
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_feat; i += stride)
+        if (!isfinite(feat[i])) f |= 2u;
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
 // J_a = (sum over agent a's envs of ep_ret) / per_agent, one 1024-thread block per agent
 __global__ void __launch_bounds__(1024) fitness_kernel(const double* __restrict__ ep_ret, int per_agent,
                                                        double* __restrict__ out) {

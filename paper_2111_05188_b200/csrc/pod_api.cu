@@ -385,6 +385,25 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         delete e;
         return pod_fail(POD_ERR_CUDA, "pod_env_create: %s", cudaGetErrorString(ce));
     }
+    {
+        // the market must be usable by the float64 ledger: close prices finite and > 0, indicators finite
+        const int64_t nc = static_cast<int64_t>(market->T_data) * cfg->n_stocks;
+        const int64_t nf = static_cast<int64_t>(market->T_data) * cfg->n_feat * cfg->n_stocks;
+        uint32_t flags = 0;
+        market_check_kernel<<<296, 256>>>(market->close, nc, market->feat, nf, e->err);
+        ce = cudaGetLastError();
+        if (ce == cudaSuccess) ce = cudaMemcpy(&flags, e->err, 4, cudaMemcpyDeviceToHost);
+        if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
+        if (ce != cudaSuccess) {
+            pod_env_destroy(e);
+            return pod_fail(POD_ERR_CUDA, "pod_env_create (market check): %s", cudaGetErrorString(ce));
+        }
+        if (flags) {
+            pod_env_destroy(e);
+            return pod_fail(POD_ERR_NONFINITE, "market: %s%s", (flags & 1u) ? "close prices must be finite and > 0 " : "",
+                            (flags & 2u) ? "indicators must be finite" : "");
+        }
+    }
     // 2-D tensor maps over the ticker-major state: one TMA box = one tile's [n][32]
     e->env_tma_ok = (cfg->n_envs % 8 == 0) ? 1 : 0;
     if (e->env_tma_ok) {

@@ -238,6 +238,18 @@ def test_error_paths():
     with pytest.raises(PodError) as ei:
         c.env.rollout(2, tr)                    # neither actor nor injected actions
     assert ei.value.name == "POD_ERR_ARG"
+    cfg = api.make_config(32, 30, 3, 50)
+    for bad_close, bad_feat in ((0.0, None), (float("inf"), None), (float("nan"), None), (None, float("nan"))):
+        close = c.close_d.clone()
+        feat = c.feat_d.clone()
+        if bad_close is not None:
+            close[17, 3] = bad_close                # a zero / infinite price has no unit price reciprocal
+        if bad_feat is not None:
+            feat[5, 1, 2] = bad_feat
+        with pytest.raises(PodError) as ei:
+            api.Env(cfg, close, feat)
+        assert ei.value.name == "POD_ERR_NONFINITE"
+    api.Env(cfg, c.close_d, c.feat_d)           # the clean market is accepted
 
 
 # ----------------------------------------------------------------- full size (bench launch config)
