@@ -155,8 +155,9 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def oracle_step_sample(w, market, weights_flat, n_envs, T, nthreads, starts):
-    """One bounded oracle pass of the hot path (rollout incl. actor, GAE, fitness, select)."""
+def oracle_step_sample(w, market, weights_flat, n_envs, T, nthreads, starts, critic):
+    """One bounded oracle pass of the hot path (rollout incl. actor and critic, GAE on the critic's
+    values with V(s_T) as bootstrap, fitness, select)."""
     import numpy as np
 
     import oracle
@@ -166,9 +167,8 @@ def oracle_step_sample(w, market, weights_flat, n_envs, T, nthreads, starts):
     env.reset(starts[:n_envs])
     t0 = time.perf_counter()
     out = env.rollout(T, "sample", weights=weights_flat[None, :], n_hidden=w.n_hidden, hidden=w.hidden,
-                      nthreads=nthreads, want=("rew", "done"))
-    v = np.zeros((T, n_envs))
-    oracle.gae(out["rew"], v, out["done"], np.zeros(n_envs), w.gamma, w.lam)
+                      nthreads=nthreads, want=("rew", "done", "val"), critic=critic[None, :])
+    oracle.gae(out["rew"], out["val"][:T], out["done"], out["val"][T], w.gamma, w.lam)
     J = oracle.fitness(env.ep_ret, 1)
     oracle.select_elite(J, 1)
     return time.perf_counter() - t0
@@ -188,18 +188,19 @@ def run_reference(args, w, rank, world):
     market = synth.make_market(w.n_stocks, T_data, w.dt, w.seed, n_feat=w.n_feat)
     aw = synth.make_actor(w.obs_dim, w.n_hidden, w.hidden, w.n_stocks, w.seed * 1000)
     wf = oracle.actor_flat(aw.W, aw.b, aw.log_std)
+    wcr = np.append(aw.w_v.astype(np.float64), aw.b_v)
     H = min(w.horizon, T_data - 2)
     starts = np.repeat(synth.tile_starts((4096 + 31) // 32, T_data, H, w.seed + 1), 32)
     cores = cpu_cores()
     # size one step to ~3 s of wall time: calibrate on one step of `cores` envs
     Ts = min(w.T, 8)
-    t1 = oracle_step_sample(w, market, wf, cores, 1, cores, starts)
+    t1 = oracle_step_sample(w, market, wf, cores, 1, cores, starts, wcr)
     per_env_step = t1 / cores * cores  # wall s per (env-step) x cores
     n_envs = int(max(cores, min(4096, (3.0 / max(per_env_step, 1e-9)) * cores / Ts)))
     n_envs = max(cores, n_envs // cores * cores)
     for _ in range(args.warmup):
-        oracle_step_sample(w, market, wf, n_envs, Ts, cores, starts)
-    times = [oracle_step_sample(w, market, wf, n_envs, Ts, cores, starts) for _ in range(args.steps)]
+        oracle_step_sample(w, market, wf, n_envs, Ts, cores, starts, wcr)
+    times = [oracle_step_sample(w, market, wf, n_envs, Ts, cores, starts, wcr) for _ in range(args.steps)]
     tot = sum(times)
     value = n_envs * Ts * args.steps / tot
     sample = (f"{n_envs} envs x {Ts} steps of workload {w.name} per step (market truncated to {T_data} rows; "
@@ -279,11 +280,11 @@ def main():
     agents = [synth.make_actor(env.obs_dim, w.n_hidden, w.hidden, n, w.seed * 1000 + rank * P + a) for a in range(P)]
     params = api.pack_actor_params(cfg, agents, w.n_hidden, w.hidden, device=dev)
     actor = api.make_actor(w.n_hidden, w.hidden, params)
-    traj = api.Trajectory.allocate(T, N, n, env.k_pad, device=dev)
-    g = torch.Generator(device=dev)
-    g.manual_seed(w.seed + 17 + rank)
-    val = torch.randn((T, N), generator=g, device=dev)      # critic values: caller input (§8(f) row 1 is next)
-    boot = torch.randn(N, generator=g, device=dev)
+    # the critic (head row n over the actor trunk, R#21) writes V(s_t) for t = 0..T during the rollout:
+    # GAE consumes it on device, V(s_T) is the bootstrap
+    traj = api.Trajectory.allocate(T, N, n, env.k_pad, device=dev, critic=True)
+    val = traj.val[:T]
+    boot = traj.val[T]
     adv = torch.empty_like(val)
     ret = torch.empty_like(val)
     fit = torch.empty(P, dtype=torch.float64, device=dev)
@@ -344,16 +345,12 @@ def main():
     if not args.no_e2e:
         env.profile(0)
         h_params = params.cpu().pin_memory()
-        h_val = val.cpu().pin_memory()
-        h_boot = boot.cpu().pin_memory()
         h_fit = torch.empty(P, dtype=torch.float64).pin_memory()
-        bi = h_params.numel() * h_params.element_size() + h_val.numel() * 4 + h_boot.numel() * 4
+        bi = h_params.numel() * h_params.element_size()
         bo = h_fit.numel() * 8
 
         def e2e_step():
             params.copy_(h_params, non_blocking=True)
-            val.copy_(h_val, non_blocking=True)
-            boot.copy_(h_boot, non_blocking=True)
             env.rollout(T, traj, actor=actor)
             api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret)
             env.fitness(fit)
@@ -425,16 +422,17 @@ def main():
             oracle.build()
             cores = cpu_cores()
             wf = oracle.actor_flat(agents[0].W, agents[0].b, agents[0].log_std)
+            wcr = np.append(agents[0].w_v.astype(np.float64), agents[0].b_v)
             env_starts = np.repeat(starts, 32)[:N]
             Ts = 4
-            t1s = oracle_step_sample(w, market, wf, cores, 1, cores, env_starts)
+            t1s = oracle_step_sample(w, market, wf, cores, 1, cores, env_starts, wcr)
             n_s = int(min(N, max(cores, (15.0 / max(t1s, 1e-9)) * cores / Ts)))
             n_s = max(cores, n_s // cores * cores)
-            tt = oracle_step_sample(w, market, wf, n_s, Ts, cores, env_starts)
+            tt = oracle_step_sample(w, market, wf, n_s, Ts, cores, env_starts, wcr)
             cpu = {"value": n_s * Ts / tt, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": f"{n_s} envs x {Ts} steps of {w.name} (float64 actor {w.n_hidden}x{w.hidden} + env "
                              f"step + GAE + fitness + select), OpenMP over envs, {tt:.1f} s"}
-        launches_per_step = 1 + 2 * T + 1 + 1 + 1   # obs0, T x (actor, env), step bump, gae, fitness
+        launches_per_step = 1 + 2 * T + 1 + 1 + 1 + 1   # obs0, T x (actor, env), V(s_T) pass, step bump, gae, fitness
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define POD_ABI_VERSION 1
+#define POD_ABI_VERSION 2
 #define POD_ENV_TILE 32      /* envs per tile: one warp; a tile shares its episode start row */
 #define POD_MAX_HIDDEN_LAYERS 4
 
@@ -118,7 +118,8 @@ typedef struct {
 typedef struct {
     int32_t obs_dim;       /* 1 + 2n + n f                                   */
     int32_t k_pad;         /* obs_dim rounded up to 64 (obs row stride)       */
-    int32_t n_out_pad;     /* n rounded up to 16 (head rows)                  */
+    int32_t n_out_pad;     /* n + 1 rounded up to 32 (head rows: 0..n-1 the  *
+                            * action means, row n the critic V, R#21)         */
     int32_t n_layers;      /* n_hidden + 1                                    */
     size_t w_offset[POD_MAX_HIDDEN_LAYERS + 1];   /* bytes, bf16 [out_l][in_l] */
     int32_t w_rows[POD_MAX_HIDDEN_LAYERS + 1];    /* out_l (padded)            */
@@ -138,7 +139,11 @@ typedef struct {
  *   mu       f32  [T][N][n]        actor mean                             (optional, NULL)
  *   dbg_aint i16  [T][N][n]        executed integer action a_t            (optional)
  *   dbg_hold i32  [T][N][n]        h_{t+1} after the trade, before reset  (optional)
- *   dbg_cash f64  [T][N]           b_{t+1} after the trade, before reset  (optional) */
+ *   dbg_cash f64  [T][N]           b_{t+1} after the trade, before reset  (optional)
+ *   val      f32  [T+1][N]         critic V(s_t), t = 0..T: head row n over the
+ *                                  actor's trunk (R#21); val[T] = V(s_T), the
+ *                                  GAE bootstrap, from one extra value-only
+ *                                  actor pass.  Feeds pod_gae directly.  (optional) */
 typedef struct {
     uint16_t* obs;
     float* act;
@@ -149,6 +154,7 @@ typedef struct {
     int16_t* dbg_aint;
     int32_t* dbg_hold;
     double* dbg_cash;
+    float* val;
 } pod_traj;
 
 /* ---------------------------------------------------------------- layout */
@@ -193,6 +199,9 @@ pod_status pod_env_reset(pod_env_t* env, const int64_t* tile_start_rows, uint16_
  *      r = scale (v' - v), done = (k+1 == H) or (t+1 == T_data-1), auto-reset
  *      with the terminal transition reported;
  *   3. s_{t+1} written to obs[t+1].
+ * With traj.val (sampled or deterministic mode), step t also writes the critic
+ * value V(s_t) from the same MLP pass (head row n), and one value-only actor
+ * pass over obs[T] writes val[T].
  * obs[0] is first written from the carried state, so buffers need not persist
  * across calls; obs[T] is the bootstrap state.  fitness_out [dev] f64
  * [n_agents] or NULL: afterwards J_a = mean over agent a's envs of the

@@ -66,7 +66,9 @@ def lib():
         L.orc_sample.argtypes = [i, vp, vp, vp, i, vp, vp]
         L.orc_sample.restype = d
         L.orc_rollout.argtypes = [C.POINTER(_Cfg), vp, vp, C.POINTER(_State), i, i, vp, vp, vp, i, i, i,
-                                  u64, vp, vp, vp, vp, vp, vp, vp, vp, vp, i]
+                                  u64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i]
+        L.orc_critic_value.argtypes = [vp, i, i, vp]
+        L.orc_critic_value.restype = d
         L.orc_rollout.restype = i64
         L.orc_gae.argtypes = [i, i, vp, vp, vp, vp, d, d, vp, vp, vp]
         L.orc_fitness.argtypes = [i, i, vp, vp]
@@ -119,6 +121,17 @@ def actor_mu(w_flat: np.ndarray, obs: np.ndarray, n_hidden: int, hidden: int, n:
     for r in range(B):
         lib().orc_actor_mu(_p(w_flat), od, n_hidden, hidden, n, act, _p(obs[r]), _p(mu[r]), _p(scratch))
     return mu
+
+
+def actor_value(W, b, w_v, b_v, obs: np.ndarray, n_hidden: int, hidden: int, act: int = 0) -> np.ndarray:
+    """Critic V(s) = w_v . h_L(s) + b_v on the actor's trunk h_L ("shared trunk -> actor head +
+    critic head"; R#21), for each row of obs [B, obs_dim] (float64).  Evaluated by the same
+    MLP routine as the actor mean, with the value row appended to the head."""
+    n = int(np.asarray(W[-1]).shape[0])
+    W_h = np.vstack([np.asarray(W[-1], dtype=np.float64), np.asarray(w_v, dtype=np.float64)[None, :]])
+    b_h = np.append(np.asarray(b[-1], dtype=np.float64), float(b_v))
+    flat = actor_flat(list(W[:-1]) + [W_h], list(b[:-1]) + [b_h], np.zeros(n + 1))
+    return actor_mu(flat, obs, n_hidden, hidden, n + 1, act)[:, n]
 
 
 def sample(mu, log_std, z, deterministic=False):
@@ -185,9 +198,10 @@ class Env:
         return float(self.cash[e] + np.dot(self.close[t].astype(np.float64), self.hold[e].astype(np.float64)))
 
     def rollout(self, T, mode="inject", u=None, a_rep=None, weights=None, n_hidden=0, hidden=0, act=0,
-                step0=0, nthreads=1, want=("obs", "rew", "done")):
+                step0=0, nthreads=1, want=("obs", "rew", "done"), critic=None):
         """mode: inject (u [T,N,n] f32), replay (a_rep [T,N,n] i16), sample, deterministic.
-        weights: [n_agents, count] float64 (actor_flat per agent)."""
+        weights: [n_agents, count] float64 (actor_flat per agent).  critic: [n_agents, hidden+1] float64
+        (w_v, b_v per agent, R#21); with "val" in want, V(s_t) for t = 0..T in sample/deterministic mode."""
         N, n, od = self.N, self.n, self.obs_dim
         modes = {"inject": 0, "replay": 1, "sample": 2, "deterministic": 3}
         out = {}
@@ -207,13 +221,15 @@ class Env:
         a_out = buf("a_int", (T, N, n), np.int32)
         hold_out = buf("hold", (T, N, n), np.int32)
         cash_out = buf("cash", (T, N), np.float64)
+        val = buf("val", (T + 1, N), np.float64)
+        cr = None if critic is None else np.ascontiguousarray(critic, dtype=np.float64)
         u = None if u is None else np.ascontiguousarray(u, dtype=np.float32)
         a_rep = None if a_rep is None else np.ascontiguousarray(a_rep, dtype=np.int16)
         w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
         ties = lib().orc_rollout(C.byref(self.cfg), _p(self.close), _p(self.feat), C.byref(self._st), int(T),
                                  modes[mode], _p(u), _p(a_rep), _p(w), int(n_hidden), int(hidden), int(act),
                                  int(step0), _p(obs), _p(mu), _p(raw), _p(logp), _p(rew), _p(done), _p(a_out),
-                                 _p(hold_out), _p(cash_out), int(nthreads))
+                                 _p(hold_out), _p(cash_out), _p(cr), _p(val), int(nthreads))
         out["near_ties"] = int(ties)
         return out
 

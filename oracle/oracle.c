@@ -262,6 +262,17 @@ void orc_actor_mu(const double* w, int obs_dim, int n_hidden, int hidden, int n,
     }
 }
 
+/* Critic ("shared trunk -> actor head + critic head", R#21):
+ * V = w_v . h_L + b_v, where h_L is the last hidden layer that orc_actor_mu
+ * leaves in scratch (x after n_hidden swaps), summed in the head's order.
+ * critic = [w_v (hidden), b_v].                                              */
+double orc_critic_value(const double* critic, int n_hidden, int hidden, const double* scratch) {
+    const double* h = scratch + ((n_hidden % 2) ? hidden : 0);
+    double s = 0.0;
+    for (int i = 0; i < hidden; ++i) s = s + critic[i] * h[i];
+    return s + critic[hidden];
+}
+
 /* Gaussian policy head (R#12): raw = mu + exp(log_std) z,
  * log pi(raw) = sum_i (-z_i^2/2 - log_std_i - ln(2 pi)/2), u = tanh(raw).
  * deterministic: z = 0.                                                      */
@@ -296,7 +307,7 @@ int64_t orc_rollout(const orc_cfg* c, const float* close, const float* feat, orc
                     const double* weights, int n_hidden, int hidden, int act, uint64_t step0,
                     double* obs, double* mu_out, double* raw_out, double* logp_out,
                     double* rew_out, uint8_t* done_out, int32_t* a_out, int32_t* hold_out,
-                    double* cash_out, int nthreads) {
+                    double* cash_out, const double* critic, double* val_out, int nthreads) {
     const int N = c->n_envs, n = c->n_stocks, f = c->n_feat;
     const int od = 1 + 2 * n + n * f;
     const int64_t wcount = orc_actor_weight_count(od, n_hidden, hidden, n);
@@ -326,6 +337,9 @@ int64_t orc_rollout(const orc_cfg* c, const float* close, const float* feat, orc
                 for (int i = 0; i < n; ++i) a[i] = (int32_t)a_rep[te * n + i];
             } else {
                 orc_actor_mu(w, od, n_hidden, hidden, n, act, o, mu, scratch);
+                if (critic && val_out)
+                    val_out[te] = orc_critic_value(critic + (int64_t)(e / per_agent) * (hidden + 1), n_hidden,
+                                                   hidden, scratch);
                 orc_normals(c->seed, c->env_offset + e, step0 + (uint64_t)t, n, z);
                 const double* log_std = w + wcount - n;
                 lp = orc_sample(n, mu, log_std, z, mode == 3, raw, u);
@@ -345,6 +359,11 @@ int64_t orc_rollout(const orc_cfg* c, const float* close, const float* feat, orc
             if (done_out) done_out[te] = (uint8_t)d;
             orc_obs(c, close, feat, st, e, o);
             if (obs) memcpy(obs + ((int64_t)(t + 1) * N + e) * od, o, sizeof(double) * (size_t)od);
+        }
+        if (mode >= 2 && critic && val_out) {   /* bootstrap V(s_T) */
+            orc_actor_mu(w, od, n_hidden, hidden, n, act, o, mu, scratch);
+            val_out[(int64_t)T * N + e] =
+                orc_critic_value(critic + (int64_t)(e / per_agent) * (hidden + 1), n_hidden, hidden, scratch);
         }
         free(o); free(mu); free(scratch); free(a);
     }

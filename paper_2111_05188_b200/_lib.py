@@ -45,7 +45,7 @@ class ActorLayout(C.Structure):
 class Traj(C.Structure):
     _fields_ = [("obs", C.c_void_p), ("act", C.c_void_p), ("logp", C.c_void_p), ("rew", C.c_void_p),
                 ("done", C.c_void_p), ("mu", C.c_void_p), ("dbg_aint", C.c_void_p), ("dbg_hold", C.c_void_p),
-                ("dbg_cash", C.c_void_p)]
+                ("dbg_cash", C.c_void_p), ("val", C.c_void_p)]
 
 
 class Transfer(C.Structure):

@@ -67,8 +67,16 @@ def pack_actor_params(cfg: _lib.EnvConfig, agents: Sequence, n_hidden: int, hidd
             raw = Wp.view(torch.uint8).numpy().ravel()
             o = int(L.w_offset[l])
             slab[a, o : o + raw.size] = raw
+            if l == L.n_layers - 1 and getattr(w, "w_v", None) is not None:
+                # critic: head row n (R#21)
+                Wp[cfg.n_stocks, : w.w_v.size] = torch.from_numpy(np.ascontiguousarray(w.w_v, np.float32)).to(torch.bfloat16)
+                raw = Wp.view(torch.uint8).numpy().ravel()
+                o = int(L.w_offset[l])
+                slab[a, o : o + raw.size] = raw
             bp = np.zeros(rows, dtype=np.float32)
             bp[: w.b[l].size] = w.b[l]
+            if l == L.n_layers - 1 and getattr(w, "w_v", None) is not None:
+                bp[cfg.n_stocks] = np.float32(w.b_v)
             o = int(L.b_offset[l])
             slab[a, o : o + 4 * rows] = bp.view(np.uint8)
         ls = np.zeros(L.n_out_pad, dtype=np.float32)
@@ -89,9 +97,11 @@ class Trajectory:
     dbg_aint: Optional[torch.Tensor] = None
     dbg_hold: Optional[torch.Tensor] = None
     dbg_cash: Optional[torch.Tensor] = None
+    val: Optional[torch.Tensor] = None    # f32 [T+1, N] critic V(s_t) (R#21)
 
     @staticmethod
-    def allocate(T: int, N: int, n: int, k_pad: int, device="cuda", debug=False, mu=False, sampled=True):
+    def allocate(T: int, N: int, n: int, k_pad: int, device="cuda", debug=False, mu=False, sampled=True,
+                 critic=False):
         z = dict(device=device)
         return Trajectory(
             obs=torch.empty((T + 1, N, k_pad), dtype=torch.bfloat16, **z),
@@ -103,12 +113,13 @@ class Trajectory:
             dbg_aint=torch.empty((T, N, n), dtype=torch.int16, **z) if debug else None,
             dbg_hold=torch.empty((T, N, n), dtype=torch.int32, **z) if debug else None,
             dbg_cash=torch.empty((T, N), dtype=torch.float64, **z) if debug else None,
+            val=torch.empty((T + 1, N), dtype=torch.float32, **z) if critic and sampled else None,
         )
 
     def c(self) -> _lib.Traj:
         return _lib.Traj(*[None if x is None else x.data_ptr() for x in
                            (self.obs, self.act, self.logp, self.rew, self.done, self.mu, self.dbg_aint,
-                            self.dbg_hold, self.dbg_cash)])
+                            self.dbg_hold, self.dbg_cash, self.val)])
 
 
 class Env:

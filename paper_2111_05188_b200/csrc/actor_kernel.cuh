@@ -67,6 +67,7 @@ struct ActorArgs {
     int32_t obs_row0;        // row of obs[t][0] in the obs tensor map = t * N
     int32_t mtile0;          // first 128-env M-tile of this launch (env groups)
     int32_t mc;              // 1: 4-CTA clusters (2 M-tiles) share weight tiles by TMA multicast
+    int32_t value_only;      // 1: only the critic V (head row n) is written (bootstrap pass over obs[T])
     uint64_t seed;
     int64_t env_offset;
     const uint64_t* step_base;   // device step counter of the handle
@@ -80,6 +81,7 @@ struct ActorArgs {
     int16_t* aint;       // [n][N] scratch
     int16_t* dbg_aint;   // [N][n] or null
     const float* znoise; // [n][N] N(0,1) noise for this step (written by the previous env-step launch)
+    float* val_out;      // [N] critic V(s_t) = head row n (R#21), or null
     uint32_t* err;
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
 };
@@ -378,7 +380,15 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             __syncwarp();
             tmem_ld8(trow + (static_cast<uint32_t>(L) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
             tmem_ld_wait();
-            if (valid && i0 < a.n) {
+            if (valid && i0 <= a.n && a.val_out && a.n < i0 + 8) {
+                // critic: head row n over the same trunk (R#21)
+                float vh = 0.0f;
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj)
+                    if (i0 + jj == a.n) vh = __uint_as_float(hv[jj]);
+                a.val_out[e] = vh + bias[tc + (a.n - i0)];
+            }
+            if (valid && i0 < a.n && !a.value_only) {
                 float raw[8], mu[8];
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         const int e = env0 + r;
-        if ((ew >> 2) == 0 && r < rows_valid && e < a.N)
+        if ((ew >> 2) == 0 && r < rows_valid && e < a.N && a.logp_out)
             a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
     }
     if (warp == 0) {

@@ -131,7 +131,8 @@ static pod_status dims_of(const pod_env_config* c, int* obs_dim, int* k_pad, int
     if (c->n_stocks < 1 || c->n_feat < 0) return pod_fail(POD_ERR_ARG, "n_stocks >= 1 and n_feat >= 0 required");
     *obs_dim = 1 + 2 * c->n_stocks + c->n_stocks * c->n_feat;
     *k_pad = static_cast<int>(round_up(static_cast<size_t>(*obs_dim), 64));
-    *n_out_pad = static_cast<int>(round_up(static_cast<size_t>(c->n_stocks), 32));
+    // head rows: the n action means, then the critic V in row n (R#21), padded to the 32-row MMA granule
+    *n_out_pad = static_cast<int>(round_up(static_cast<size_t>(c->n_stocks) + 1, 32));
     if (*k_pad > ENV_MAX_KPAD || c->n_stocks > ENV_MAX_STOCKS)
         return pod_fail(POD_ERR_UNSUPPORTED, "obs_dim %d exceeds the kernel limit (k_pad <= %d, n <= %d)", *obs_dim,
                         ENV_MAX_KPAD, ENV_MAX_STOCKS);
@@ -148,7 +149,7 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
         return pod_fail(POD_ERR_UNSUPPORTED, "n_hidden must be in [1, %d]", POD_MAX_HIDDEN_LAYERS);
     if (!(hidden == 128 || hidden == 256 || hidden == 512))
         return pod_fail(POD_ERR_UNSUPPORTED, "hidden must be one of 128, 256, 512");
-    if (nop > 128) return pod_fail(POD_ERR_UNSUPPORTED, "n_stocks > 128");
+    if (nop > 128) return pod_fail(POD_ERR_UNSUPPORTED, "n_stocks + 1 > 128");
     memset(out, 0, sizeof(*out));
     out->obs_dim = od;
     out->k_pad = kp;
@@ -178,7 +179,7 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
 
 struct GraphKey {
     int32_t T, deterministic, n_hidden, hidden, act, profile;
-    const void* ptrs[12];
+    const void* ptrs[13];
     size_t param_bytes;
 };
 
@@ -542,6 +543,29 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
                                      cudaEventRecordExternal);
     };
     const int sampling = (!p.injected && !p.aa.deterministic) ? 1 : 0;
+    auto launch_actor = [&](ActorArgs& aa) {
+        // one 2-CTA cluster per 128-env tile (column split of every layer)
+        cudaLaunchConfig_t lc{};
+        const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
+        // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
+        // every agent has an even number of full M-tiles and so does this launch
+        aa.mc = (!p.pair && e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
+        lc.gridDim = dim3(static_cast<unsigned>(2 * mtiles));
+        lc.blockDim = dim3(ACT_THREADS);
+        lc.dynamicSmemBytes = p.actor_smem;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (aa.mc || p.pair) ? 4 : 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        if (p.pair)
+            cudaLaunchKernelEx(&lc, actor_pair_kernel, p.maps, aa);
+        else
+            cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
+    };
     EnvArgs a0 = env_args(e, 1);
     a0.tile0 = t0;
     a0.obs_out = tr->obs;
@@ -564,27 +588,8 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
             aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
             aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
-            // one 2-CTA cluster per 128-env tile (column split of every layer)
-            cudaLaunchConfig_t lc{};
-            const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
-            // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
-            // every agent has an even number of full M-tiles and so does this launch
-            aa.mc = (!p.pair && e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
-            lc.gridDim = dim3(static_cast<unsigned>(2 * mtiles));
-            lc.blockDim = dim3(ACT_THREADS);
-            lc.dynamicSmemBytes = p.actor_smem;
-            lc.stream = s;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = (aa.mc || p.pair) ? 4 : 2;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            if (p.pair)
-                cudaLaunchKernelEx(&lc, actor_pair_kernel, p.maps, aa);
-            else
-                cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
+            aa.val_out = tr->val ? tr->val + static_cast<int64_t>(t) * N : nullptr;
+            launch_actor(aa);
         }
         mark(t, 1);
         mark(t, 2);
@@ -599,6 +604,21 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         a.noise_t = t + 1;
         env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
         mark(t, 3);
+    }
+    if (!p.injected && tr->val) {
+        // critic bootstrap V(s_T): one value-only pass of the actor over obs[T] (no sampling, no action)
+        ActorArgs aa = p.aa;
+        aa.t = T;
+        aa.obs_row0 = T * N;
+        aa.mtile0 = m0;
+        aa.value_only = 1;
+        aa.deterministic = 1;
+        aa.act_out = nullptr;
+        aa.logp_out = nullptr;
+        aa.mu_out = nullptr;
+        aa.dbg_aint = nullptr;
+        aa.val_out = tr->val + static_cast<int64_t>(T) * N;
+        launch_actor(aa);
     }
 }
 
@@ -672,7 +692,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             // the 2-SM (cta_group::2) variant: opt-in — its MMA phase is faster but its
             // epilogue/synchronisation currently costs more than it saves (measured)
             const char* pp = getenv("POD_PAIR");
-            p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1';
+            p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1' && !tr->val;   // pair kernel: no critic output
         }
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
@@ -736,8 +756,8 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         key.ptrs[0] = actor->params;
     }
     const void* ptrs[] = {tr->obs, tr->act, tr->logp, tr->rew, tr->done, tr->mu, tr->dbg_aint,
-                          tr->dbg_hold, tr->dbg_cash, injected_u, fitness_out};
-    for (int i = 0; i < 11; ++i) key.ptrs[1 + i] = ptrs[i];
+                          tr->dbg_hold, tr->dbg_cash, injected_u, fitness_out, tr->val};
+    for (int i = 0; i < 12; ++i) key.ptrs[1 + i] = ptrs[i];
     GraphEntry* hit = nullptr;
     for (auto& g : e->graphs)
         if (memcmp(&g.key, &key, sizeof(key)) == 0) hit = &g;

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 from scipy.signal import lfilter
@@ -182,10 +183,13 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
 class ActorWeights:
     """One agent's actor: layers W[l] [out, in] (bf16-representable float32),
     b[l] [out] float32, log_std [n] float32.  Layer 0 has in = obs_dim, the
-    hidden layers in = hidden, the head out = n."""
+    hidden layers in = hidden, the head out = n.  Critic (R#21): V(s) =
+    w_v . h_L(s) + b_v on the same trunk (w_v [hidden] bf16-representable)."""
     W: list
     b: list
     log_std: np.ndarray
+    w_v: Optional[np.ndarray] = None
+    b_v: float = 0.0
 
 
 def make_actor(obs_dim: int, n_hidden: int, hidden: int, n: int, seed: int,
@@ -199,7 +203,10 @@ def make_actor(obs_dim: int, n_hidden: int, hidden: int, n: int, seed: int,
         Ws.append(bf16_round(W.astype(np.float32)))
         bs.append((rng.standard_normal(fan_out) * bias_scale).astype(np.float32))
     ls = np.full(n, log_std, dtype=np.float32)
-    return ActorWeights(W=Ws, b=bs, log_std=ls)
+    # critic row, drawn after the actor's so the actor weights do not depend on it
+    w_v = bf16_round((rng.standard_normal(dims[-2]) / math.sqrt(dims[-2])).astype(np.float32))
+    b_v = float(np.float32(rng.standard_normal() * bias_scale))
+    return ActorWeights(W=Ws, b=bs, log_std=ls, w_v=w_v, b_v=b_v)
 
 
 # ---------------------------------------------------------------------------

@@ -367,3 +367,50 @@ def test_pair_kernel_matches_single_cta_kernel(monkeypatch):
     mu0 = outs[0].mu.cpu().numpy().astype(np.float64)
     mu1 = outs[1].mu.cpu().numpy().astype(np.float64)
     np.testing.assert_allclose(mu1, mu0, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("n,nh,hid", [(100, 3, 512), (30, 2, 128), (32, 2, 256)])
+def test_critic_value_parity(n, nh, hid):
+    """R#21: V(s_t) = head row n over the trunk, written per step; V(s_T) by the value-only pass.
+    Compared with the oracle's float64 forward on the GPU's own bf16 observations (the actor bar);
+    the actor's own outputs are bit-identical with and without the critic output."""
+    outs = []
+    for critic in (False, True):
+        c = Case(n=n, f=3, T_data=600, N=256, H=7, seed=31)
+        aws, params, actor = _actor(c, nh, hid)
+        tr = api.Trajectory.allocate(9, c.N, c.n, c.k_pad, debug=True, critic=critic)
+        c.env.reset(c.starts)
+        c.env.rollout(9, tr, actor=actor)
+        c.env.check()
+        outs.append(tr)
+    for name in ("obs", "act", "logp", "mu", "rew", "done", "dbg_hold"):
+        assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
+    tr = outs[1]
+    obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
+    val_g = tr.val.cpu().numpy().astype(np.float64)
+    aw = aws[0]
+    for t in range(10):
+        v_o = oracle.actor_value(aw.W, aw.b, aw.w_v, aw.b_v, obs_g[t], nh, hid)
+        rms = math.sqrt(float(np.mean(v_o ** 2)))
+        assert np.all(np.abs(val_g[t] - v_o) <= 2e-2 * (np.abs(v_o) + rms)), t
+    # the device values feed GAE directly (bootstrap = val[T])
+    adv, ret = api.pod_gae(tr.rew, tr.val[:-1].contiguous(), tr.done, tr.val[-1].contiguous(), 0.99, 0.95)
+    adv_o, ret_o, mag = oracle.gae(tr.rew.cpu().numpy(), val_g[:-1], tr.done.cpu().numpy(), val_g[-1], 0.99, 0.95)
+    gae_check(adv, ret, adv_o, ret_o, mag)
+
+
+def test_critic_deterministic_and_graph_reuse():
+    """Critic output in deterministic mode, and across repeated (graph-cached) rollouts."""
+    c = Case(n=30, f=3, T_data=400, N=96, H=50, seed=32)
+    aws, params, actor = _actor(c, 2, 128)
+    tr = api.Trajectory.allocate(4, c.N, c.n, c.k_pad, critic=True)
+    c.env.reset(c.starts)
+    vals = []
+    for _ in range(3):
+        c.env.rollout(4, tr, actor=actor, deterministic=True)
+        vals.append(tr.val.clone())
+    obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
+    v_o = np.stack([oracle.actor_value(aws[0].W, aws[0].b, aws[0].w_v, aws[0].b_v, obs_g[t], 2, 128) for t in range(5)])
+    rms = math.sqrt(float(np.mean(v_o ** 2)))
+    assert np.all(np.abs(vals[-1].cpu().numpy() - v_o) <= 2e-2 * (np.abs(v_o) + rms))
+    assert not torch.equal(vals[0], vals[1])   # the envs moved on between calls

@@ -29,7 +29,7 @@ def test_exports_match_header():
     L = _lib.load()
     for name in declared:
         assert hasattr(L, name), name
-    assert L.pod_abi_version() == 1
+    assert L.pod_abi_version() == 2
     assert L.pod_status_string(3) == b"POD_ERR_RANGE"
 
 
@@ -67,9 +67,14 @@ def test_pack_actor_params_roundtrip():
         raw = slab[L.w_offset[l] : L.w_offset[l] + rows * cols * 2].view(np.uint16).astype(np.uint32) << 16
         W = raw.view(np.float32).reshape(rows, cols)
         np.testing.assert_array_equal(W[: aw.W[l].shape[0], : aw.W[l].shape[1]], aw.W[l])
-        assert not W[aw.W[l].shape[0]:].any() and not W[:, aw.W[l].shape[1]:].any()
         b = slab[L.b_offset[l] : L.b_offset[l] + rows * 4].view(np.float32)
         np.testing.assert_array_equal(b[: aw.b[l].size], aw.b[l])
+        r0 = aw.W[l].shape[0]
+        if l == 2:   # head row n = the critic (R#21)
+            np.testing.assert_array_equal(W[r0, : aw.w_v.size], aw.w_v)
+            assert b[r0] == np.float32(aw.b_v)
+            r0 += 1
+        assert not W[r0:].any() and not W[:, aw.W[l].shape[1]:].any() and not b[r0:].any()
     ls = slab[L.log_std_offset : L.log_std_offset + 32 * 4].view(np.float32)
     np.testing.assert_array_equal(ls[:30], aw.log_std)
 

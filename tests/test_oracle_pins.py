@@ -289,6 +289,43 @@ def test_actor_matches_numpy_matmul(act):
     np.testing.assert_allclose(mu, ref, rtol=1e-12, atol=1e-12)
 
 
+def test_critic_value_pins():
+    """R#21: V = w_v . h_L + b_v on the actor's trunk.  Pins: a zero trunk gives V = b_v exactly; a
+    general trunk equals a numpy float64 forward; the actor mean is unaffected by the critic row."""
+    od, nh, H, n = 9, 2, 8, 3
+    W = [np.zeros((H, od)), np.zeros((H, H)), np.zeros((n, H))]
+    b = [np.zeros(H), np.zeros(H), np.zeros(n)]
+    x = np.random.default_rng(4).normal(size=(5, od))
+    np.testing.assert_array_equal(oracle.actor_value(W, b, np.ones(H), -0.75, x, nh, H), np.full(5, -0.75))
+    for act in (0, 1):
+        aw = synth.make_actor(23, 3, 16, 5, seed=6, bias_scale=0.3)
+        x = np.random.default_rng(7).normal(size=(6, 23))
+        v = oracle.actor_value(aw.W, aw.b, aw.w_v, aw.b_v, x, 3, 16, act)
+        h = x
+        f = (lambda z: np.maximum(z, 0.0)) if act == 0 else np.tanh
+        for l in range(3):
+            h = f(h @ aw.W[l].astype(np.float64).T + aw.b[l].astype(np.float64))
+        np.testing.assert_allclose(v, h @ aw.w_v.astype(np.float64) + aw.b_v, rtol=1e-12, atol=1e-12)
+        mu = oracle.actor_mu(oracle.actor_flat(aw.W, aw.b, aw.log_std), x, 3, 16, 5, act)
+        np.testing.assert_allclose(mu, h @ aw.W[3].astype(np.float64).T + aw.b[3].astype(np.float64),
+                                   rtol=1e-12, atol=1e-12)
+
+
+def test_rollout_critic_matches_standalone_value():
+    """The rollout's trunk-sharing critic (orc_critic_value) equals the head-row evaluation of
+    actor_value on the recorded observations, bit for bit, including the bootstrap V(s_T)."""
+    m = _market(n=4, T_data=200, seed=5)
+    od = 1 + 2 * 4 + 4 * 3
+    aw = synth.make_actor(od, 3, 16, 4, seed=9)
+    w = oracle.actor_flat(aw.W, aw.b, aw.log_std)[None, :]
+    cr = np.append(aw.w_v.astype(np.float64), aw.b_v)[None, :]
+    env = oracle.Env(m.close, m.feat, 3, horizon=4, C0=1e4, seed=11)
+    env.reset([3, 50, 90])
+    out = env.rollout(6, "sample", weights=w, n_hidden=3, hidden=16, want=("obs", "val"), critic=cr)
+    for t in range(7):
+        np.testing.assert_array_equal(out["val"][t], oracle.actor_value(aw.W, aw.b, aw.w_v, aw.b_v, out["obs"][t], 3, 16))
+
+
 def test_sample_logprob_is_gaussian_density():
     # S:L263: log_prob equals an independent evaluation of the Gaussian density
     rng = np.random.default_rng(2)
