@@ -144,8 +144,9 @@ def env_bytes_per_env(n, f, obs_dim):
 
 
 def gae_bytes(T, N):
-    """r, V read 4+4, done 1, adv, ret written 4+4 per element; boot 4 per env."""
-    return 17.0 * T * N + 4.0 * N
+    """r, V read 4+4, done 1, adv, ret written 4+4 per element; boot 4 per env; the per-buffer
+    normalisation rereads and rewrites adv (+8 per element; R#23)."""
+    return 25.0 * T * N + 4.0 * N
 
 
 def cpu_cores():
@@ -168,7 +169,8 @@ def oracle_step_sample(w, market, weights_flat, n_envs, T, nthreads, starts, cri
     t0 = time.perf_counter()
     out = env.rollout(T, "sample", weights=weights_flat[None, :], n_hidden=w.n_hidden, hidden=w.hidden,
                       nthreads=nthreads, want=("rew", "done", "val"), critic=critic[None, :])
-    oracle.gae(out["rew"], out["val"][:T], out["done"], out["val"][T], w.gamma, w.lam)
+    adv, _, _ = oracle.gae(out["rew"], out["val"][:T], out["done"], out["val"][T], w.gamma, w.lam)
+    oracle.gae_normalize(adv)
     J = oracle.fitness(env.ep_ret, 1)
     oracle.select_elite(J, 1)
     return time.perf_counter() - t0
@@ -280,13 +282,14 @@ def main():
     agents = [synth.make_actor(env.obs_dim, w.n_hidden, w.hidden, n, w.seed * 1000 + rank * P + a) for a in range(P)]
     params = api.pack_actor_params(cfg, agents, w.n_hidden, w.hidden, device=dev)
     actor = api.make_actor(w.n_hidden, w.hidden, params)
-    # the critic (head row n over the actor trunk, R#21) writes V(s_t) for t = 0..T during the rollout:
+    # the critic (head row n over the actor trunk, R#22) writes V(s_t) for t = 0..T during the rollout:
     # GAE consumes it on device, V(s_T) is the bootstrap
     traj = api.Trajectory.allocate(T, N, n, env.k_pad, device=dev, critic=True)
     val = traj.val[:T]
     boot = traj.val[T]
     adv = torch.empty_like(val)
     ret = torch.empty_like(val)
+    adv_stats = torch.empty(2, dtype=torch.float64, device=dev)   # per-buffer advantage normalisation (R#23)
     fit = torch.empty(P, dtype=torch.float64, device=dev)
     comm = api.Comm(world, rank, P)
     k_elite = args.elite_k or max(1, (P * world) // 2)
@@ -299,7 +302,7 @@ def main():
     def step(measure: bool):
         env.rollout(T, traj, actor=actor)
         ev_g0.record(stream)
-        api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret)
+        api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret, normalize=True, stats=adv_stats)
         ev_g1.record(stream)
         env.fitness(fit)
         comm.select_elite(fit, k_elite, params)
@@ -352,7 +355,7 @@ def main():
         def e2e_step():
             params.copy_(h_params, non_blocking=True)
             env.rollout(T, traj, actor=actor)
-            api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret)
+            api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret, normalize=True, stats=adv_stats)
             env.fitness(fit)
             comm.select_elite(fit, k_elite, params)
             h_fit.copy_(fit, non_blocking=True)

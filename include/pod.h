@@ -119,7 +119,7 @@ typedef struct {
     int32_t obs_dim;       /* 1 + 2n + n f                                   */
     int32_t k_pad;         /* obs_dim rounded up to 64 (obs row stride)       */
     int32_t n_out_pad;     /* n + 1 rounded up to 32 (head rows: 0..n-1 the  *
-                            * action means, row n the critic V, R#21)         */
+                            * action means, row n the critic V, R#22)         */
     int32_t n_layers;      /* n_hidden + 1                                    */
     size_t w_offset[POD_MAX_HIDDEN_LAYERS + 1];   /* bytes, bf16 [out_l][in_l] */
     int32_t w_rows[POD_MAX_HIDDEN_LAYERS + 1];    /* out_l (padded)            */
@@ -141,7 +141,7 @@ typedef struct {
  *   dbg_hold i32  [T][N][n]        h_{t+1} after the trade, before reset  (optional)
  *   dbg_cash f64  [T][N]           b_{t+1} after the trade, before reset  (optional)
  *   val      f32  [T+1][N]         critic V(s_t), t = 0..T: head row n over the
- *                                  actor's trunk (R#21); val[T] = V(s_T), the
+ *                                  actor's trunk (R#22); val[T] = V(s_T), the
  *                                  GAE bootstrap, from one extra value-only
  *                                  actor pass.  Feeds pod_gae directly.  (optional) */
 typedef struct {
@@ -250,10 +250,16 @@ pod_status pod_env_check(pod_env_t* env, void* stream);
  *   delta_t = r_t + gamma (1-d_t) V_{t+1} - V_t,  V_T = boot,
  *   A_t = delta_t + gamma lambda (1-d_t) A_{t+1}, A_T = 0,  R_t = A_t + V_t.
  * rew, val f32 [T][N], done u8 [T][N], boot f32 [N] -> adv, ret f32 [T][N], all
- * [dev], row-major (time-major).  T, N >= 1.  Errors: ARG, CUDA. */
+ * [dev], row-major (time-major).  T, N >= 1.
+ * adv_stats [dev] f64 [2] or NULL: per-buffer advantage normalisation (S:L278,
+ * R#23): the scan also accumulates S1 = sum A, S2 = sum A^2 (float64) into
+ * adv_stats (zeroed first), then adv is rewritten in place as (A - m) / s with
+ * m = S1/(T N), s = sqrt(S2/(T N) - m^2) (all zeros if s == 0); ret keeps the
+ * unnormalised A_t + V_t.  Stream-ordered, no host synchronisation.
+ * Errors: ARG, CUDA. */
 pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, const float* boot,
                    int32_t T, int32_t N, float gamma, float lambda, float* adv, float* ret,
-                   void* stream);
+                   double* adv_stats, void* stream);
 
 /* -------------------------------------------------- generational evolution */
 /* Selector plan ("redistributes the agents with the highest scores to

@@ -13,6 +13,7 @@ float64 layout (documented in oracle.c, ``orc_actor_mu``).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -125,7 +126,7 @@ def actor_mu(w_flat: np.ndarray, obs: np.ndarray, n_hidden: int, hidden: int, n:
 
 def actor_value(W, b, w_v, b_v, obs: np.ndarray, n_hidden: int, hidden: int, act: int = 0) -> np.ndarray:
     """Critic V(s) = w_v . h_L(s) + b_v on the actor's trunk h_L ("shared trunk -> actor head +
-    critic head"; R#21), for each row of obs [B, obs_dim] (float64).  Evaluated by the same
+    critic head"; R#22), for each row of obs [B, obs_dim] (float64).  Evaluated by the same
     MLP routine as the actor mean, with the value row appended to the head."""
     n = int(np.asarray(W[-1]).shape[0])
     W_h = np.vstack([np.asarray(W[-1], dtype=np.float64), np.asarray(w_v, dtype=np.float64)[None, :]])
@@ -201,7 +202,7 @@ class Env:
                 step0=0, nthreads=1, want=("obs", "rew", "done"), critic=None):
         """mode: inject (u [T,N,n] f32), replay (a_rep [T,N,n] i16), sample, deterministic.
         weights: [n_agents, count] float64 (actor_flat per agent).  critic: [n_agents, hidden+1] float64
-        (w_v, b_v per agent, R#21); with "val" in want, V(s_t) for t = 0..T in sample/deterministic mode."""
+        (w_v, b_v per agent, R#22); with "val" in want, V(s_t) for t = 0..T in sample/deterministic mode."""
         N, n, od = self.N, self.n, self.obs_dim
         modes = {"inject": 0, "replay": 1, "sample": 2, "deterministic": 3}
         out = {}
@@ -246,6 +247,16 @@ def gae(r, v, d, boot, gamma, lam):
     mag = np.zeros((T, N))
     lib().orc_gae(T, N, _p(r), _p(v), _p(d), _p(boot), float(gamma), float(lam), _p(adv), _p(ret), _p(mag))
     return adv, ret, mag
+
+
+def gae_normalize(adv):
+    """Per-buffer advantage normalisation ("advantages then normalized to zero mean / unit variance
+    per buffer"; R#23): (A - m) / s, m the mean, s the population standard deviation over the
+    whole buffer; a constant buffer (s = 0) maps to zeros.  float64."""
+    a = np.asarray(adv, dtype=np.float64)
+    m = a.sum() / a.size
+    s = math.sqrt(((a - m) ** 2).sum() / a.size)
+    return np.zeros_like(a) if s == 0.0 else (a - m) / s
 
 
 def fitness(ep_ret, n_agents):

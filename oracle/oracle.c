@@ -262,7 +262,7 @@ void orc_actor_mu(const double* w, int obs_dim, int n_hidden, int hidden, int n,
     }
 }
 
-/* Critic ("shared trunk -> actor head + critic head", R#21):
+/* Critic ("shared trunk -> actor head + critic head", R#22):
  * V = w_v . h_L + b_v, where h_L is the last hidden layer that orc_actor_mu
  * leaves in scratch (x after n_hidden swaps), summed in the head's order.
  * critic = [w_v (hidden), b_v].                                              */

@@ -87,7 +87,7 @@ def load():
         "pod_env_fitness": ([vp, vp, vp], C.c_int),
         "pod_env_read_state": ([vp, vp, vp, vp, vp, vp], C.c_int),
         "pod_env_check": ([vp, vp], C.c_int),
-        "pod_gae": ([vp, vp, vp, vp, i32, i32, f, f, vp, vp, vp], C.c_int),
+        "pod_gae": ([vp, vp, vp, vp, i32, i32, f, f, vp, vp, vp, vp], C.c_int),
         "pod_elite_plan": ([vp, i32, i32, vp], C.c_int),
         "pod_elite_transfers": ([vp, i32, i32, i32, P(Transfer), i32, P(i32)], C.c_int),
         "pod_comm_unique_id": ([vp], C.c_int),

@@ -68,7 +68,7 @@ def pack_actor_params(cfg: _lib.EnvConfig, agents: Sequence, n_hidden: int, hidd
             o = int(L.w_offset[l])
             slab[a, o : o + raw.size] = raw
             if l == L.n_layers - 1 and getattr(w, "w_v", None) is not None:
-                # critic: head row n (R#21)
+                # critic: head row n (R#22)
                 Wp[cfg.n_stocks, : w.w_v.size] = torch.from_numpy(np.ascontiguousarray(w.w_v, np.float32)).to(torch.bfloat16)
                 raw = Wp.view(torch.uint8).numpy().ravel()
                 o = int(L.w_offset[l])
@@ -97,7 +97,7 @@ class Trajectory:
     dbg_aint: Optional[torch.Tensor] = None
     dbg_hold: Optional[torch.Tensor] = None
     dbg_cash: Optional[torch.Tensor] = None
-    val: Optional[torch.Tensor] = None    # f32 [T+1, N] critic V(s_t) (R#21)
+    val: Optional[torch.Tensor] = None    # f32 [T+1, N] critic V(s_t) (R#22)
 
     @staticmethod
     def allocate(T: int, N: int, n: int, k_pad: int, device="cuda", debug=False, mu=False, sampled=True,
@@ -204,12 +204,16 @@ def make_actor(n_hidden: int, hidden: int, params: torch.Tensor, act: int = 0) -
     return _lib.Actor(n_hidden, hidden, act, 0, params.data_ptr(), params.shape[1] if params.dim() == 2 else params.numel())
 
 
-def pod_gae(rew, val, done, boot, gamma, lam, adv=None, ret=None, stream=None):
+def pod_gae(rew, val, done, boot, gamma, lam, adv=None, ret=None, stream=None, normalize=False, stats=None):
+    """GAE over [T, N]; normalize=True also rewrites adv as (A - mean) / std over the buffer (R#23),
+    with the float64 sums (sum A, sum A^2) left in `stats` (a [2] float64 device tensor, allocated if None)."""
     T, N = rew.shape
     adv = torch.empty_like(rew) if adv is None else adv
     ret = torch.empty_like(rew) if ret is None else ret
+    if normalize and stats is None:
+        stats = torch.empty(2, dtype=torch.float64, device=rew.device)
     check(load().pod_gae(_ptr(rew), _ptr(val), _ptr(done), _ptr(boot), T, N, float(gamma), float(lam), _ptr(adv),
-                         _ptr(ret), _stream(stream)), "pod_gae")
+                         _ptr(ret), _ptr(stats) if normalize else None, _stream(stream)), "pod_gae")
     return adv, ret
 
 

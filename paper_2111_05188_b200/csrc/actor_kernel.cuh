@@ -81,7 +81,7 @@ struct ActorArgs {
     int16_t* aint;       // [n][N] scratch
     int16_t* dbg_aint;   // [N][n] or null
     const float* znoise; // [n][N] N(0,1) noise for this step (written by the previous env-step launch)
-    float* val_out;      // [N] critic V(s_t) = head row n (R#21), or null
+    float* val_out;      // [N] critic V(s_t) = head row n (R#22), or null
     uint32_t* err;
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
 };
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             tmem_ld8(trow + (static_cast<uint32_t>(L) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
             tmem_ld_wait();
             if (valid && i0 <= a.n && a.val_out && a.n < i0 + 8) {
-                // critic: head row n over the same trunk (R#21)
+                // critic: head row n over the same trunk (R#22)
                 float vh = 0.0f;
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj)

@@ -47,6 +47,19 @@ __device__ __forceinline__ void gae_row(float r, float v, uint8_t d, float gamma
     v_next = v;
 }
 
+// per-buffer advantage statistics (R#23): this warp's sums of A and A^2, float64, one atomic pair
+__device__ __forceinline__ void gae_stats_flush(double s1, double s2, double* stats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_down_sync(0xffffffffu, s1, o);
+        s2 += __shfl_down_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(stats, s1);
+        atomicAdd(stats + 1, s2);
+    }
+}
+
 struct GaeMaps {
     CUtensorMap r, v, d;   // 2-D [T][N], box {32, 32}
 };
@@ -54,7 +67,8 @@ struct GaeMaps {
 __global__ void __launch_bounds__(32 * GAE_WARPS)
     gae_kernel(const __grid_constant__ GaeMaps maps, const float* __restrict__ rew, const float* __restrict__ val,
                const uint8_t* __restrict__ done, const float* __restrict__ boot, int T, int N, float gamma,
-               float lambda, float* __restrict__ adv, float* __restrict__ ret, int use_bulk) {
+               float lambda, float* __restrict__ adv, float* __restrict__ ret, int use_bulk,
+               double* __restrict__ stats) {
     extern __shared__ __align__(128) uint8_t gsm[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -68,14 +82,18 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
     float a_next = 0.0f;
     const int nchunks = (T + GAE_L - 1) / GAE_L;
 
+    double s1 = 0.0, s2 = 0.0;   // advantage statistics (stats != null)
     const bool bulk = use_bulk != 0;
     if (!bulk) {
         for (int t = T - 1; t >= 0; --t) {
             if (active) {
                 const int64_t i = static_cast<int64_t>(t) * N + e;
                 gae_row(rew[i], val[i], done[i], gamma, gl, v_next, a_next, adv + i, ret + i);
+                s1 += a_next;
+                s2 += static_cast<double>(a_next) * a_next;
             }
         }
+        if (stats) gae_stats_flush(s1, s2, stats);
         return;
     }
 
@@ -138,10 +156,15 @@ __global__ void __launch_bounds__(32 * GAE_WARPS)
                     const int64_t i = static_cast<int64_t>(t) * N + e;
                     adv[i] = delta[q];
                     ret[i] = delta[q] + vv[q];
+                    if (stats) {
+                        s1 += delta[q];
+                        s2 += static_cast<double>(delta[q]) * delta[q];
+                    }
                 }
             }
         }
     }
+    if (stats) gae_stats_flush(s1, s2, stats);
 }
 
 inline size_t gae_smem_bytes() { return GAE_WARPS * (GAE_STAGES * sizeof(GaeStage) + 128); }
@@ -171,7 +194,8 @@ inline size_t gae_seg_smem_bytes(int seg, int cpw) {
 
 __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
     gae_seg_kernel(const __grid_constant__ GaeMaps maps, const float* __restrict__ boot, int T, int N, float gamma,
-                   float lambda, float* __restrict__ adv, float* __restrict__ ret, int cpw) {
+                   float lambda, float* __restrict__ adv, float* __restrict__ ret, int cpw,
+                   double* __restrict__ stats) {
     extern __shared__ __align__(128) uint8_t gsm[];
     const int seg = blockDim.x >> 5;
     const int w = threadIdx.x >> 5;
@@ -230,6 +254,7 @@ __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
     float a_next = 0.f;
     for (int u = 0; u < w; ++u) a_next = sum->aloc[u][lane] + sum->prod[u][lane] * a_next;
     // pass 2: sequential recurrence from the exact entry state, same arithmetic as gae_row
+    double s1 = 0.0, s2 = 0.0;
     v_next = v_in;
     for (int j = j0; j < j1; ++j) {
         const int t_base = T - (j + 1) * GAE_L;
@@ -245,11 +270,36 @@ __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
                 const int64_t i = static_cast<int64_t>(t_base + q) * N + e;
                 adv[i] = A;
                 ret[i] = A + v;
+                s1 += A;
+                s2 += static_cast<double>(A) * A;
             }
             a_next = A;
             v_next = v;
         }
     }
+    if (stats) gae_stats_flush(s1, s2, stats);
+}
+
+// advantage normalisation in place (R#23): A <- (A - m) / s, m = S1 / count, s^2 = S2 / count - m^2
+__global__ void adv_normalize_kernel(float* __restrict__ adv, int64_t count, const double* __restrict__ stats,
+                                     int vec4) {
+    const double m = stats[0] / static_cast<double>(count);
+    const double var = stats[1] / static_cast<double>(count) - m * m;
+    const float mf = static_cast<float>(m);
+    const float inv = var > 0.0 ? static_cast<float>(1.0 / sqrt(var)) : 0.0f;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t n4 = vec4 ? count / 4 : 0;
+    float4* a4 = reinterpret_cast<float4*>(adv);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 x = a4[i];
+        x.x = (x.x - mf) * inv;
+        x.y = (x.y - mf) * inv;
+        x.z = (x.z - mf) * inv;
+        x.w = (x.w - mf) * inv;
+        a4[i] = x;
+    }
+    for (int64_t i = 4 * n4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+        adv[i] = (adv[i] - mf) * inv;
 }
 
 }  // namespace pod

@@ -131,7 +131,7 @@ static pod_status dims_of(const pod_env_config* c, int* obs_dim, int* k_pad, int
     if (c->n_stocks < 1 || c->n_feat < 0) return pod_fail(POD_ERR_ARG, "n_stocks >= 1 and n_feat >= 0 required");
     *obs_dim = 1 + 2 * c->n_stocks + c->n_stocks * c->n_feat;
     *k_pad = static_cast<int>(round_up(static_cast<size_t>(*obs_dim), 64));
-    // head rows: the n action means, then the critic V in row n (R#21), padded to the 32-row MMA granule
+    // head rows: the n action means, then the critic V in row n (R#22), padded to the 32-row MMA granule
     *n_out_pad = static_cast<int>(round_up(static_cast<size_t>(c->n_stocks) + 1, 32));
     if (*k_pad > ENV_MAX_KPAD || c->n_stocks > ENV_MAX_STOCKS)
         return pod_fail(POD_ERR_UNSUPPORTED, "obs_dim %d exceeds the kernel limit (k_pad <= %d, n <= %d)", *obs_dim,
@@ -884,8 +884,31 @@ extern "C" pod_status pod_env_read_state(pod_env_t* e, int32_t* hold, double* ca
 }
 
 // ------------------------------------------------------------ GAE
+static pod_status gae_launch(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
+                             int32_t N, float gamma, float lambda, float* adv, float* ret, double* stats,
+                             cudaStream_t stream);
+
 extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
-                              int32_t N, float gamma, float lambda, float* adv, float* ret, void* stream) {
+                              int32_t N, float gamma, float lambda, float* adv, float* ret, double* adv_stats,
+                              void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (adv_stats) {
+        if (reinterpret_cast<uintptr_t>(adv_stats) % 8 != 0) return pod_fail(POD_ERR_ARG, "adv_stats must be 8-byte aligned");
+        POD_CUDA(cudaMemsetAsync(adv_stats, 0, 2 * sizeof(double), s));
+    }
+    pod_status st = gae_launch(rew, val, done, boot, T, N, gamma, lambda, adv, ret, adv_stats, s);
+    if (st || !adv_stats) return st;
+    const int64_t count = static_cast<int64_t>(T) * N;
+    const int64_t want = (count / 4 + 255) / 256;
+    const unsigned blocks = static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
+    adv_normalize_kernel<<<blocks, 256, 0, s>>>(adv, count, adv_stats, reinterpret_cast<uintptr_t>(adv) % 16 == 0);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+static pod_status gae_launch(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
+                             int32_t N, float gamma, float lambda, float* adv, float* ret, double* stats,
+                             cudaStream_t stream) {
     if (!rew || !val || !done || !boot || !adv || !ret) return pod_fail(POD_ERR_ARG, "GAE pointers must be non-NULL");
     if (T < 1 || N < 1) return pod_fail(POD_ERR_ARG, "T and N must be >= 1");
     if (static_cast<int64_t>(T) * N >= (1ll << 40)) return pod_fail(POD_ERR_SHAPE, "T * N too large");
@@ -963,8 +986,8 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
                 seg_attr = want;
             }
         }
-        gae_seg_kernel<<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw),
-                         static_cast<cudaStream_t>(stream)>>>(maps, boot, T, N, gamma, lambda, adv, ret, cpw);
+        gae_seg_kernel<<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw), stream>>>(
+            maps, boot, T, N, gamma, lambda, adv, ret, cpw, stats);
         POD_CUDA(cudaGetLastError());
         return POD_OK;
     }
@@ -976,8 +999,8 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
                                         static_cast<int>(gae_smem_bytes()));
     });
     POD_CUDA(attr_err);
-    gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), static_cast<cudaStream_t>(stream)>>>(
-        maps, rew, val, done, boot, T, N, gamma, lambda, adv, ret, use_bulk);
+    gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), stream>>>(maps, rew, val, done, boot, T, N, gamma, lambda,
+                                                                       adv, ret, use_bulk, stats);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }

@@ -183,7 +183,7 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
 class ActorWeights:
     """One agent's actor: layers W[l] [out, in] (bf16-representable float32),
     b[l] [out] float32, log_std [n] float32.  Layer 0 has in = obs_dim, the
-    hidden layers in = hidden, the head out = n.  Critic (R#21): V(s) =
+    hidden layers in = hidden, the head out = n.  Critic (R#22): V(s) =
     w_v . h_L(s) + b_v on the same trunk (w_v [hidden] bf16-representable)."""
     W: list
     b: list

@@ -200,6 +200,24 @@ def test_gae_parity(T, N, path, monkeypatch):
     gae_check(adv, ret, adv_o, ret_o, mag)
 
 
+@pytest.mark.parametrize("path", ["seq", "seg"])
+@pytest.mark.parametrize("T,N", [(256, 8192), (77, 100), (33, 4096), (5, 3)])
+def test_gae_normalized_parity(T, N, path, monkeypatch):
+    """R#23: per-buffer advantage normalisation fused with the scan (float64 sums) + in-place rewrite."""
+    monkeypatch.setenv("POD_GAE_PATH", path)
+    r, v, d, boot = synth.gae_inputs(T, N, seed=T * 3 + N)
+    adv_o, ret_o, mag = oracle.gae(r, v, d, boot, 0.99, 0.95)
+    an_o = oracle.gae_normalize(adv_o)
+    s_o = float(np.sqrt(((adv_o - adv_o.mean()) ** 2).mean()))
+    adv, ret = api.pod_gae(*(torch.from_numpy(x).cuda() for x in (r, v, d, boot)), 0.99, 0.95, normalize=True)
+    an_g = adv.cpu().numpy().astype(np.float64)
+    # error of A (<= 1e-5 M_t, plus the float32 rounding of A) carried through (A - m) / s
+    # (the mean and the standard deviation move by at most the mean error bound, hence the (1 + |A'|) factor)
+    tol = (1e-5 * mag + 1e-6 + 1e-5 * mag.mean() + 1e-6) / s_o * (1.0 + np.abs(an_o)) + 2e-6 * np.abs(an_o)
+    assert np.all(np.abs(an_g - an_o) <= tol)
+    np.testing.assert_allclose(ret.cpu().numpy(), ret_o, rtol=0, atol=float((1e-5 * mag + 1e-6).max()))
+
+
 def test_gae_worked_example_on_gpu():
     r = torch.tensor([[1.0], [0.0], [2.0]]).cuda()
     v = torch.tensor([[0.5], [0.2], [0.1]]).cuda()
@@ -371,7 +389,7 @@ def test_pair_kernel_matches_single_cta_kernel(monkeypatch):
 
 @pytest.mark.parametrize("n,nh,hid", [(100, 3, 512), (30, 2, 128), (32, 2, 256)])
 def test_critic_value_parity(n, nh, hid):
-    """R#21: V(s_t) = head row n over the trunk, written per step; V(s_T) by the value-only pass.
+    """R#22: V(s_t) = head row n over the trunk, written per step; V(s_T) by the value-only pass.
     Compared with the oracle's float64 forward on the GPU's own bf16 observations (the actor bar);
     the actor's own outputs are bit-identical with and without the critic output."""
     outs = []

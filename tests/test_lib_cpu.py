@@ -70,7 +70,7 @@ def test_pack_actor_params_roundtrip():
         b = slab[L.b_offset[l] : L.b_offset[l] + rows * 4].view(np.float32)
         np.testing.assert_array_equal(b[: aw.b[l].size], aw.b[l])
         r0 = aw.W[l].shape[0]
-        if l == 2:   # head row n = the critic (R#21)
+        if l == 2:   # head row n = the critic (R#22)
             np.testing.assert_array_equal(W[r0, : aw.w_v.size], aw.w_v)
             assert b[r0] == np.float32(aw.b_v)
             r0 += 1

@@ -289,8 +289,21 @@ def test_actor_matches_numpy_matmul(act):
     np.testing.assert_allclose(mu, ref, rtol=1e-12, atol=1e-12)
 
 
+def test_gae_normalize_pins():
+    """R#23: zero mean / unit variance per buffer.  Worked example [1, 2, 3] -> m = 2,
+    s = sqrt(2/3) -> [-sqrt(3/2), 0, sqrt(3/2)]; constant buffer -> zeros; the result has mean 0 and
+    population variance 1, and is invariant to an affine change a A + b (a > 0) of the input."""
+    np.testing.assert_allclose(oracle.gae_normalize(np.array([[1.0, 2.0, 3.0]])), [[-math.sqrt(1.5), 0.0, math.sqrt(1.5)]],
+                               rtol=1e-15, atol=1e-15)
+    np.testing.assert_array_equal(oracle.gae_normalize(np.full((4, 5), 2.5)), np.zeros((4, 5)))
+    x = np.random.default_rng(3).normal(size=(64, 33)) * 3.0 + 1.7
+    y = oracle.gae_normalize(x)
+    assert abs(y.mean()) < 1e-13 and abs(y.var() - 1.0) < 1e-12
+    np.testing.assert_allclose(oracle.gae_normalize(0.25 * x - 4.0), y, rtol=1e-12, atol=1e-12)
+
+
 def test_critic_value_pins():
-    """R#21: V = w_v . h_L + b_v on the actor's trunk.  Pins: a zero trunk gives V = b_v exactly; a
+    """R#22: V = w_v . h_L + b_v on the actor's trunk.  Pins: a zero trunk gives V = b_v exactly; a
     general trunk equals a numpy float64 forward; the actor mean is unaffected by the critic row."""
     od, nh, H, n = 9, 2, 8, 3
     W = [np.zeros((H, od)), np.zeros((H, H)), np.zeros((n, H))]
