@@ -127,6 +127,8 @@ typedef struct {
     size_t b_offset[POD_MAX_HIDDEN_LAYERS + 1];   /* bytes, float32 [out_l]    */
     size_t log_std_offset;                        /* bytes, float32 [n_out_pad] */
     size_t param_bytes;                           /* minimal slab size, %1024==0 */
+    size_t n_elems;        /* parameters per slab incl. padding: sum rows*cols + sum rows + n_out_pad
+                            * (the float32 vector pod_fuse_pods works on, same order as the slab) */
 } pod_actor_layout;
 
 /* Trajectory buffers [dev] (transitions stay as tensors in
@@ -260,6 +262,26 @@ pod_status pod_env_check(pod_env_t* env, void* stream);
 pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, const float* boot,
                    int32_t T, int32_t N, float gamma, float lambda, float* adv, float* ret,
                    double* adv_stats, void* stream);
+
+/* ------------------------------------------------------ K-pod ensemble fusion */
+/* Fuse the K pods of each agent once per epoch ("fusing the trained
+ * models from K pods at each epoch"; P:L372 parameters, not gradients, are
+ * exchanged, using the soft update; R#24):
+ *   mean = (1/K) sum_pods theta,  fused = tau mean + (1 - tau) prev,
+ *   every pod's theta <- fused, prev <- fused.
+ * The pods of agent a are its K_local consecutive slots a*K_local .. +K_local-1
+ * of `params` on every rank of `comm` (comm NULL: this process only), so
+ * K = K_local * nranks.  params [dev] [P_local][param_bytes] slabs in the
+ * pod_actor_layout of (cfg, n_hidden, hidden), in/out; bf16 weights are
+ * rounded to nearest even from the float32 result.  prev [dev] f32
+ * [P_local/K_local][layout.n_elems] the previous fused parameters (in/out);
+ * may be NULL only when tau == 1 (hard adoption, S:L368 default).  work [dev]
+ * f32 [P_local/K_local][layout.n_elems] scratch.  tau in [0, 1].
+ * Stream-ordered; the cross-rank sum is one ncclAllReduce on `stream`.
+ * Errors: ARG, SHAPE, UNSUPPORTED, NCCL, CUDA. */
+pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                         void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
+                         float* prev, float* work, void* stream);
 
 /* -------------------------------------------------- generational evolution */
 /* Selector plan ("redistributes the agents with the highest scores to

@@ -259,6 +259,14 @@ def gae_normalize(adv):
     return np.zeros_like(a) if s == 0.0 else (a - m) / s
 
 
+def fuse(snapshots, prev, tau):
+    """K-pod fusion (S:L302–310 soft_update, S:L364–372 fuse; R#24):
+    fused = tau * mean(snapshots) + (1 - tau) * prev, elementwise, float64.  snapshots [K, E]."""
+    snap = np.asarray(snapshots, dtype=np.float64)
+    mean = snap.sum(axis=0) / snap.shape[0]
+    return tau * mean + (1.0 - tau) * np.asarray(prev, dtype=np.float64)
+
+
 def fitness(ep_ret, n_agents):
     ep = np.ascontiguousarray(ep_ret, dtype=np.float64)
     J = np.zeros(n_agents)

@@ -39,7 +39,7 @@ class ActorLayout(C.Structure):
     _fields_ = [("obs_dim", C.c_int32), ("k_pad", C.c_int32), ("n_out_pad", C.c_int32), ("n_layers", C.c_int32),
                 ("w_offset", C.c_size_t * (MAX_HIDDEN + 1)), ("w_rows", C.c_int32 * (MAX_HIDDEN + 1)),
                 ("w_cols", C.c_int32 * (MAX_HIDDEN + 1)), ("b_offset", C.c_size_t * (MAX_HIDDEN + 1)),
-                ("log_std_offset", C.c_size_t), ("param_bytes", C.c_size_t)]
+                ("log_std_offset", C.c_size_t), ("param_bytes", C.c_size_t), ("n_elems", C.c_size_t)]
 
 
 class Traj(C.Structure):
@@ -54,7 +54,7 @@ class Transfer(C.Structure):
 
 EXPORTS = ["pod_status_string", "pod_last_error", "pod_abi_version", "pod_actor_layout_get",
            "pod_env_workspace_size", "pod_env_create", "pod_env_destroy", "pod_env_reset", "pod_rollout",
-           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan",
+           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan", "pod_fuse_pods",
            "pod_elite_transfers", "pod_comm_unique_id", "pod_comm_init", "pod_comm_destroy", "pod_select_elite"]
 
 _lib = None
@@ -87,6 +87,7 @@ def load():
         "pod_env_fitness": ([vp, vp, vp], C.c_int),
         "pod_env_read_state": ([vp, vp, vp, vp, vp, vp], C.c_int),
         "pod_env_check": ([vp, vp], C.c_int),
+        "pod_fuse_pods": ([vp, P(EnvConfig), i32, i32, vp, sz, i32, i32, f, vp, vp, vp], C.c_int),
         "pod_gae": ([vp, vp, vp, vp, i32, i32, f, f, vp, vp, vp, vp], C.c_int),
         "pod_elite_plan": ([vp, i32, i32, vp], C.c_int),
         "pod_elite_transfers": ([vp, i32, i32, i32, P(Transfer), i32, P(i32)], C.c_int),

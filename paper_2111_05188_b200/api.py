@@ -234,6 +234,21 @@ def pod_elite_transfers(plan: np.ndarray, P_local: int, rank: int):
     return [(ops[i].kind, ops[i].peer, ops[i].src_local, ops[i].dst_local) for i in range(n.value)]
 
 
+def fuse_pods(cfg: _lib.EnvConfig, n_hidden: int, hidden: int, params: torch.Tensor, K_local: int, tau: float = 1.0,
+              prev: Optional[torch.Tensor] = None, comm: Optional["Comm"] = None, work: Optional[torch.Tensor] = None,
+              stream=None):
+    """K-pod ensemble fusion (pod_fuse_pods, R#24): params uint8 [P_local, param_bytes] (slots a*K_local + k are
+    agent a's pods), prev float32 [P_local/K_local, n_elems] (in/out; optional when tau == 1)."""
+    L = actor_layout(cfg, n_hidden, hidden)
+    P_local = params.shape[0]
+    if work is None:
+        work = torch.empty((P_local // K_local, int(L.n_elems)), dtype=torch.float32, device=params.device)
+    check(load().pod_fuse_pods(comm.h if comm is not None else None, C.byref(cfg), n_hidden, hidden, _ptr(params),
+                               params.shape[1], P_local, int(K_local), float(tau), _ptr(prev), _ptr(work),
+                               _stream(stream)), "pod_fuse_pods")
+    return prev
+
+
 class Comm:
     """NCCL communicator of libpod (one process per GPU).  The torch process
     group (if any) only broadcasts the 128-byte unique id."""

@@ -10,12 +10,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
 #include "actor_kernel.cuh"
 #include "actor_pair_kernel.cuh"
 #include "env_kernel.cuh"
+#include "fuse_kernel.cuh"
 #include "gae_kernel.cuh"
 #include "pod.h"
 #include "pod_internal.h"
@@ -171,6 +173,9 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
     out->log_std_offset = off;
     off += static_cast<size_t>(nop) * 4;
     out->param_bytes = round_up(off, 1024);
+    size_t ne = static_cast<size_t>(nop);
+    for (int l = 0; l <= n_hidden; ++l) ne += static_cast<size_t>(out->w_rows[l]) * (out->w_cols[l] + 1);
+    out->n_elems = ne;
     return POD_OK;
 }
 
@@ -1001,6 +1006,63 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
     POD_CUDA(attr_err);
     gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), stream>>>(maps, rew, val, done, boot, T, N, gamma, lambda,
                                                                        adv, ret, use_bulk, stats);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+// ------------------------------------------------------------ K-pod ensemble fusion (R#24)
+extern "C" pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                    void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
+                                    float* prev, float* work, void* stream) {
+    if (!params || !work) return pod_fail(POD_ERR_ARG, "params and work must be non-NULL");
+    if (K_local < 1 || P_local < 1 || P_local % K_local != 0)
+        return pod_fail(POD_ERR_ARG, "P_local (%d) must be a positive multiple of K_local (%d)", P_local, K_local);
+    if (!(tau >= 0.0f && tau <= 1.0f)) return pod_fail(POD_ERR_ARG, "tau must be in [0, 1]");
+    if (!prev && tau != 1.0f) return pod_fail(POD_ERR_ARG, "prev is required when tau < 1");
+    pod_actor_layout L;
+    pod_status st = pod_actor_layout_get(cfg, n_hidden, hidden, &L);
+    if (st) return st;
+    if (param_bytes < L.param_bytes || param_bytes % 16 != 0)
+        return pod_fail(POD_ERR_SHAPE, "param_bytes %zu must be >= %zu and a multiple of 16", param_bytes, L.param_bytes);
+    st = pod_require_sm100();
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    FuseArgs a{};
+    uint64_t flat = 0;
+    int ns = 0;
+    for (int l = 0; l < L.n_layers; ++l) {
+        a.seg[ns++] = FuseSeg{L.w_offset[l], flat, static_cast<uint32_t>(L.w_rows[l]) * L.w_cols[l], 1u};
+        flat += static_cast<uint64_t>(L.w_rows[l]) * L.w_cols[l];
+    }
+    for (int l = 0; l < L.n_layers; ++l) {
+        a.seg[ns++] = FuseSeg{L.b_offset[l], flat, static_cast<uint32_t>(L.w_rows[l]), 0u};
+        flat += static_cast<uint64_t>(L.w_rows[l]);
+    }
+    a.seg[ns++] = FuseSeg{L.log_std_offset, flat, static_cast<uint32_t>(L.n_out_pad), 0u};
+    flat += static_cast<uint64_t>(L.n_out_pad);
+    a.n_seg = ns;
+    a.K_local = K_local;
+    a.n_elems = static_cast<int64_t>(flat);
+    a.param_bytes = param_bytes;
+    a.params = static_cast<char*>(params);
+    a.work = work;
+    a.prev = prev;
+    const int nranks = comm ? pod_comm_size(comm) : 1;
+    a.scale = 1.0f / static_cast<float>(K_local * nranks);
+    a.tau = tau;
+    const int A_local = P_local / K_local;
+    if (a.n_elems % 8 != 0 || param_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(params) % 16 != 0 ||
+        reinterpret_cast<uintptr_t>(work) % 16 != 0 || (prev && reinterpret_cast<uintptr_t>(prev) % 16 != 0))
+        return pod_fail(POD_ERR_ARG, "params, prev and work must be 16-byte aligned");
+    const int64_t groups8 = a.n_elems / 8;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((groups8 + 255) / 256, 8 * 148)), static_cast<unsigned>(A_local));
+    fuse_sum_kernel<<<grid, 256, 0, s>>>(a);
+    POD_CUDA(cudaGetLastError());
+    if (comm && nranks > 1) {
+        st = pod_comm_allreduce_sum_f32(comm, work, static_cast<size_t>(A_local) * a.n_elems, s);
+        if (st) return st;
+    }
+    fuse_blend_kernel<<<grid, 256, 0, s>>>(a);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }

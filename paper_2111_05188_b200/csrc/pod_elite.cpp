@@ -75,6 +75,8 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+        nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -100,14 +102,15 @@ NcclApi* nccl() {
     LOAD(CommInitRank);
     LOAD(CommDestroy);
     LOAD(AllGather);
+    LOAD(AllReduce);
     LOAD(Send);
     LOAD(Recv);
     LOAD(GroupStart);
     LOAD(GroupEnd);
     LOAD(GetErrorString);
 #undef LOAD
-    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.Send || !api.Recv || !api.GroupStart ||
-        !api.GroupEnd) {
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.Send || !api.Recv ||
+        !api.GroupStart || !api.GroupEnd) {
         api.h = nullptr;
         return nullptr;
     }
@@ -221,5 +224,15 @@ extern "C" pod_status pod_select_elite(pod_comm_t* c, const double* fitness_loca
         }
         NCCL_TRY(api->GroupEnd());
     }
+    return POD_OK;
+}
+
+int pod_comm_size(const pod_comm_t* c) { return c ? c->nranks : 1; }
+
+// in-place sum over the communicator's ranks (K-pod fusion): one ncclAllReduce on `stream`
+pod_status pod_comm_allreduce_sum_f32(pod_comm_t* c, float* buf, size_t count, cudaStream_t stream) {
+    NcclApi* api = nccl();
+    if (!api) return pod_fail(POD_ERR_NCCL, "NCCL not loaded");
+    NCCL_TRY(api->AllReduce(buf, buf, count, ncclFloat32, ncclSum, c->comm, stream));
     return POD_OK;
 }

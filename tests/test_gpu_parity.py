@@ -432,3 +432,55 @@ def test_critic_deterministic_and_graph_reuse():
     rms = math.sqrt(float(np.mean(v_o ** 2)))
     assert np.all(np.abs(vals[-1].cpu().numpy() - v_o) <= 2e-2 * (np.abs(v_o) + rms))
     assert not torch.equal(vals[0], vals[1])   # the envs moved on between calls
+
+
+def _slab_flat(slab: np.ndarray, L) -> np.ndarray:
+    """Widen one parameter slab (bf16 weights, f32 biases / log-std) to the float64 flat vector of
+    pod_actor_layout order (W_0..W_L, b_0..b_L, log_std)."""
+    parts = []
+    for l in range(L.n_layers):
+        n = L.w_rows[l] * L.w_cols[l]
+        raw = slab[L.w_offset[l] : L.w_offset[l] + 2 * n].view(np.uint16).astype(np.uint32) << 16
+        parts.append(raw.view(np.float32).astype(np.float64))
+    for l in range(L.n_layers):
+        parts.append(slab[L.b_offset[l] : L.b_offset[l] + 4 * L.w_rows[l]].view(np.float32).astype(np.float64))
+    parts.append(slab[L.log_std_offset : L.log_std_offset + 4 * L.n_out_pad].view(np.float32).astype(np.float64))
+    return np.concatenate(parts)
+
+
+@pytest.mark.parametrize("tau", [1.0, 0.3, 0.0])
+def test_fuse_pods_parity(tau):
+    """R#24: K_local = 4 pods of 2 agents on one GPU; every pod's slab <- narrow(tau mean + (1-tau) prev),
+    prev <- the float32 fused vector; compared with the float64 oracle (bf16 weights within one bf16 ulp,
+    float32 entries within 2 ulp), all pods of an agent bit-identical."""
+    c = Case(n=30, f=3, T_data=300, N=64, H=20)
+    nh, hid, K, A = 2, 128, 4, 2
+    aws = [synth.make_actor(c.obs_dim, nh, hid, c.n, 100 + s) for s in range(K * A)]
+    params = api.pack_actor_params(c.cfg, aws, nh, hid)
+    L = api.actor_layout(c.cfg, nh, hid)
+    E = int(L.n_elems)
+    before = params.cpu().numpy()
+    flats = np.stack([_slab_flat(before[s], L) for s in range(K * A)])
+    prev0 = torch.from_numpy(np.random.default_rng(9).normal(size=(A, E)).astype(np.float32)).cuda()
+    prev = prev0.clone() if tau != 1.0 else None
+    api.fuse_pods(c.cfg, nh, hid, params, K, tau=tau, prev=prev)
+    after = params.cpu().numpy()
+    nw = sum(L.w_rows[l] * L.w_cols[l] for l in range(L.n_layers))
+    for a in range(A):
+        exp = oracle.fuse(flats[a * K : (a + 1) * K], prev0[a].cpu().numpy().astype(np.float64), tau)
+        for k in range(K):
+            assert np.array_equal(after[a * K + k], after[a * K]), (a, k)
+        got = _slab_flat(after[a * K], L)
+        # float32 sum + blend: a few roundings relative to the magnitudes involved; bf16: one more ulp
+        mag = tau * np.abs(flats[a * K : (a + 1) * K]).mean(axis=0) + (1.0 - tau) * np.abs(prev0[a].cpu().numpy())
+        tol32 = 8.0 * 2.0 ** -24 * mag
+        assert np.all(np.abs(got[:nw] - exp[:nw]) <= np.abs(exp[:nw]) * 2.0 ** -8 + 2.0 * tol32[:nw]), a
+        assert np.all(np.abs(got[nw:] - exp[nw:]) <= tol32[nw:]), a
+        if prev is not None:
+            assert np.all(np.abs(prev[a].cpu().numpy() - exp) <= tol32), a
+    # the fused actor still runs
+    actor = api.make_actor(nh, hid, params)
+    tr = api.Trajectory.allocate(2, c.N, c.n, c.k_pad)
+    c.env.reset(c.starts)
+    c.env.rollout(2, tr, actor=actor)
+    c.env.check()

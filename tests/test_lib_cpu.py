@@ -79,6 +79,16 @@ def test_pack_actor_params_roundtrip():
     np.testing.assert_array_equal(ls[:30], aw.log_std)
 
 
+def test_layout_n_elems():
+    """pod_actor_layout.n_elems (the float32 vector of pod_fuse_pods) counts every slab entry once."""
+    for n, nh, hid in ((30, 2, 128), (100, 3, 512), (32, 1, 256)):
+        cfg = api.make_config(64, n, 3, 10)
+        L = api.actor_layout(cfg, nh, hid)
+        ne = sum(L.w_rows[l] * L.w_cols[l] + L.w_rows[l] for l in range(L.n_layers)) + L.n_out_pad
+        assert L.n_elems == ne
+        assert L.n_out_pad >= n + 1 and L.n_out_pad % 32 == 0   # row n is the critic (R#22)
+
+
 def test_elite_plan_matches_oracle():
     rng = np.random.default_rng(0)
     for _ in range(200):

@@ -302,6 +302,19 @@ def test_gae_normalize_pins():
     np.testing.assert_allclose(oracle.gae_normalize(0.25 * x - 4.0), y, rtol=1e-12, atol=1e-12)
 
 
+def test_fuse_pins():
+    """R#24 pins: S:L371 fuse([0,0],[2,4], tau=1) = [1,2]; S:L310 soft update target [0,2], source [2,4],
+    tau = 0.5 -> [1,3] (a single snapshot is its own mean); tau = 0 keeps prev; K identical snapshots with
+    tau = 1 return the snapshot; the mean is symmetric in the pods."""
+    np.testing.assert_array_equal(oracle.fuse([[0.0, 0.0], [2.0, 4.0]], [9.0, 9.0], 1.0), [1.0, 2.0])
+    np.testing.assert_array_equal(oracle.fuse([[2.0, 4.0]], [0.0, 2.0], 0.5), [1.0, 3.0])
+    x = np.random.default_rng(5).normal(size=(3, 7))
+    p = np.random.default_rng(6).normal(size=7)
+    np.testing.assert_array_equal(oracle.fuse(x, p, 0.0), p)
+    np.testing.assert_array_equal(oracle.fuse(np.tile(x[0], (4, 1)), p, 1.0), x[0])
+    np.testing.assert_allclose(oracle.fuse(x[::-1], p, 0.3), oracle.fuse(x, p, 0.3), rtol=1e-15)
+
+
 def test_critic_value_pins():
     """R#22: V = w_v . h_L + b_v on the actor's trunk.  Pins: a zero trunk gives V = b_v exactly; a
     general trunk equals a numpy float64 forward; the actor mean is unaffected by the critic row."""
