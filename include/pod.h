@@ -142,6 +142,9 @@ typedef struct {
  *   dbg_aint i16  [T][N][n]        executed integer action a_t            (optional)
  *   dbg_hold i32  [T][N][n]        h_{t+1} after the trade, before reset  (optional)
  *   dbg_cash f64  [T][N]           b_{t+1} after the trade, before reset  (optional)
+ *   equity   f64  [T][N]           account value v_{t+1} = b + p_{t+1}^T h after
+ *                                  step t, before any auto-reset (the backtest
+ *                                  curve, R#25)                            (optional)
  *   val      f32  [T+1][N]         critic V(s_t), t = 0..T: head row n over the
  *                                  actor's trunk (R#22); val[T] = V(s_T), the
  *                                  GAE bootstrap, from one extra value-only
@@ -157,6 +160,7 @@ typedef struct {
     int32_t* dbg_hold;
     double* dbg_cash;
     float* val;
+    double* equity;
 } pod_traj;
 
 /* ---------------------------------------------------------------- layout */
@@ -282,6 +286,29 @@ pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, cons
 pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
                          void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
                          float* prev, float* work, void* stream);
+
+/* ----------------------------------------------------------- evaluator */
+/* Backtest metrics of one account-value curve per env (§5.2
+ * "cumulative return ... annual return ... annual volatility ... Sharpe ratio
+ * ... max drawdown"; R#25): v_0 = v0[e], v_t = curve[t-1][e] for
+ * t = 1..T (one episode: a deterministic rollout whose horizon covers T, e.g.
+ * traj.equity), rho_t = v_t / v_{t-1} - 1:
+ *   out[0][e] cumulative return (v_T - v_0) / v_0
+ *   out[1][e] annual return (v_T / v_0)^(ppy / T) - 1
+ *   out[2][e] annual volatility std(rho) sqrt(ppy)   (sample, n - 1; 0 if T < 2)
+ *   out[3][e] Sharpe (mean(rho) - rf) / std(rho) sqrt(ppy); NaN if std = 0 or T < 2
+ *   out[4][e] max drawdown min_t (v_t / max_{s<=t} v_s - 1)   (<= 0)
+ * v0 [dev] f64 [N], curve [dev] f64 [T][N], out [dev] f64 [5][N]; float64
+ * throughout.  T >= 1, ppy > 0.  Errors: ARG, CUDA. */
+pod_status pod_backtest_metrics(const double* v0, const double* curve, int32_t T, int32_t N,
+                                double periods_per_year, double rf_per_period, double* out, void* stream);
+
+/* Early-stop rule of the evaluator ("stop the training process using
+ * the early stopping mechanism", "keeps track of the best agent so far";
+ * S:L441–448; R#25), host only: best = argmax of history (earliest wins);
+ * stop = 1 when the latest entry is at least `patience` entries after best.
+ * Errors: ARG (empty history, patience < 0, NULL). */
+pod_status pod_early_stop(const double* history, int32_t len, int32_t patience, int32_t* stop, int32_t* best);
 
 /* -------------------------------------------------- generational evolution */
 /* Selector plan ("redistributes the agents with the highest scores to

@@ -59,7 +59,7 @@ def lib():
         L.orc_map_action.restype = i
         L.orc_reset.argtypes = [C.POINTER(_Cfg), C.POINTER(_State)]
         L.orc_obs.argtypes = [C.POINTER(_Cfg), vp, vp, C.POINTER(_State), i, vp]
-        L.orc_env_step.argtypes = [C.POINTER(_Cfg), vp, C.POINTER(_State), i, vp, vp, vp, vp, vp]
+        L.orc_env_step.argtypes = [C.POINTER(_Cfg), vp, C.POINTER(_State), i, vp, vp, vp, vp, vp, vp]
         L.orc_env_step.restype = i
         L.orc_actor_weight_count.argtypes = [i, i, i, i]
         L.orc_actor_weight_count.restype = i64
@@ -67,7 +67,7 @@ def lib():
         L.orc_sample.argtypes = [i, vp, vp, vp, i, vp, vp]
         L.orc_sample.restype = d
         L.orc_rollout.argtypes = [C.POINTER(_Cfg), vp, vp, C.POINTER(_State), i, i, vp, vp, vp, i, i, i,
-                                  u64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i]
+                                  u64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i]
         L.orc_critic_value.argtypes = [vp, i, i, vp]
         L.orc_critic_value.restype = d
         L.orc_rollout.restype = i64
@@ -191,7 +191,7 @@ class Env:
         hp = np.zeros(self.n, dtype=np.int32)
         cp = np.zeros(1)
         d = lib().orc_env_step(C.byref(self.cfg), _p(self.close), C.byref(self._st), int(e), _p(a),
-                               _p(r), _p(nt), _p(hp), _p(cp))
+                               _p(r), _p(nt), _p(hp), _p(cp), None)
         return float(r[0]), bool(d), int(nt[0]), hp, float(cp[0])
 
     def account_value(self, e):
@@ -223,6 +223,7 @@ class Env:
         hold_out = buf("hold", (T, N, n), np.int32)
         cash_out = buf("cash", (T, N), np.float64)
         val = buf("val", (T + 1, N), np.float64)
+        asset = buf("asset", (T, N), np.float64)   # account value v_{t+1} after step t, before any reset
         cr = None if critic is None else np.ascontiguousarray(critic, dtype=np.float64)
         u = None if u is None else np.ascontiguousarray(u, dtype=np.float32)
         a_rep = None if a_rep is None else np.ascontiguousarray(a_rep, dtype=np.int16)
@@ -230,7 +231,7 @@ class Env:
         ties = lib().orc_rollout(C.byref(self.cfg), _p(self.close), _p(self.feat), C.byref(self._st), int(T),
                                  modes[mode], _p(u), _p(a_rep), _p(w), int(n_hidden), int(hidden), int(act),
                                  int(step0), _p(obs), _p(mu), _p(raw), _p(logp), _p(rew), _p(done), _p(a_out),
-                                 _p(hold_out), _p(cash_out), _p(cr), _p(val), int(nthreads))
+                                 _p(hold_out), _p(cash_out), _p(cr), _p(val), _p(asset), int(nthreads))
         out["near_ties"] = int(ties)
         return out
 
@@ -265,6 +266,61 @@ def fuse(snapshots, prev, tau):
     snap = np.asarray(snapshots, dtype=np.float64)
     mean = snap.sum(axis=0) / snap.shape[0]
     return tau * mean + (1.0 - tau) * np.asarray(prev, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# evaluator: backtest metrics of an account-value curve and the early-stop rule (
+# S:L441–449; R#25).  curve = [v_0, v_1, ..., v_T], float64.
+def cumulative_return(curve):
+    """S:L519 "subtracting the initial value from the final portfolio value, then dividing by the initial value"."""
+    v = np.asarray(curve, dtype=np.float64)
+    return (v[-1] - v[0]) / v[0]
+
+
+def period_returns(curve):
+    v = np.asarray(curve, dtype=np.float64)
+    return v[1:] / v[:-1] - 1.0
+
+
+def annual_return_volatility(curve, periods_per_year):
+    """annual return (v_T/v_0)^(ppy/T) - 1; volatility = sample (n-1) std of the period returns * sqrt(ppy)."""
+    v = np.asarray(curve, dtype=np.float64)
+    T = v.size - 1
+    rho = period_returns(v)
+    ann = (v[-1] / v[0]) ** (periods_per_year / T) - 1.0
+    vol = math.sqrt(((rho - rho.mean()) ** 2).sum() / (rho.size - 1)) * math.sqrt(periods_per_year) if rho.size > 1 else 0.0
+    return ann, vol
+
+
+def sharpe(curve, periods_per_year, rf_per_period=0.0):
+    """(mean(rho) - rf) / std(rho) * sqrt(ppy), sample std; zero volatility -> NaN (degenerate)."""
+    rho = period_returns(curve)
+    if rho.size < 2:
+        return float("nan")
+    sd = math.sqrt(((rho - rho.mean()) ** 2).sum() / (rho.size - 1))
+    return float("nan") if sd == 0.0 else (rho.mean() - rf_per_period) / sd * math.sqrt(periods_per_year)
+
+
+def max_drawdown(curve):
+    """min over t of (v_t / max_{s<=t} v_s - 1), single-pass running peak."""
+    v = np.asarray(curve, dtype=np.float64)
+    peak = -math.inf
+    mdd = 0.0
+    for x in v:
+        peak = max(peak, x)
+        mdd = min(mdd, x / peak - 1.0)
+    return mdd
+
+
+def early_stop(history, patience):
+    """best = argmax (earliest wins); stop when the latest entry is at least `patience` entries
+    after the best (the S:L446 example [1, 2, 1.5, 1.4, 1.3], patience 3 -> stop fixes ">= patience";
+    DESIGN.md R#25)."""
+    h = list(history)
+    if not h:
+        raise ValueError("empty history")
+    best = max(range(len(h)), key=lambda i: (h[i], -i))
+    return (len(h) - 1 - best) >= patience, best
 
 
 def fitness(ep_ret, n_agents):

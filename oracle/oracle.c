@@ -165,7 +165,7 @@ void orc_obs(const orc_cfg* c, const float* close, const float* feat,
  * hold_post / cash_post (optional) get h_{t+1}, b_{t+1} before any reset.  */
 int orc_env_step(const orc_cfg* c, const float* close, orc_state* st, int e,
                  const int32_t* a, double* reward, int64_t* near_tie,
-                 int32_t* hold_post, double* cash_post) {
+                 int32_t* hold_post, double* cash_post, double* asset_post) {
     const int n = c->n_stocks;
     const int64_t t = st->start[e] + st->k[e];
     int32_t* h = st->hold + (int64_t)e * n;
@@ -211,6 +211,7 @@ int orc_env_step(const orc_cfg* c, const float* close, orc_state* st, int e,
     *reward = r;
     if (hold_post) memcpy(hold_post, h, sizeof(int32_t) * (size_t)n);
     if (cash_post) *cash_post = cash;
+    if (asset_post) *asset_post = v1;
     if (done) {
         st->ep_ret[e] = st->disc[e];
         env_reset(c, st, e);
@@ -307,7 +308,7 @@ int64_t orc_rollout(const orc_cfg* c, const float* close, const float* feat, orc
                     const double* weights, int n_hidden, int hidden, int act, uint64_t step0,
                     double* obs, double* mu_out, double* raw_out, double* logp_out,
                     double* rew_out, uint8_t* done_out, int32_t* a_out, int32_t* hold_out,
-                    double* cash_out, const double* critic, double* val_out, int nthreads) {
+                    double* cash_out, const double* critic, double* val_out, double* asset_out, int nthreads) {
     const int N = c->n_envs, n = c->n_stocks, f = c->n_feat;
     const int od = 1 + 2 * n + n * f;
     const int64_t wcount = orc_actor_weight_count(od, n_hidden, hidden, n);
@@ -353,7 +354,8 @@ int64_t orc_rollout(const orc_cfg* c, const float* close, const float* feat, orc
             int64_t nt = 0;
             int d = orc_env_step(c, close, st, e, a, &r, &nt,
                                  hold_out ? hold_out + te * n : NULL,
-                                 cash_out ? cash_out + te : NULL);
+                                 cash_out ? cash_out + te : NULL,
+                                 asset_out ? asset_out + te : NULL);
             ties += nt;
             if (rew_out) rew_out[te] = r;
             if (done_out) done_out[te] = (uint8_t)d;

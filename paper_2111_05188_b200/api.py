@@ -98,10 +98,11 @@ class Trajectory:
     dbg_hold: Optional[torch.Tensor] = None
     dbg_cash: Optional[torch.Tensor] = None
     val: Optional[torch.Tensor] = None    # f32 [T+1, N] critic V(s_t) (R#22)
+    equity: Optional[torch.Tensor] = None  # f64 [T, N] account value after each step (R#25)
 
     @staticmethod
     def allocate(T: int, N: int, n: int, k_pad: int, device="cuda", debug=False, mu=False, sampled=True,
-                 critic=False):
+                 critic=False, equity=False):
         z = dict(device=device)
         return Trajectory(
             obs=torch.empty((T + 1, N, k_pad), dtype=torch.bfloat16, **z),
@@ -114,12 +115,13 @@ class Trajectory:
             dbg_hold=torch.empty((T, N, n), dtype=torch.int32, **z) if debug else None,
             dbg_cash=torch.empty((T, N), dtype=torch.float64, **z) if debug else None,
             val=torch.empty((T + 1, N), dtype=torch.float32, **z) if critic and sampled else None,
+            equity=torch.empty((T, N), dtype=torch.float64, **z) if equity else None,
         )
 
     def c(self) -> _lib.Traj:
         return _lib.Traj(*[None if x is None else x.data_ptr() for x in
                            (self.obs, self.act, self.logp, self.rew, self.done, self.mu, self.dbg_aint,
-                            self.dbg_hold, self.dbg_cash, self.val)])
+                            self.dbg_hold, self.dbg_cash, self.val, self.equity)])
 
 
 class Env:
@@ -247,6 +249,26 @@ def fuse_pods(cfg: _lib.EnvConfig, n_hidden: int, hidden: int, params: torch.Ten
                                params.shape[1], P_local, int(K_local), float(tau), _ptr(prev), _ptr(work),
                                _stream(stream)), "pod_fuse_pods")
     return prev
+
+
+def backtest_metrics(v0: torch.Tensor, curve: torch.Tensor, periods_per_year: float, rf_per_period: float = 0.0,
+                     stream=None) -> torch.Tensor:
+    """Evaluator metrics per env (pod_backtest_metrics, R#25): returns f64 [5, N] = cumulative return, annual
+    return, annual volatility, Sharpe (NaN if degenerate), max drawdown."""
+    T, N = curve.shape
+    out = torch.empty((5, N), dtype=torch.float64, device=curve.device)
+    check(load().pod_backtest_metrics(_ptr(v0), _ptr(curve), T, N, float(periods_per_year), float(rf_per_period),
+                                      _ptr(out), _stream(stream)), "pod_backtest_metrics")
+    return out
+
+
+def early_stop(history, patience: int):
+    """(stop, best) of the evaluator's early-stop rule (pod_early_stop, R#25)."""
+    h = np.ascontiguousarray(history, dtype=np.float64)
+    stop, best = C.c_int32(0), C.c_int32(0)
+    check(load().pod_early_stop(h.ctypes.data_as(C.c_void_p), h.size, int(patience), C.byref(stop), C.byref(best)),
+          "pod_early_stop")
+    return bool(stop.value), int(best.value)
 
 
 class Comm:

@@ -79,6 +79,7 @@ struct EnvArgs {
     uint16_t* obs_out;        // [N][k_pad] bf16 slice (s_{t+1}, or s_t for mode 1/2), may be null
     int32_t* dbg_hold;        // [N][n] slice or null
     double* dbg_cash;         // [N] slice or null
+    double* equity;           // [N] slice of step t: v_{t+1} before any reset, or null
     uint32_t* err;
 };
 
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 a.rew[e] = static_cast<float>(r);
                 a.done[e] = done ? 1 : 0;
                 if (a.dbg_cash) a.dbg_cash[e] = cash;
+                if (a.equity) a.equity[e] = v1;
                 if (!isfinite(v1)) atomicOr(a.err, 2u);
                 if (done) a.ep_ret[e] = disc;
             }

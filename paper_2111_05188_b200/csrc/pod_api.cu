@@ -18,6 +18,7 @@
 #include "actor_pair_kernel.cuh"
 #include "env_kernel.cuh"
 #include "fuse_kernel.cuh"
+#include "metrics_kernel.cuh"
 #include "gae_kernel.cuh"
 #include "pod.h"
 #include "pod_internal.h"
@@ -184,7 +185,7 @@ extern "C" pod_status pod_actor_layout_get(const pod_env_config* cfg, int32_t n_
 
 struct GraphKey {
     int32_t T, deterministic, n_hidden, hidden, act, profile;
-    const void* ptrs[13];
+    const void* ptrs[14];
     size_t param_bytes;
 };
 
@@ -605,6 +606,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         a.obs_out = tr->obs + static_cast<int64_t>(t + 1) * N * e->k_pad;
         a.dbg_hold = tr->dbg_hold ? tr->dbg_hold + static_cast<int64_t>(t) * N * n : nullptr;
         a.dbg_cash = tr->dbg_cash ? tr->dbg_cash + static_cast<int64_t>(t) * N : nullptr;
+        a.equity = tr->equity ? tr->equity + static_cast<int64_t>(t) * N : nullptr;
         a.gen_noise = (sampling && t + 1 < T) ? 1 : 0;   // noise for the actor launch of step t+1
         a.noise_t = t + 1;
         env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
@@ -761,8 +763,8 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         key.ptrs[0] = actor->params;
     }
     const void* ptrs[] = {tr->obs, tr->act, tr->logp, tr->rew, tr->done, tr->mu, tr->dbg_aint,
-                          tr->dbg_hold, tr->dbg_cash, injected_u, fitness_out, tr->val};
-    for (int i = 0; i < 12; ++i) key.ptrs[1 + i] = ptrs[i];
+                          tr->dbg_hold, tr->dbg_cash, injected_u, fitness_out, tr->val, tr->equity};
+    for (int i = 0; i < 13; ++i) key.ptrs[1 + i] = ptrs[i];
     GraphEntry* hit = nullptr;
     for (auto& g : e->graphs)
         if (memcmp(&g.key, &key, sizeof(key)) == 0) hit = &g;
@@ -1064,5 +1066,32 @@ extern "C" pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg,
     }
     fuse_blend_kernel<<<grid, 256, 0, s>>>(a);
     POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+// ------------------------------------------------------------ evaluator (R#25)
+extern "C" pod_status pod_backtest_metrics(const double* v0, const double* curve, int32_t T, int32_t N,
+                                           double periods_per_year, double rf_per_period, double* out, void* stream) {
+    if (!v0 || !curve || !out) return pod_fail(POD_ERR_ARG, "v0, curve and out must be non-NULL");
+    if (T < 1 || N < 1) return pod_fail(POD_ERR_ARG, "T and N must be >= 1");
+    if (!(periods_per_year > 0.0)) return pod_fail(POD_ERR_ARG, "periods_per_year must be > 0");
+    pod_status st = pod_require_sm100();
+    if (st) return st;
+    backtest_metrics_kernel<<<static_cast<unsigned>((N + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        v0, curve, T, N, periods_per_year, rf_per_period, out);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+extern "C" pod_status pod_early_stop(const double* history, int32_t len, int32_t patience, int32_t* stop,
+                                     int32_t* best) {
+    if (!history || !stop || !best) return pod_fail(POD_ERR_ARG, "NULL argument");
+    if (len < 1) return pod_fail(POD_ERR_ARG, "history is empty");
+    if (patience < 0) return pod_fail(POD_ERR_ARG, "patience must be >= 0");
+    int b = 0;
+    for (int i = 1; i < len; ++i)
+        if (history[i] > history[b]) b = i;   // strict: the earliest maximum wins
+    *best = b;
+    *stop = (len - 1 - b) >= patience ? 1 : 0;
     return POD_OK;
 }

@@ -484,3 +484,29 @@ def test_fuse_pods_parity(tau):
     c.env.reset(c.starts)
     c.env.rollout(2, tr, actor=actor)
     c.env.check()
+
+
+def test_equity_curve_exact_and_backtest_metrics():
+    """R#25: traj.equity (v_{t+1} after each step) equals the oracle's float64 account value bit for bit;
+    the device backtest metrics of those curves match the oracle's metric definitions."""
+    c = Case(n=30, f=3, T_data=400, N=96, H=300, seed=41)
+    T = 60
+    u = synth.injected_u("uniform", T, c.N, c.n, 5)
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, sampled=False, equity=True)
+    c.env.reset(c.starts)
+    _, _, v0, _ = c.env.read_state()
+    c.env.rollout(T, tr, injected_u=torch.from_numpy(u).cuda())
+    o = c.oracle_env()
+    out = o.rollout(T, "inject", u=u, want=("asset",))
+    np.testing.assert_array_equal(tr.equity.cpu().numpy(), out["asset"])
+    m = api.backtest_metrics(v0, tr.equity, 252.0).cpu().numpy()
+    curves = np.concatenate([v0.cpu().numpy()[None, :], out["asset"]], axis=0)
+    for e in range(c.N):
+        cv = curves[:, e]
+        ann, vol = oracle.annual_return_volatility(cv, 252.0)
+        exp = [oracle.cumulative_return(cv), ann, vol, oracle.sharpe(cv, 252.0), oracle.max_drawdown(cv)]
+        np.testing.assert_allclose(m[:, e], exp, rtol=1e-11, atol=1e-13, equal_nan=True)
+    # degenerate curve: constant value -> zero return / volatility / drawdown, Sharpe NaN
+    flat = torch.full((5, 3), 7.0, dtype=torch.float64, device="cuda")
+    mf = api.backtest_metrics(torch.full((3,), 7.0, dtype=torch.float64, device="cuda"), flat, 252.0).cpu().numpy()
+    assert np.all(mf[[0, 1, 2, 4]] == 0.0) and np.all(np.isnan(mf[3]))

@@ -89,6 +89,21 @@ def test_layout_n_elems():
         assert L.n_out_pad >= n + 1 and L.n_out_pad % 32 == 0   # row n is the critic (R#22)
 
 
+def test_early_stop_matches_oracle():
+    """pod_early_stop (host) vs the oracle rule (R#25) on the S:L446–448 examples and random histories."""
+    assert api.early_stop([1.0, 2.0, 1.5, 1.4, 1.3], 3) == (True, 1)
+    assert api.early_stop([1.0, 2.0, 3.0, 4.0], 2) == (False, 3)
+    assert api.early_stop([2.0, 2.0], 1)[1] == 0
+    rng = np.random.default_rng(4)
+    for _ in range(300):
+        h = rng.integers(0, 6, size=int(rng.integers(1, 12))).astype(float)
+        p = int(rng.integers(0, 5))
+        assert api.early_stop(h, p) == oracle.early_stop(h, p)
+    with pytest.raises(_lib.PodError) as ei:
+        api.early_stop([], 1)
+    assert ei.value.name == "POD_ERR_ARG"
+
+
 def test_elite_plan_matches_oracle():
     rng = np.random.default_rng(0)
     for _ in range(200):

@@ -505,3 +505,46 @@ def test_select_brute_force_and_invariants():
         oracle.select_elite(np.array([1.0, np.nan]), 1)
     with pytest.raises(ValueError):
         oracle.select_elite(np.array([1.0]), 2)
+
+
+# ---------------------------------------------------------------------------
+# evaluator metrics (R#25)
+# ---------------------------------------------------------------------------
+def test_backtest_metric_pins():
+    assert oracle.cumulative_return([1_000_000.0, 1_700_000.0, 2_495_530.0]) == pytest.approx(1.49553, abs=1e-12)
+    assert oracle.cumulative_return([5.0, 5.0, 5.0]) == 0.0
+    assert oracle.cumulative_return([10.0, 4.0, 0.0]) == -1.0
+    # max drawdown vs an exhaustive peak-trough pair scan
+    assert oracle.max_drawdown([100.0, 120.0, 90.0, 110.0]) == pytest.approx(-0.25, abs=1e-15)
+    assert oracle.max_drawdown([100.0]) == 0.0
+    assert oracle.max_drawdown(np.arange(1.0, 20.0)) == 0.0
+    rng = np.random.default_rng(8)
+    for _ in range(20):
+        v = np.cumprod(1.0 + rng.normal(0, 0.05, size=30)) * 100.0
+        brute = min([0.0] + [v[j] / v[i] - 1.0 for i in range(30) for j in range(i, 30)])
+        assert oracle.max_drawdown(v) == pytest.approx(brute, abs=1e-15)
+    # constant per-period return r with ppy = T: annual return (1 + r)^T - 1, volatility 0
+    r, T = 0.01, 12
+    curve = 100.0 * (1.0 + r) ** np.arange(T + 1)
+    ann, vol = oracle.annual_return_volatility(curve, T)
+    assert ann == pytest.approx((1 + r) ** T - 1, rel=1e-12) and vol == pytest.approx(0.0, abs=1e-12)
+    ann, vol = oracle.annual_return_volatility([1.0, 2.0], 1)
+    assert ann == pytest.approx(1.0, rel=1e-15)
+    # Sharpe: zero-mean alternating returns -> 0; constant returns -> degenerate (NaN); S:L539 worked case
+    alt = np.cumprod(np.r_[1.0, np.tile([1.01, 1.0 / 1.01], 5)])
+    rho = oracle.period_returns(alt)
+    assert oracle.sharpe(alt, 252) == pytest.approx(rho.mean() / rho.std(ddof=1) * math.sqrt(252), rel=1e-12)
+    assert math.isnan(oracle.sharpe(2.0 ** np.arange(6.0), 252))   # returns exactly 1.0 each period
+    c3 = np.cumprod([1.0, 1.01, 1.02, 0.995])
+    rho3 = np.array([0.01, 0.02, -0.005])
+    assert oracle.sharpe(c3, 252) == pytest.approx(rho3.mean() / np.std(rho3, ddof=1) * math.sqrt(252), rel=1e-10)
+
+
+def test_early_stop_pins():
+    # S:L446–448
+    assert oracle.early_stop([1.0, 2.0, 1.5, 1.4, 1.3], 3) == (True, 1)
+    assert oracle.early_stop([1.0, 2.0, 3.0, 4.0], 2) == (False, 3)
+    assert oracle.early_stop([2.0, 2.0], 1)[1] == 0          # earliest wins
+    assert oracle.early_stop([2.0, 2.0], 2) == (False, 0)
+    with pytest.raises(ValueError):
+        oracle.early_stop([], 1)
