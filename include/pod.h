@@ -287,6 +287,51 @@ pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_
                          void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
                          float* prev, float* work, void* stream);
 
+/* ------------------------------------------------------------ PPO update */
+/* Learner hyper-parameters (P:L472 PPO; Table 3 via S:L239–241; R#26). */
+typedef struct {
+    float ratio_clip;      /* epsilon, Table 3 "Ratio clip (PPO)" 0.25        */
+    float entropy_coef;    /* Table 3 "Lambda entropy (PPO)" 0.02            */
+    float value_coef;      /* 0.5 (S:L239 design decision)                   */
+    float learning_rate;   /* Table 3 2^-14                                  */
+    float adam_beta1;      /* 0.9                                            */
+    float adam_beta2;      /* 0.999                                          */
+    float adam_eps;        /* 1e-8                                           */
+    float reserved;
+} pod_ppo_hparams;
+
+/* Workspace bytes of pod_ppo_update for minibatches of `batch` rows (host). */
+pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, int32_t batch,
+                                  size_t* bytes);
+
+/* PPO clipped-surrogate update of one agent (R#26), on
+ * the device buffers of a rollout: for each of the n_minibatches minibatches
+ * (rows perm[j*batch .. (j+1)*batch) of the flattened buffer; the caller
+ * shuffles and concatenates repeat_times permutations), with
+ *   rho = exp(logp_theta(raw | s) - logp_old),
+ *   L = -mean[min(rho A, clip(rho, 1-eps, 1+eps) A)] - c_ent H(pi)
+ *       + c_v mean[(V(s) - R)^2],   H(pi) = sum_i (log sigma_i + (1 + ln 2 pi)/2),
+ * the gradient of L (float32 forward + backward through the bf16-rollout MLP's
+ * float32 master copy; GEMMs on cuBLAS) and one Adam step (bias-corrected,
+ * step t = adam_t + j + 1):  m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
+ *   theta <- theta - lr (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps).
+ * Afterwards the agent's rollout slab `params` (pod_actor_layout; agent 0 of
+ * the slab array) is rewritten from theta (bf16 weights, RNE).
+ *   master, adam_m, adam_v [dev] f32 [layout.n_elems] (pod_fuse_pods order), in/out;
+ *   obs [dev] bf16 [M][k_pad], act_raw f32 [M][n], logp_old, adv, ret f32 [M]
+ *   (traj.obs rows 0..T-1, traj.act, traj.logp, normalised advantages, returns);
+ *   perm [dev] i32 [n_minibatches * batch] row indices in [0, M);
+ *   losses [dev] f64 [4] accumulates (sum of the surrogate objective, sum of
+ *   (V - R)^2, entropy per minibatch, rows); grad_out [dev] f32 [n_elems] or
+ *   NULL: the last minibatch's gradient (diagnostics); ws >=
+ *   pod_ppo_workspace_size.  Stream-ordered.  Errors: ARG, SHAPE, UNSUPPORTED, CUDA. */
+pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, int32_t act,
+                          const pod_ppo_hparams* hp, float* master, float* adam_m, float* adam_v, int64_t adam_t,
+                          void* params, size_t param_bytes, const uint16_t* obs, const float* act_raw,
+                          const float* logp_old, const float* adv, const float* ret, int64_t M,
+                          const int32_t* perm, int32_t batch, int32_t n_minibatches, double* losses,
+                          float* grad_out, void* ws, size_t ws_bytes, void* stream);
+
 /* ----------------------------------------------------------- evaluator */
 /* Backtest metrics of one account-value curve per env (§5.2
  * "cumulative return ... annual return ... annual volatility ... Sharpe ratio

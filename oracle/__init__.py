@@ -323,6 +323,77 @@ def early_stop(history, patience):
     return (len(h) - 1 - best) >= patience, best
 
 
+# ---------------------------------------------------------------------------
+# PPO learner (Table 3; R#26), float64, on the flat parameter vector in the
+# documented slab order: W_0 [h][k_pad], W_1..W_{L-1} [h][h], W_L [n_out_pad][h], b_0.., b_L, log_std [n_out_pad].
+def ppo_unflatten(theta, k_pad, hidden, n_hidden, n_out_pad):
+    th = np.asarray(theta, dtype=np.float64)
+    shapes = [(hidden, k_pad)] + [(hidden, hidden)] * (n_hidden - 1) + [(n_out_pad, hidden)]
+    Ws, bs, o = [], [], 0
+    for r, c in shapes:
+        Ws.append(th[o : o + r * c].reshape(r, c))
+        o += r * c
+    for r, _ in shapes:
+        bs.append(th[o : o + r])
+        o += r
+    ls = th[o : o + n_out_pad]
+    assert o + n_out_pad == th.size
+    return Ws, bs, ls
+
+
+def ppo_loss_grad(theta, dims, obs, act_raw, logp_old, adv, ret, eps, c_ent, c_v, act=0):
+    """Minibatch loss L = -mean(min(rho A, clip(rho, 1-eps, 1+eps) A)) - c_ent H + c_v mean((V - R)^2),
+    H = sum_i (log sigma_i + (1 + ln 2 pi)/2), and its analytic gradient (backpropagation written out; the
+    min's derivative is that of rho A when rho A <= clip(rho) A, else 0).  dims = (k_pad, hidden, n_hidden,
+    n, n_out_pad).  Returns (L, grad [same layout as theta], (sum objective, sum (V-R)^2, H))."""
+    k_pad, hidden, n_hidden, n, n_out_pad = dims
+    Ws, bs, ls = ppo_unflatten(theta, k_pad, hidden, n_hidden, n_out_pad)
+    X = [np.asarray(obs, dtype=np.float64)]
+    f = (lambda z: np.maximum(z, 0.0)) if act == 0 else np.tanh
+    for l in range(n_hidden):
+        X.append(f(X[-1] @ Ws[l].T + bs[l]))
+    Z = X[-1] @ Ws[-1].T + bs[-1]
+    B = Z.shape[0]
+    mu, V = Z[:, :n], Z[:, n]
+    sig = np.exp(ls[:n])
+    raw = np.asarray(act_raw, dtype=np.float64)
+    z = (raw - mu) / sig
+    logp = (-0.5 * z * z - ls[:n] - 0.5 * math.log(2 * math.pi)).sum(axis=1)
+    A = np.asarray(adv, dtype=np.float64)
+    R = np.asarray(ret, dtype=np.float64)
+    rho = np.exp(logp - np.asarray(logp_old, dtype=np.float64))
+    s1 = rho * A
+    s2 = np.clip(rho, 1.0 - eps, 1.0 + eps) * A
+    active = s1 <= s2
+    obj = np.where(active, s1, s2)
+    H = float((ls[:n] + 0.5 * (1.0 + math.log(2 * math.pi))).sum())
+    Lval = -obj.mean() - c_ent * H + c_v * ((V - R) ** 2).mean()
+    coef = np.where(active, -A * rho / B, 0.0)                 # dL/dlogp per sample
+    dZ = np.zeros_like(Z)
+    dZ[:, :n] = coef[:, None] * z / sig
+    dZ[:, n] = 2.0 * c_v * (V - R) / B
+    g_ls = np.zeros(n_out_pad)
+    g_ls[:n] = (coef[:, None] * (z * z - 1.0)).sum(axis=0) - c_ent
+    gW, gb = [None] * (n_hidden + 1), [None] * (n_hidden + 1)
+    d = dZ
+    for l in range(n_hidden, -1, -1):
+        gW[l] = d.T @ X[l]
+        gb[l] = d.sum(axis=0)
+        if l > 0:
+            dx = d @ Ws[l]
+            d = dx * ((X[l] > 0.0) if act == 0 else (1.0 - X[l] ** 2))
+    grad = np.concatenate([g.ravel() for g in gW] + [g.ravel() for g in gb] + [g_ls])
+    return Lval, grad, (float(obj.sum()), float(((V - R) ** 2).sum()), H)
+
+
+def adam_step(theta, m, v, g, t, lr, b1=0.9, b2=0.999, eps=1e-8):
+    """Bias-corrected Adam (Kingma & Ba) for minimisation; t counts from 1.  Returns (theta, m, v)."""
+    m = b1 * np.asarray(m, dtype=np.float64) + (1.0 - b1) * g
+    v = b2 * np.asarray(v, dtype=np.float64) + (1.0 - b2) * g * g
+    th = np.asarray(theta, dtype=np.float64) - lr * (m / (1.0 - b1 ** t)) / (np.sqrt(v / (1.0 - b2 ** t)) + eps)
+    return th, m, v
+
+
 def fitness(ep_ret, n_agents):
     ep = np.ascontiguousarray(ep_ret, dtype=np.float64)
     J = np.zeros(n_agents)

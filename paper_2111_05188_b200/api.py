@@ -271,6 +271,46 @@ def early_stop(history, patience: int):
     return bool(stop.value), int(best.value)
 
 
+class PPOLearner:
+    """PPO clipped-surrogate learner of agent 0 (pod_ppo_update, R#26) on a float32 master copy of the rollout
+    slab, with Adam moments; `update` runs minibatches over the flattened rollout buffers and refreshes the
+    rollout slab (bf16) in place."""
+
+    def __init__(self, cfg: _lib.EnvConfig, n_hidden: int, hidden: int, params: torch.Tensor, act: int = 0,
+                 batch: int = 1024, ratio_clip=0.25, entropy_coef=0.02, value_coef=0.5, learning_rate=2.0 ** -14,
+                 betas=(0.9, 0.999), adam_eps=1e-8):
+        self.cfg, self.n_hidden, self.hidden, self.act, self.batch = cfg, n_hidden, hidden, act, batch
+        self.params = params
+        L = actor_layout(cfg, n_hidden, hidden)
+        self.n_elems = int(L.n_elems)
+        dev = params.device
+        self.master = torch.empty(self.n_elems, dtype=torch.float32, device=dev)
+        # widen the rollout slab of agent 0 into the master copy (fusion with K = 1, tau = 1: slab unchanged)
+        fuse_pods(cfg, n_hidden, hidden, params[:1], 1, tau=1.0, prev=self.master.view(1, -1))
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        self.t = 0
+        self.hp = _lib.PpoHparams(ratio_clip, entropy_coef, value_coef, learning_rate, betas[0], betas[1], adam_eps, 0.0)
+        nb = C.c_size_t(0)
+        check(load().pod_ppo_workspace_size(C.byref(cfg), n_hidden, hidden, batch, C.byref(nb)), "pod_ppo_workspace_size")
+        self.ws = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+        self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    def update(self, obs: torch.Tensor, act_raw: torch.Tensor, logp_old: torch.Tensor, adv: torch.Tensor,
+               ret: torch.Tensor, perm: torch.Tensor, grad_out: Optional[torch.Tensor] = None, stream=None):
+        """obs bf16 [M, k_pad], act_raw f32 [M, n], logp_old/adv/ret f32 [M], perm i32 [n_mb * batch]."""
+        M = obs.shape[0]
+        n_mb = perm.numel() // self.batch
+        self.losses.zero_()
+        check(load().pod_ppo_update(C.byref(self.cfg), self.n_hidden, self.hidden, self.act, C.byref(self.hp),
+                                    _ptr(self.master), _ptr(self.m), _ptr(self.v), self.t, _ptr(self.params),
+                                    self.params.shape[1], _ptr(obs), _ptr(act_raw), _ptr(logp_old), _ptr(adv),
+                                    _ptr(ret), M, _ptr(perm), self.batch, n_mb, _ptr(self.losses), _ptr(grad_out),
+                                    _ptr(self.ws), self.ws.numel(), _stream(stream)), "pod_ppo_update")
+        self.t += n_mb
+        return self.losses
+
+
 class Comm:
     """NCCL communicator of libpod (one process per GPU).  The torch process
     group (if any) only broadcasts the 128-byte unique id."""

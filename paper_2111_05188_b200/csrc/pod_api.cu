@@ -1095,3 +1095,5 @@ extern "C" pod_status pod_early_stop(const double* history, int32_t len, int32_t
     *stop = (len - 1 - b) >= patience ? 1 : 0;
     return POD_OK;
 }
+
+#include "pod_ppo.cuh"

@@ -1,0 +1,201 @@
+// pod_ppo.cuh — host side of pod_ppo_update (included by pod_api.cu; kernels in ppo_kernel.cuh).
+// Forward/backward GEMMs are plain float32 library GEMMs (cuBLAS, column-major view of the
+// row-major [rows][cols] matrices); every other step runs in this library's kernels.
+#pragma once
+#include <cublas_v2.h>
+
+#include "ppo_kernel.cuh"
+
+namespace pod {
+
+struct PpoWs {
+    size_t x0, h, zh, d0, d1, act, lpo, adv, ret, grad, total;
+};
+
+inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, int B, int n) {
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    PpoWs w{};
+    size_t o = 0;
+    w.x0 = o;  o += up(sizeof(float) * B * L.k_pad);
+    w.h = o;   o += up(sizeof(float) * static_cast<size_t>(B) * hidden * n_hidden);
+    w.zh = o;  o += up(sizeof(float) * static_cast<size_t>(B) * L.n_out_pad);
+    const size_t dmax = static_cast<size_t>(B) * (hidden > L.n_out_pad ? hidden : L.n_out_pad);
+    w.d0 = o;  o += up(sizeof(float) * dmax);
+    w.d1 = o;  o += up(sizeof(float) * dmax);
+    w.act = o; o += up(sizeof(float) * static_cast<size_t>(B) * n);
+    w.lpo = o; o += up(sizeof(float) * B);
+    w.adv = o; o += up(sizeof(float) * B);
+    w.ret = o; o += up(sizeof(float) * B);
+    w.grad = o; o += up(sizeof(float) * L.n_elems);
+    w.total = o;
+    return w;
+}
+
+inline cublasHandle_t ppo_cublas() {
+    static thread_local cublasHandle_t h = nullptr;
+    static thread_local int dev = -1;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!h || d != dev) {
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+        cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);   // float32 GEMMs, no TF32
+        dev = d;
+    }
+    return h;
+}
+
+}  // namespace pod
+
+extern "C" pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                             int32_t batch, size_t* bytes) {
+    if (!bytes) return pod_fail(POD_ERR_ARG, "bytes is NULL");
+    if (batch < 1) return pod_fail(POD_ERR_ARG, "batch must be >= 1");
+    pod_actor_layout L;
+    pod_status st = pod_actor_layout_get(cfg, n_hidden, hidden, &L);
+    if (st) return st;
+    *bytes = pod::ppo_ws_layout(L, n_hidden, hidden, batch, cfg->n_stocks).total;
+    return POD_OK;
+}
+
+#define POD_CUBLAS(call)                                                                      \
+    do {                                                                                      \
+        cublasStatus_t _s = (call);                                                           \
+        if (_s != CUBLAS_STATUS_SUCCESS) return pod_fail(POD_ERR_CUDA, "%s: cuBLAS status %d", #call, static_cast<int>(_s)); \
+    } while (0)
+
+extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, int32_t act,
+                                     const pod_ppo_hparams* hp, float* master, float* adam_m, float* adam_v,
+                                     int64_t adam_t, void* params, size_t param_bytes, const uint16_t* obs,
+                                     const float* act_raw, const float* logp_old, const float* adv, const float* ret,
+                                     int64_t M, const int32_t* perm, int32_t batch, int32_t n_minibatches,
+                                     double* losses, float* grad_out, void* ws, size_t ws_bytes, void* stream) {
+    using namespace pod;
+    if (!hp || !master || !adam_m || !adam_v || !params || !obs || !act_raw || !logp_old || !adv || !ret || !perm ||
+        !losses || !ws)
+        return pod_fail(POD_ERR_ARG, "NULL argument");
+    if (act != 0 && act != 1) return pod_fail(POD_ERR_ARG, "act must be 0 (ReLU) or 1 (tanh)");
+    if (batch < 1 || n_minibatches < 0 || M < 1 || adam_t < 0) return pod_fail(POD_ERR_ARG, "bad batch / M / adam_t");
+    if (!(hp->ratio_clip > 0.0f && hp->ratio_clip < 1.0f) || !(hp->learning_rate > 0.0f) || hp->entropy_coef < 0.0f ||
+        hp->value_coef < 0.0f || !(hp->adam_beta1 >= 0.0f && hp->adam_beta1 < 1.0f) ||
+        !(hp->adam_beta2 >= 0.0f && hp->adam_beta2 < 1.0f) || !(hp->adam_eps > 0.0f))
+        return pod_fail(POD_ERR_ARG, "hyper-parameters out of range (0 < ratio_clip < 1, lr > 0, betas in [0,1))");
+    pod_actor_layout L;
+    pod_status st = pod_actor_layout_get(cfg, n_hidden, hidden, &L);
+    if (st) return st;
+    if (param_bytes < L.param_bytes || param_bytes % 16 != 0)
+        return pod_fail(POD_ERR_SHAPE, "param_bytes %zu must be >= %zu and a multiple of 16", param_bytes, L.param_bytes);
+    const int n = cfg->n_stocks;
+    const PpoWs W = ppo_ws_layout(L, n_hidden, hidden, batch, n);
+    if (ws_bytes < W.total) return pod_fail(POD_ERR_ARG, "workspace needs %zu bytes", W.total);
+    if (reinterpret_cast<uintptr_t>(ws) % 256 != 0 || reinterpret_cast<uintptr_t>(master) % 16 != 0 ||
+        reinterpret_cast<uintptr_t>(params) % 16 != 0)
+        return pod_fail(POD_ERR_ARG, "ws must be 256-byte aligned, master and params 16-byte aligned");
+    st = pod_require_sm100();
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cublasHandle_t cb = ppo_cublas();
+    if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate failed");
+    POD_CUBLAS(cublasSetStream(cb, s));
+    char* w = static_cast<char*>(ws);
+    float* x0 = reinterpret_cast<float*>(w + W.x0);
+    float* hbuf = reinterpret_cast<float*>(w + W.h);
+    float* zh = reinterpret_cast<float*>(w + W.zh);
+    float* d0 = reinterpret_cast<float*>(w + W.d0);
+    float* d1 = reinterpret_cast<float*>(w + W.d1);
+    float* act_b = reinterpret_cast<float*>(w + W.act);
+    float* lpo_b = reinterpret_cast<float*>(w + W.lpo);
+    float* adv_b = reinterpret_cast<float*>(w + W.adv);
+    float* ret_b = reinterpret_cast<float*>(w + W.ret);
+    float* grad = reinterpret_cast<float*>(w + W.grad);
+    // flat offsets (elements) of W_l, b_l, log_std: pod_fuse_pods order
+    int64_t woff[POD_MAX_HIDDEN_LAYERS + 1], boff[POD_MAX_HIDDEN_LAYERS + 1];
+    int64_t f = 0;
+    for (int l = 0; l < L.n_layers; ++l) {
+        woff[l] = f;
+        f += static_cast<int64_t>(L.w_rows[l]) * L.w_cols[l];
+    }
+    for (int l = 0; l < L.n_layers; ++l) {
+        boff[l] = f;
+        f += L.w_rows[l];
+    }
+    const int64_t lsoff = f;
+    const float one = 1.0f, zero = 0.0f;
+    const int B = batch;
+    const unsigned eg = 148 * 4;
+    for (int j = 0; j < n_minibatches; ++j) {
+        ppo_gather_kernel<<<B, 128, 0, s>>>(obs, act_raw, logp_old, adv, ret, perm + static_cast<int64_t>(j) * B, B,
+                                            L.k_pad, n, x0, act_b, lpo_b, adv_b, ret_b);
+        // forward: X_{l+1} = act(X_l W_l^T + b_l); head without activation
+        const float* xin = x0;
+        for (int l = 0; l < L.n_layers; ++l) {
+            const int rows = L.w_rows[l], cols = L.w_cols[l];
+            const bool head = l == L.n_layers - 1;
+            float* out = head ? zh : hbuf + static_cast<int64_t>(l) * B * hidden;
+            POD_CUBLAS(cublasSgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, rows, B, cols, &one, master + woff[l], cols, xin, cols,
+                                   &zero, out, rows));
+            ppo_bias_act_kernel<<<eg, 256, 0, s>>>(out, master + boff[l], B, rows, head ? -1 : act);
+            xin = out;
+        }
+        // head loss and dL/d(head output) -> d0 [B][n_out_pad]; gradient vector cleared first
+        POD_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * L.n_elems, s));
+        PpoHead hh{B, n, L.n_out_pad, hp->ratio_clip, hp->entropy_coef, hp->value_coef, act_b, lpo_b, adv_b, ret_b,
+                   zh, master + lsoff, d0, grad + lsoff, losses};
+        ppo_head_kernel<<<(B + 127) / 128, 128, 0, s>>>(hh);
+        ppo_entropy_kernel<<<1, 128, 0, s>>>(master + lsoff, n, hp->entropy_coef, grad + lsoff, losses);
+        // backward: dW_l = delta_l^T X_l, db_l = colsum(delta_l), delta_{l-1} = (delta_l W_l) * act'(X_l)
+        float* dcur = d0;
+        float* dnext = d1;
+        for (int l = L.n_layers - 1; l >= 0; --l) {
+            const int rows = L.w_rows[l], cols = L.w_cols[l];
+            const float* xl = l == 0 ? x0 : hbuf + static_cast<int64_t>(l - 1) * B * hidden;
+            POD_CUBLAS(cublasSgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, cols, rows, B, &one, xl, cols, dcur, rows, &zero,
+                                   grad + woff[l], cols));
+            ppo_colsum_kernel<<<(rows + 127) / 128, 128, 0, s>>>(dcur, B, rows, grad + boff[l]);
+            if (l > 0) {
+                POD_CUBLAS(cublasSgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, cols, B, rows, &one, master + woff[l], cols, dcur,
+                                       rows, &zero, dnext, cols));
+                ppo_act_grad_kernel<<<eg, 256, 0, s>>>(dnext, xl, static_cast<int64_t>(B) * cols, act);
+                float* t = dcur;
+                dcur = dnext;
+                dnext = t;
+            }
+        }
+        const int64_t step = adam_t + j + 1;
+        const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta1), static_cast<double>(step)));
+        const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta2), static_cast<double>(step)));
+        if (grad_out && j == n_minibatches - 1)
+            POD_CUDA(cudaMemcpyAsync(grad_out, grad, sizeof(float) * L.n_elems, cudaMemcpyDeviceToDevice, s));
+        ppo_adam_kernel<<<eg, 256, 0, s>>>(master, adam_m, adam_v, grad, static_cast<int64_t>(L.n_elems),
+                                           hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps, c1, c2);
+        POD_CUDA(cudaGetLastError());
+    }
+    // refresh the rollout slab (agent 0) from the master copy: the fusion narrowing with K = 1, tau = 1
+    FuseArgs fa{};
+    {
+        uint64_t fl = 0;
+        int ns = 0;
+        for (int l = 0; l < L.n_layers; ++l) {
+            fa.seg[ns++] = FuseSeg{L.w_offset[l], fl, static_cast<uint32_t>(L.w_rows[l]) * L.w_cols[l], 1u};
+            fl += static_cast<uint64_t>(L.w_rows[l]) * L.w_cols[l];
+        }
+        for (int l = 0; l < L.n_layers; ++l) {
+            fa.seg[ns++] = FuseSeg{L.b_offset[l], fl, static_cast<uint32_t>(L.w_rows[l]), 0u};
+            fl += static_cast<uint64_t>(L.w_rows[l]);
+        }
+        fa.seg[ns++] = FuseSeg{L.log_std_offset, fl, static_cast<uint32_t>(L.n_out_pad), 0u};
+        fl += static_cast<uint64_t>(L.n_out_pad);
+        fa.n_seg = ns;
+        fa.K_local = 1;
+        fa.n_elems = static_cast<int64_t>(fl);
+        fa.param_bytes = param_bytes;
+        fa.params = static_cast<char*>(params);
+        fa.work = master;
+        fa.prev = nullptr;
+        fa.scale = 1.0f;
+        fa.tau = 1.0f;
+    }
+    const int64_t g8 = fa.n_elems / 8;
+    fuse_blend_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>((g8 + 255) / 256, 8 * 148)), 1), 256, 0, s>>>(fa);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}

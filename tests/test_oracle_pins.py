@@ -548,3 +548,80 @@ def test_early_stop_pins():
     assert oracle.early_stop([2.0, 2.0], 2) == (False, 0)
     with pytest.raises(ValueError):
         oracle.early_stop([], 1)
+
+
+# ---------------------------------------------------------------------------
+# PPO learner (R#26)
+# ---------------------------------------------------------------------------
+def _ppo_problem(seed, act=1, B=24):
+    rng = np.random.default_rng(seed)
+    dims = (8, 5, 2, 2, 4)   # k_pad, hidden, n_hidden, n, n_out_pad
+    k_pad, hid, nh, n, nop = dims
+    ne = hid * k_pad + hid * hid + nop * hid + hid + hid + nop + nop
+    theta = rng.normal(size=ne) * 0.5
+    obs = np.zeros((B, k_pad))
+    obs[:, :6] = rng.normal(size=(B, 6))
+    act_raw = rng.normal(size=(B, n))
+    return rng, dims, theta, obs, act_raw
+
+
+def test_ppo_gradient_matches_finite_differences():
+    """the analytic gradient of the total loss matches central finite differences (here within 1e-6
+    relative, float64), on a smooth (tanh) network with ratios away from the clip boundaries."""
+    rng, dims, theta, obs, act_raw = _ppo_problem(1)
+    B = obs.shape[0]
+    adv = rng.normal(size=B)
+    ret = rng.normal(size=B)
+    # logp_old = current logp + offsets chosen so rho sits well inside or well outside [0.75, 1.25]
+    k_pad, hid, nh, n, nop = dims
+    Ws, bs, ls = oracle.ppo_unflatten(theta, k_pad, hid, nh, nop)
+    h = obs
+    for l in range(nh):
+        h = np.tanh(h @ Ws[l].T + bs[l])
+    mu = (h @ Ws[-1].T + bs[-1])[:, :n]
+    z = (act_raw - mu) / np.exp(ls[:n])
+    logp = (-0.5 * z * z - ls[:n] - 0.5 * math.log(2 * math.pi)).sum(axis=1)
+    shift = rng.choice([-0.6, -0.05, 0.0, 0.05, 0.6], size=B)
+    lpo = logp + shift
+    args = (dims, obs, act_raw, lpo, adv, ret, 0.25, 0.02, 0.5, 1)
+    L, g, _ = oracle.ppo_loss_grad(theta, *args)
+    hstep = 1e-6
+    idx = rng.choice(theta.size, size=60, replace=False)
+    for i in idx:
+        tp, tm = theta.copy(), theta.copy()
+        tp[i] += hstep
+        tm[i] -= hstep
+        fd = (oracle.ppo_loss_grad(tp, *args)[0] - oracle.ppo_loss_grad(tm, *args)[0]) / (2 * hstep)
+        assert abs(fd - g[i]) <= 1e-6 * max(1.0, abs(g[i])) + 1e-8, (i, fd, g[i])
+
+
+def test_ppo_clip_pins():
+    """rho = 1 everywhere -> the clipped surrogate's gradient equals the unclipped one.
+    S:L291: rho = 2, A > 0, eps = 0.25 -> the contribution uses 1.25 A (and no policy gradient)."""
+    rng, dims, theta, obs, act_raw = _ppo_problem(2)
+    B = obs.shape[0]
+    k_pad, hid, nh, n, nop = dims
+    Ws, bs, ls = oracle.ppo_unflatten(theta, k_pad, hid, nh, nop)
+    h = obs
+    for l in range(nh):
+        h = np.tanh(h @ Ws[l].T + bs[l])
+    mu = (h @ Ws[-1].T + bs[-1])[:, :n]
+    z = (act_raw - mu) / np.exp(ls[:n])
+    logp = (-0.5 * z * z - ls[:n] - 0.5 * math.log(2 * math.pi)).sum(axis=1)
+    adv = rng.normal(size=B)
+    ret = rng.normal(size=B)
+    _, g_clip, _ = oracle.ppo_loss_grad(theta, dims, obs, act_raw, logp, adv, ret, 0.25, 0.0, 0.0, 1)
+    _, g_free, _ = oracle.ppo_loss_grad(theta, dims, obs, act_raw, logp, adv, ret, 1e9, 0.0, 0.0, 1)
+    np.testing.assert_allclose(g_clip, g_free, rtol=1e-12, atol=1e-15)
+    A = np.abs(adv) + 0.1
+    L, g, (sobj, _, _) = oracle.ppo_loss_grad(theta, dims, obs, act_raw, logp - math.log(2.0), A, ret, 0.25, 0.0, 0.0, 1)
+    assert sobj == pytest.approx(1.25 * A.sum(), rel=1e-12)
+    nW = hid * k_pad + hid * hid + nop * hid
+    np.testing.assert_array_equal(g[:nW][: hid * k_pad], 0.0)    # no policy gradient flows through the clip
+
+
+def test_adam_first_step_is_normalised_gradient():
+    """Bias-corrected Adam's first step: m_hat = g, v_hat = g^2, so the update is -lr g / (|g| + eps)."""
+    g = np.array([1e-3, -2.0, 0.0, 5e-9])
+    th, m, v = oracle.adam_step(np.zeros(4), np.zeros(4), np.zeros(4), g, 1, 0.01)
+    np.testing.assert_allclose(th, -0.01 * g / (np.abs(g) + 1e-8), rtol=1e-12, atol=0.0)
