@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t tmem = *tslot;
     unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 64 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = clock64();
+#ifdef POD_EXP_GTIME
+    if (threadIdx.x == 0 && a.t < 1024) atomicMin(&g_gtime[a.t][0], gtimer());
+#endif
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -450,6 +453,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         tmem_dealloc(tmem, tcols);
     }
     if (tr && threadIdx.x == 0) tr[26] = clock64();
+#ifdef POD_EXP_GTIME
+    if (threadIdx.x == 0 && a.t < 1024) atomicMax(&g_gtime[a.t][1], gtimer());
+#endif
 }
 
 }  // namespace pod

@@ -121,6 +121,9 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     const int tile = a.tile0 + static_cast<int>(blockIdx.x);
     unsigned long long* trc = (a.trace && a.mode == 0) ? a.trace + tile * 8 : nullptr;
     if (trc && threadIdx.x == 0) trc[0] = clock64();
+#ifdef POD_EXP_GTIME
+    if (threadIdx.x == 0 && a.mode == 0 && a.noise_t - 1 < 1024) atomicMin(&g_gtime[a.noise_t - 1][2], gtimer());
+#endif
     const int n = a.n;
     const int e_pad = env_e_pad(n);
     const EnvSmemLayout SL = env_smem_layout(n, a.k_pad);
@@ -444,6 +447,9 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     }
     __syncthreads();
     if (trc && threadIdx.x == 0) trc[6] = clock64();
+#ifdef POD_EXP_GTIME
+    if (threadIdx.x == 0 && a.mode == 0 && a.noise_t - 1 < 1024) atomicMax(&g_gtime[a.noise_t - 1][3], gtimer());
+#endif
 }
 
 // injected actions: a[i][e] = sgn(u) floor(|u| h_max + 1/2)  (R#6)

@@ -1097,3 +1097,14 @@ extern "C" pod_status pod_early_stop(const double* history, int32_t len, int32_t
 }
 
 #include "pod_ppo.cuh"
+
+#ifdef POD_EXP_GTIME
+extern "C" int pod_debug_gtime(unsigned long long* host, int reset) {
+    if (reset) {
+        static unsigned long long init[1024][4];
+        for (int i = 0; i < 1024; ++i) { init[i][0] = ~0ull; init[i][1] = 0; init[i][2] = ~0ull; init[i][3] = 0; }
+        return cudaMemcpyToSymbol(pod::g_gtime, init, sizeof(init)) == cudaSuccess ? 0 : 1;
+    }
+    return cudaMemcpyFromSymbol(host, pod::g_gtime, sizeof(unsigned long long) * 1024 * 4) == cudaSuccess ? 0 : 1;
+}
+#endif
