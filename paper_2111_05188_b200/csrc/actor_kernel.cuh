@@ -112,7 +112,29 @@ __device__ __forceinline__ float tanh_sfu(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 2.8853900817779268f));   // 2 log2(e)
     return 1.0f - __fdividef(2.0f, e + 1.0f);
 }
-__device__ __forceinline__ float act_fn(float x, int act) { return act == 0 ? fmaxf(x, 0.0f) : tanh_sfu(x); }
+// 32 accumulator columns + bias -> activation -> 16 packed bf16 pairs.  The activation is CTA-uniform:
+// one branch around two straight-line bodies (a per-element select issued both the ReLU and the SFU
+// tanh sequence, with a branch per element, for every element: 2.5x the epilogue's cost)
+__device__ __forceinline__ void epi_pack(const uint32_t (&v)[32], const float4* b4, int act, uint32_t (&pk)[16]) {
+    if (act == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float4 b = b4[q];
+            pk[2 * q] = pack_bf16x2(fmaxf(__uint_as_float(v[4 * q]) + b.x, 0.0f),
+                                    fmaxf(__uint_as_float(v[4 * q + 1]) + b.y, 0.0f));
+            pk[2 * q + 1] = pack_bf16x2(fmaxf(__uint_as_float(v[4 * q + 2]) + b.z, 0.0f),
+                                        fmaxf(__uint_as_float(v[4 * q + 3]) + b.w, 0.0f));
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float4 b = b4[q];
+            pk[2 * q] = pack_bf16x2(tanh_sfu(__uint_as_float(v[4 * q]) + b.x), tanh_sfu(__uint_as_float(v[4 * q + 1]) + b.y));
+            pk[2 * q + 1] =
+                pack_bf16x2(tanh_sfu(__uint_as_float(v[4 * q + 2]) + b.z), tanh_sfu(__uint_as_float(v[4 * q + 3]) + b.w));
+        }
+    }
+}
 
 __global__ void __launch_bounds__(ACT_THREADS, 1)
     actor_forward_kernel(const __grid_constant__ ActorMaps maps, const ActorArgs a) {
@@ -336,14 +358,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 tmem_ld_wait();
                 const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
                 uint32_t pk[16];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 b = b4[q];
-                    pk[2 * q] = pack_bf16x2(act_fn(__uint_as_float(v[4 * q]) + b.x, a.act),
-                                            act_fn(__uint_as_float(v[4 * q + 1]) + b.y, a.act));
-                    pk[2 * q + 1] = pack_bf16x2(act_fn(__uint_as_float(v[4 * q + 2]) + b.z, a.act),
-                                                act_fn(__uint_as_float(v[4 * q + 3]) + b.w, a.act));
-                }
+                epi_pack(v, b4, a.act, pk);
                 const int atom_g = static_cast<int>(rank) * na + j;           // global atom of h_{l+1}
                 const uint32_t atom = act_s + static_cast<uint32_t>(atom_g) * 16384u;
 #pragma unroll
@@ -393,24 +408,37 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             }
             if (valid && i0 < a.n && !a.value_only) {
                 float raw[8], mu[8];
+                int16_t ai8[8];
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                    const int i = i0 + jj;
                     mu[jj] = __uint_as_float(hv[jj]) + bias[tc + jj];
                     raw[jj] = mu[jj];
-                    if (i < a.n) {
-                        // noise z ~ N(0,1) for (env, step, ticker), generated by the previous env-step launch
-                        const float z = zr[cc * 8 + jj];
-                        const float ls = log_std[tc + jj];
-                        bad |= !isfinite(mu[jj]);
-                        raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
-                        logp += (-0.5f * z * z - ls) - half_ln_2pi;
-                        const float u = tanh_sfu(raw[jj]);
-                        const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
-                        const int ai = u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m);
-                        a.aint[static_cast<int64_t>(i) * a.N + e] = static_cast<int16_t>(ai);
-                        if (a.dbg_aint) a.dbg_aint[static_cast<int64_t>(e) * a.n + i] = static_cast<int16_t>(ai);
-                    }
+                }
+                // one ticker: noise z ~ N(0,1) for (env, step, ticker) generated by the previous env-step
+                // launch, raw = mu + sigma z, log-prob term, tanh on the SFU, integer map in float64
+                auto sample = [&](int jj) {
+                    const float z = zr[cc * 8 + jj];
+                    const float ls = log_std[tc + jj];
+                    bad |= !isfinite(mu[jj]);
+                    raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
+                    logp += (-0.5f * z * z - ls) - half_ln_2pi;
+                    const float u = tanh_sfu(raw[jj]);
+                    const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
+                    ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
+                    a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
+                };
+                // chunk-uniform branch: straight-line code for the full 8-ticker chunks
+                if (i0 + 8 <= a.n) {
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) sample(jj);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        if (i0 + jj < a.n) sample(jj);
+                }
+                if (a.dbg_aint) {
+                    for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
+                        a.dbg_aint[static_cast<int64_t>(e) * a.n + i0 + jj] = ai8[jj];
                 }
                 float* arow = a.act_out + static_cast<int64_t>(e) * a.n + i0;
                 float* mrow = a.mu_out ? a.mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;

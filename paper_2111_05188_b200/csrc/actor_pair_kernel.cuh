@@ -247,14 +247,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 tmem_ld_wait();
                 const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
                 uint32_t pk[16];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 b = b4[q];
-                    pk[2 * q] = pack_bf16x2(act_fn(__uint_as_float(v[4 * q]) + b.x, a.act),
-                                            act_fn(__uint_as_float(v[4 * q + 1]) + b.y, a.act));
-                    pk[2 * q + 1] = pack_bf16x2(act_fn(__uint_as_float(v[4 * q + 2]) + b.z, a.act),
-                                                act_fn(__uint_as_float(v[4 * q + 3]) + b.w, a.act));
-                }
+                epi_pack(v, b4, a.act, pk);
                 const int atom_g = static_cast<int>(chalf) * na + j;
                 const uint32_t atom = act_s + static_cast<uint32_t>(atom_g) * 16384u;
 #pragma unroll
