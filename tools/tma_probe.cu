@@ -12,7 +12,8 @@ using namespace pod;
 constexpr int STAGES = 5;
 constexpr int TILE = 16384;
 
-__global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUtensorMap map, const char* src, int mode,
+__global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUtensorMap map,
+                                                    const __grid_constant__ CUtensorMap map64, const char* src, int mode,
                                                     int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
@@ -32,7 +33,9 @@ __global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUte
             if (q >= iters) break;
             const int tile = (q + blockIdx.x * 7) % tiles;
             mbar_arrive_expect_tx(bars + 8 * s, TILE);
-            if (mode == 0) {
+            if (mode == 3) {
+                tma_load_2d(base + s * TILE, &map64, (tile % 16) * 32, (tile / 16) * 256, bars + 8 * s);
+            } else if (mode == 0) {
                 tma_load_2d(base + s * TILE, &map, (tile % 8) * 64, (tile / 8) * 128, bars + 8 * s);
             } else if (mode == 1) {
                 bulk_g2s(base + s * TILE, src + static_cast<size_t>(tile) * TILE, TILE, bars + 8 * s);
@@ -68,13 +71,17 @@ int main() {
     cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
     ((EncodeFn)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUtensorMap map64;
+    cuuint32_t box64[2] = {32, 256};
+    ((EncodeFn)fn)(&map64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, dims, str, box64, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int smem = STAGES * TILE + 1024 + 64;
     cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const char* names[] = {"tensor TMA 128x128B SW128", "bulk 16 KB contiguous", "bulk 2 x 8 KB"};
+    const char* names[] = {"tensor TMA 128x128B SW128", "bulk 16 KB contiguous", "bulk 2 x 8 KB", "tensor TMA 256x64B SW64"};
     for (int grid : {1, 128, 148}) {
-        for (int mode = 0; mode < 3; ++mode) {
+        for (int mode = 0; mode < 4; ++mode) {
             const int iters = 200;
-            for (int rep = 0; rep < 2; ++rep) stream_kernel<<<grid, 64, smem>>>(map, d, mode, iters, out);
+            for (int rep = 0; rep < 2; ++rep) stream_kernel<<<grid, 64, smem>>>(map, map64, d, mode, iters, out);
             cudaDeviceSynchronize();
             unsigned long long h[256];
             cudaMemcpy(h, out, 8 * grid, cudaMemcpyDeviceToHost);
