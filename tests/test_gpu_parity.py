@@ -595,3 +595,56 @@ def test_ppo_learner_improves_surrogate():
         objs.append(ls[0] / ls[3])
     assert objs[-1] > objs[0]
     assert torch.isfinite(learner.master).all()
+
+
+# ----------------------------------------------------------------- shape sweep (edge configurations)
+@pytest.mark.parametrize("n,f,N,nh,hid,act,agents,h_max,cost", [
+    (1, 3, 1, 1, 128, 0, 1, 100, 0.002),      # one stock, one env (a 1-lane ragged tile)
+    (102, 3, 64, 2, 256, 1, 1, 100, 0.002),   # the largest observation (obs_dim 511 of k_pad 512), tanh
+    (30, 0, 96, 4, 128, 0, 1, 100, 0.0),      # no indicator channels, four hidden layers, zero cost
+    (64, 3, 200, 1, 512, 1, 2, 7, 0.01),      # n % 32 == 0 (critic row in a fresh pad block), 2 agents, small h_max
+    (5, 1, 33, 3, 128, 0, 1, 100, 0.002),     # one indicator channel, ragged second tile
+])
+def test_shape_sweep(n, f, N, nh, hid, act, agents, h_max, cost):
+    """Sampled rollout with critic on edge configurations: actor means and critic values vs the float64
+    oracle on the GPU's observations, Gaussian noise and log-probs vs the oracle's Philox/Box-Muller, and
+    the executed actions replayed through the oracle environment (holdings, cash, rewards bit-exact)."""
+    c = Case(n=n, f=f, T_data=300, N=N, H=40, n_agents=agents, h_max=h_max, cost=cost, seed=60 + n)
+    aws, params, actor = _actor(c, nh, hid, n_agents=agents, act=act)
+    T = 5
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, debug=True, critic=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    c.env.check()
+    obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
+    mu_g = tr.mu.cpu().numpy().astype(np.float64)
+    raw_g = tr.act.cpu().numpy().astype(np.float64)
+    logp_g = tr.logp.cpu().numpy().astype(np.float64)
+    val_g = tr.val.cpu().numpy().astype(np.float64)
+    per = N // agents
+    for a in range(agents):
+        rows = slice(a * per, (a + 1) * per)
+        aw = aws[a]
+        w = oracle.actor_flat(aw.W, aw.b, aw.log_std)
+        ls = aw.log_std.astype(np.float64)
+        for t in range(T + 1):
+            v_o = oracle.actor_value(aw.W, aw.b, aw.w_v, aw.b_v, obs_g[t, rows], nh, hid, act)
+            rms = math.sqrt(float(np.mean(v_o ** 2)))
+            # with one env the rms is V itself, and V can cancel to near 0: also allow 1e-2 of the
+            # magnitude of its terms, sum |w_v| h + |b_v| (bf16 activations carry ~2^-8 of each term)
+            v_abs = np.abs(oracle.actor_value(aw.W, aw.b, np.abs(aw.w_v), abs(aw.b_v), obs_g[t, rows], nh, hid, act))
+            assert np.all(np.abs(val_g[t, rows] - v_o) <= 2e-2 * (np.abs(v_o) + rms) + 1e-2 * v_abs + 1e-6), (a, t)
+            if t == T:
+                break
+            mu_o = oracle.actor_mu(w, obs_g[t, rows], nh, hid, n, act)
+            mu_check(mu_g[t, rows], mu_o)
+            for e in range(a * per, (a + 1) * per):
+                z_o = oracle.normals(c.cfg.seed, c.cfg.env_offset + e, t, n)
+                z_g = (raw_g[t, e] - mu_g[t, e]) / np.exp(ls)
+                assert np.all(np.abs(z_g - z_o) <= 2e-5 * np.abs(z_o) + 5e-4), (t, e)
+                lp_o = float(np.sum(-0.5 * z_o * z_o - ls - 0.5 * math.log(2 * math.pi)))
+                terms = float(np.sum(0.5 * z_o * z_o + np.abs(ls) + 0.5 * math.log(2 * math.pi)))
+                assert abs(logp_g[t, e] - lp_o) <= 1e-5 * terms + 1e-4, (t, e)
+    o = c.oracle_env()
+    out = o.rollout(T, "replay", a_rep=tr.dbg_aint.cpu().numpy(), want=("obs", "rew", "done", "hold", "cash"))
+    assert_env_exact(tr, out, c.obs_dim)
