@@ -41,15 +41,31 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        cmd = nvcc_cmd()
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if verbose or r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError("nvcc failed building libpod.so")
-        with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
-            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    """Compile libpod.so if it is missing or older than its sources.  Several processes (one per GPU
+    under torchrun) may call this at once: an exclusive file lock serialises them, the first one
+    builds into a temporary file that is renamed into place, the others find it up to date."""
+    import fcntl
+
+    if not (force or needs_build()):
+        return LIB
+    with open(os.path.join(HERE, ".build.lock"), "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            if force or needs_build():
+                tmp = LIB + ".%d.tmp" % os.getpid()
+                cmd = nvcc_cmd(tmp)
+                r = subprocess.run(cmd, capture_output=True, text=True)
+                if verbose or r.returncode != 0:
+                    sys.stderr.write(r.stdout + r.stderr)
+                if r.returncode != 0:
+                    if os.path.exists(tmp):
+                        os.remove(tmp)
+                    raise RuntimeError("nvcc failed building libpod.so")
+                os.replace(tmp, LIB)
+                with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
+                    f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
     return LIB
 
 
