@@ -66,6 +66,7 @@ struct ActorArgs {
     int32_t t;               // step within the rollout
     int32_t obs_row0;        // row of obs[t][0] in the obs tensor map = t * N
     int32_t mtile0;          // first 128-env M-tile of this launch (env groups)
+    int32_t mtiles;          // M-tiles of this launch; cluster c processes mtile0 + c, + c + nclusters, ...
     int32_t mc;              // 1: 4-CTA clusters (2 M-tiles) share weight tiles by TMA multicast
     int32_t value_only;      // 1: only the critic V (head row n) is written (bootstrap pass over obs[T])
     uint64_t seed;
@@ -101,7 +102,7 @@ constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
     return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_STAGE_BYTES +
-           ACT_BIAS_FLOATS * 4 + 4 * 128 * 4 + 256;   // + barriers
+           ACT_BIAS_FLOATS * 4 + 2 * 4 * 128 * 4 + 256;   // + double-buffered log-prob partials + barriers
 }
 
 // tanh(x) = 1 - 2 / (e^{2x} + 1) on the SFU (ex2.approx, approximate reciprocal): absolute error
@@ -156,23 +157,37 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t stage_bytes = ACT_STAGE_BYTES;
     const uint32_t bias_off = ka * 16384u + ACT_STAGES * stage_bytes;
     float* bias_s = reinterpret_cast<float*>(base + bias_off);                 // [ACT_BIAS_FLOATS]
-    float* logp_s = bias_s + ACT_BIAS_FLOATS;                                  // [4][128] (CTA 0)
-    const uint32_t bar_s = base_u32 + bias_off + ACT_BIAS_FLOATS * 4 + 4 * 128 * 4;
+    float* logp_s0 = bias_s + ACT_BIAS_FLOATS;                                 // [2 tiles][4][128] (CTA 0)
+    const uint32_t bar_s = base_u32 + bias_off + ACT_BIAS_FLOATS * 4 + 2 * 4 * 128 * 4;
     const uint32_t full_b = bar_s;                                   // [STAGES]
     const uint32_t empty_b = bar_s + 8u * ACT_STAGES;                // [STAGES]
     const uint32_t obs_b = bar_s + 16u * ACT_STAGES;
     const uint32_t accum_b = obs_b + 8u;
     const uint32_t ownrdy_b = obs_b + 16u;     // [4] atom j of this CTA's half of h_{l+1} written (256 arrivals)
     const uint32_t peerrdy_b = obs_b + 48u;    // [4] atom j of the peer's half landed (expect_tx)
-    const uint32_t tslot_s = obs_b + 80u;
+    const uint32_t actfree_b = obs_b + 80u;    // this CTA's MMAs of a tile are done reading act_s (commit)
+    const uint32_t logp_b = obs_b + 88u;       // CTA 0: a tile's 4 x 128 log-prob partials written (512 arrivals)
+    const uint32_t logpfree_b = obs_b + 96u;   // [2] CTA 1: CTA 0 has read partial buffer p (1 remote arrival)
+    const uint32_t tslot_s = obs_b + 112u;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
-    const int mtile = a.mtile0 + static_cast<int>(blockIdx.x >> 1);
-    const int agent = mtile / a.tiles_per_agent;
-    const int tile_in_agent = mtile % a.tiles_per_agent;
-    const int env0 = agent * a.per_agent + tile_in_agent * 128;
-    int rows_valid = a.per_agent - tile_in_agent * 128;
-    rows_valid = rows_valid > 128 ? 128 : rows_valid;
+    // persistent over M-tiles: cluster c (one CTA pair per M-tile) takes tiles mtile0 + c + it * nclusters
+    const int cid = static_cast<int>(blockIdx.x >> 1);
+    const int ncl = static_cast<int>(gridDim.x >> 1);
+    struct Tile {
+        int agent, env0, rows_valid;
+    };
+    auto tile_of = [&](int it, Tile& tl) -> bool {
+        const int k = cid + it * ncl;
+        if (k >= a.mtiles) return false;
+        const int mtile = a.mtile0 + k;
+        tl.agent = mtile / a.tiles_per_agent;
+        const int tile_in_agent = mtile % a.tiles_per_agent;
+        tl.env0 = tl.agent * a.per_agent + tile_in_agent * 128;
+        const int rv = a.per_agent - tile_in_agent * 128;
+        tl.rows_valid = rv > 128 ? 128 : rv;
+        return true;
+    };
 
     const int hid_half = a.hidden / 2;
     const int head_half = a.n_out_pad / 2;
@@ -190,6 +205,10 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             }
             mbar_init(obs_b, 1);
             mbar_init(accum_b, 2);        // one multicast commit from each CTA of the pair
+            mbar_init(actfree_b, 1);
+            mbar_init(logp_b, 512);
+            mbar_init(logpfree_b, 1);
+            mbar_init(logpfree_b + 8u, 1);
             for (int j = 0; j < 4; ++j) {
                 mbar_init(ownrdy_b + 8u * j, 256);   // the 256 epilogue threads
                 mbar_init(peerrdy_b + 8u * j, 1);    // the MMA thread's expect_tx + the peer's bytes
@@ -214,36 +233,42 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
-            const int kb0 = a.k_pad / 64;
-            mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
-            for (int kb = 0; kb < kb0; ++kb)
-                tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, a.obs_row0 + env0, obs_b);
             int stage = 0, seq = 0;
             uint32_t phase = 0;
-            for (int l = 0; l < a.n_layers; ++l) {
-                const int K = l == 0 ? a.k_pad : a.hidden;
-                const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
-                const int bn = actor_bn(half);
-                const int KB = K / ACT_BK;                                          // 32-wide K blocks
-                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);   // own half of h_l first
-                for (int c = 0; c < half / bn; ++c) {
-                    for (int j = 0; j < KB; ++j) {
-                        const int kb = (j + kb0) % KB;
-                        mbar_wait(empty_b + 8u * stage, phase ^ 1u);
-                        mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * (ACT_BK * 2));
-                        if (!a.mc) {
-                            tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
-                                        static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage);
-                        } else if ((seq & 1) == static_cast<int>(cr >> 1)) {
-                            // alternate tiles: this CTA fetches it for itself and its partner
-                            tma_load_3d_mc(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
-                                           static_cast<int>(rank) * half + c * bn, agent, full_b + 8u * stage, share_mask);
-                        }
-                        if (tr && seq < 16) tr[48 + seq] = clock64();
-                        ++seq;
-                        if (++stage == ACT_STAGES) {
-                            stage = 0;
-                            phase ^= 1u;
+            Tile tl;
+            for (int it = 0; tile_of(it, tl); ++it) {
+                // the obs tile goes into act_s once this CTA's MMAs of the previous tile are done with it
+                if (it > 0) mbar_wait(actfree_b, static_cast<uint32_t>(it - 1) & 1u);
+                const int kb0 = a.k_pad / 64;
+                mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
+                for (int kb = 0; kb < kb0; ++kb)
+                    tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, a.obs_row0 + tl.env0, obs_b);
+                for (int l = 0; l < a.n_layers; ++l) {
+                    const int K = l == 0 ? a.k_pad : a.hidden;
+                    const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
+                    const int bn = actor_bn(half);
+                    const int KB = K / ACT_BK;                                          // 32-wide K blocks
+                    const int kbo = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);   // own half of h_l first
+                    for (int c = 0; c < half / bn; ++c) {
+                        for (int j = 0; j < KB; ++j) {
+                            const int kb = (j + kbo) % KB;
+                            mbar_wait(empty_b + 8u * stage, phase ^ 1u);
+                            mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * (ACT_BK * 2));
+                            if (!a.mc) {
+                                tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
+                                            static_cast<int>(rank) * half + c * bn, tl.agent, full_b + 8u * stage);
+                            } else if ((seq & 1) == static_cast<int>(cr >> 1)) {
+                                // alternate tiles: this CTA fetches it for itself and its partner
+                                tma_load_3d_mc(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
+                                               static_cast<int>(rank) * half + c * bn, tl.agent, full_b + 8u * stage,
+                                               share_mask);
+                            }
+                            if (tr && seq < 16) tr[48 + seq] = clock64();
+                            ++seq;
+                            if (++stage == ACT_STAGES) {
+                                stage = 0;
+                                phase ^= 1u;
+                            }
                         }
                     }
                 }
@@ -253,57 +278,63 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
         if (lane == 0) {
-            mbar_wait(obs_b, 0);
-            tc_fence_after();
-            if (tr) tr[1] = clock64();
             const uint64_t adesc0 = sw128_desc(act_s);
             const uint64_t bdesc0 = sw64_desc(ring_s);
             int stage = 0;
             uint32_t phase = 0;
             const int na = a.hidden / 128;           // activation atoms (64 cols) per CTA half
-            for (int l = 0; l < a.n_layers; ++l) {
-                if (tr) tr[2 + 4 * l] = clock64();
-                const int K = l == 0 ? a.k_pad : a.hidden;
-                const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
-                const int bn = actor_bn(half);
-                const uint32_t idesc = idesc_bf16_f32(128, static_cast<uint32_t>(bn));
-                const int KB = K / ACT_BK;                 // 32-wide K blocks (two per activation atom)
-                const int kb0 = l == 0 ? 0 : static_cast<int>(rank) * na * 2;   // own atoms of h_l first
-                const uint32_t par = static_cast<uint32_t>(l - 1) & 1u;
-                for (int c = 0; c < half / bn; ++c) {
-                    for (int j = 0; j < KB; ++j) {
-                        const int kb = j + kb0 < KB ? j + kb0 : j + kb0 - KB;
-                        if (l > 0 && c == 0 && (j & 1) == 0) {
-                            // h_l atom by atom: own atoms as the epilogue finishes them, then the
-                            // peer's atoms as its bulk copies land
-                            const int ja = j >> 1;
-                            if (ja < na) {
-                                mbar_wait(ownrdy_b + 8u * ja, par);
-                            } else {
-                                mbar_arrive_expect_tx(peerrdy_b + 8u * (ja - na), 16384u);
-                                mbar_wait(peerrdy_b + 8u * (ja - na), par);
+            Tile tl;
+            for (int it = 0; tile_of(it, tl); ++it) {
+                mbar_wait(obs_b, static_cast<uint32_t>(it) & 1u);
+                tc_fence_after();
+                if (tr && it == 0) tr[1] = clock64();
+                for (int l = 0; l < a.n_layers; ++l) {
+                    const int g = it * a.n_layers + l;                 // layer count over tiles: TMEM buffer g & 1
+                    if (tr && it == 0) tr[2 + 4 * l] = clock64();
+                    const int K = l == 0 ? a.k_pad : a.hidden;
+                    const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
+                    const int bn = actor_bn(half);
+                    const uint32_t idesc = idesc_bf16_f32(128, static_cast<uint32_t>(bn));
+                    const int KB = K / ACT_BK;                 // 32-wide K blocks (two per activation atom)
+                    const int kbo = l == 0 ? 0 : static_cast<int>(rank) * na * 2;   // own atoms of h_l first
+                    // phase of the atom barriers: one completion per hidden epilogue, over tiles
+                    const uint32_t par = static_cast<uint32_t>(it * (a.n_layers - 1) + l - 1) & 1u;
+                    for (int c = 0; c < half / bn; ++c) {
+                        for (int j = 0; j < KB; ++j) {
+                            const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
+                            if (l > 0 && c == 0 && (j & 1) == 0) {
+                                // h_l atom by atom: own atoms as the epilogue finishes them, then the
+                                // peer's atoms as its bulk copies land
+                                const int ja = j >> 1;
+                                if (ja < na) {
+                                    mbar_wait(ownrdy_b + 8u * ja, par);
+                                } else {
+                                    mbar_arrive_expect_tx(peerrdy_b + 8u * (ja - na), 16384u);
+                                    mbar_wait(peerrdy_b + 8u * (ja - na), par);
+                                }
+                                tc_fence_after();
                             }
+                            mbar_wait(full_b + 8u * stage, phase);
                             tc_fence_after();
-                        }
-                        mbar_wait(full_b + 8u * stage, phase);
-                        tc_fence_after();
-                        if (tr && l == 0 && c * KB + j < 16) tr[32 + c * KB + j] = clock64();
-                        // descriptors: precomputed bases + the start-address field (16-B units)
-                        const uint64_t ad = adesc0 + (((kb >> 1) * 16384u + (kb & 1) * 64u) >> 4);
-                        const uint64_t bd = bdesc0 + ((stage * stage_bytes) >> 4);
-                        const uint32_t dt = tmem + (static_cast<uint32_t>(l) & 1u) * tbuf + static_cast<uint32_t>(c * bn);
-                        mma_bf16(dt, ad, bd, idesc, j != 0);
-                        mma_bf16(dt, ad + 2, bd + 2, idesc, 1u);
-                        if (a.mc) mma_commit_mc(empty_b + 8u * stage, share_mask);   // free it in both CTAs
-                        else mma_commit(empty_b + 8u * stage);
-                        if (++stage == ACT_STAGES) {
-                            stage = 0;
-                            phase ^= 1u;
+                            if (tr && it == 0 && l == 0 && c * KB + j < 16) tr[32 + c * KB + j] = clock64();
+                            // descriptors: precomputed bases + the start-address field (16-B units)
+                            const uint64_t ad = adesc0 + (((kb >> 1) * 16384u + (kb & 1) * 64u) >> 4);
+                            const uint64_t bd = bdesc0 + ((stage * stage_bytes) >> 4);
+                            const uint32_t dt = tmem + (static_cast<uint32_t>(g) & 1u) * tbuf + static_cast<uint32_t>(c * bn);
+                            mma_bf16(dt, ad, bd, idesc, j != 0);
+                            mma_bf16(dt, ad + 2, bd + 2, idesc, 1u);
+                            if (a.mc) mma_commit_mc(empty_b + 8u * stage, share_mask);   // free it in both CTAs
+                            else mma_commit(empty_b + 8u * stage);
+                            if (++stage == ACT_STAGES) {
+                                stage = 0;
+                                phase ^= 1u;
+                            }
                         }
                     }
+                    if (tr && it == 0) tr[3 + 4 * l] = clock64();
+                    mma_commit_mc(accum_b, pair_mask);
                 }
-                if (tr) tr[3 + 4 * l] = clock64();
-                mma_commit_mc(accum_b, pair_mask);
+                mma_commit(actfree_b);   // the next tile's obs may overwrite act_s once these MMAs are done
             }
         }
         __syncwarp();
@@ -315,167 +346,182 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         const int hh = ew >> 2;                    // which half of this CTA's columns
         const int r = quad * 32 + lane;            // row of the tile == TMEM lane
         const uint32_t trow = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        const int e = env0 + r;
-        const bool valid = r < rows_valid && e < a.N;
-        const char* slab = a.params + agent * a.param_bytes;
-        // stage this CTA's halves of the biases and log-std in smem
-        {
-            int off = 0;
-            for (int l = 0; l < a.n_layers; ++l) {
-                const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
-                const float* b = reinterpret_cast<const float*>(slab + a.b_off[l]) + rank * half;
-                for (int j = etid; j < half; j += 256) bias_s[off + j] = b[j];
-                off += half;
-            }
-            const float* ls = reinterpret_cast<const float*>(slab + a.log_std_off) + rank * head_half;
-            for (int j = etid; j < head_half; j += 256) {
-                bias_s[off + j] = ls[j];
-                bias_s[off + head_half + j] = expf(ls[j]);   // sigma
-            }
-        }
-        // prefetch this thread's head noise z (written by the previous env-step launch):
-        // one round of independent loads, long before the head needs them
-        const int hq = head_half / 2;                                    // tickers of this thread
-        float zr[ACT_MAX_HQ];
-#pragma unroll
-        for (int q = 0; q < ACT_MAX_HQ; ++q) {
-            const int i = static_cast<int>(rank) * head_half + hh * hq + q;
-            zr[q] = (q < hq && valid && i < a.n && !a.deterministic) ? a.znoise[static_cast<int64_t>(i) * a.N + e] : 0.0f;
-        }
-        named_bar_sync(1, 256);
-        int boff = 0;
-        for (int l = 0; l < a.n_layers - 1; ++l) {
-            mbar_wait(accum_b, static_cast<uint32_t>(l) & 1u);   // both CTAs done reading h_l
-            tc_fence_after();
-            if (tr && etid == 0) tr[4 + 4 * l] = clock64();
-            // h_{l+1} atom by atom (64 columns = 8 warps x 32 columns x 128 rows), so the next
-            // layer's MMAs and the DSMEM copy of each atom start as soon as it is written
-            const int na = hid_half / 64;
-            for (int j = 0; j < na; ++j) {
-                const int tc = j * 64 + hh * 32;                      // TMEM column (local)
-                uint32_t v[32];
-                tmem_ld32(trow + (static_cast<uint32_t>(l) & 1u) * tbuf + static_cast<uint32_t>(tc), v);
-                tmem_ld_wait();
-                const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
-                uint32_t pk[16];
-                epi_pack(v, b4, a.act, pk);
-                const int atom_g = static_cast<int>(rank) * na + j;           // global atom of h_{l+1}
-                const uint32_t atom = act_s + static_cast<uint32_t>(atom_g) * 16384u;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    st_shared_v4(atom + sw128_offset(static_cast<uint32_t>(r), static_cast<uint32_t>(hh * 4 + q)),
-                                 pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                fence_proxy_async_smem();
-                tc_fence_before();
-                mbar_arrive(ownrdy_b + 8u * j);
-                if (etid == 0) {
-                    // the whole atom is written: ship it to the same offset in the peer
-                    mbar_wait(ownrdy_b + 8u * j, static_cast<uint32_t>(l) & 1u);
-                    bulk_s2peer(mapa_shared(atom, peer), atom, 16384u, mapa_shared(peerrdy_b + 8u * j, peer));
+        const int hq = head_half / 2;              // head tickers of this thread
+        int staged_agent = -1;
+        Tile tl;
+        for (int it = 0; tile_of(it, tl); ++it) {
+            const int e = tl.env0 + r;
+            const bool valid = r < tl.rows_valid && e < a.N;
+            if (tl.agent != staged_agent) {
+                // stage this CTA's halves of the agent's biases and log-std in smem
+                if (staged_agent >= 0) named_bar_sync(1, 256);   // every thread is done with the previous agent's
+                const char* slab = a.params + tl.agent * a.param_bytes;
+                int off = 0;
+                for (int l = 0; l < a.n_layers; ++l) {
+                    const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
+                    const float* b = reinterpret_cast<const float*>(slab + a.b_off[l]) + rank * half;
+                    for (int j = etid; j < half; j += 256) bias_s[off + j] = b[j];
+                    off += half;
                 }
+                const float* ls = reinterpret_cast<const float*>(slab + a.log_std_off) + rank * head_half;
+                for (int j = etid; j < head_half; j += 256) {
+                    bias_s[off + j] = ls[j];
+                    bias_s[off + head_half + j] = expf(ls[j]);   // sigma
+                }
+                staged_agent = tl.agent;
             }
-            boff += hid_half;
-            if (tr && etid == 0) tr[5 + 4 * l] = clock64();
-        }
-        // ----- head: this CTA's tickers [rank*head_half, ...), this warp's quarter of them
-        const int L = a.n_layers - 1;
-        mbar_wait(accum_b, static_cast<uint32_t>(L) & 1u);
-        tc_fence_after();
-        if (tr && etid == 0) tr[24] = clock64();
-        const float* bias = bias_s + boff;
-        const float* log_std = bias_s + boff + head_half;
-        const float* sigma = bias_s + boff + 2 * head_half;
-        float logp = 0.0f;
-        bool bad = false;
-        const float half_ln_2pi = 0.918938533204672742f;
-        const bool vec = (a.n % 4) == 0;
+            // prefetch this thread's head noise z (written by the previous env-step launch):
+            // one round of independent loads, long before the head needs them
+            float zr[ACT_MAX_HQ];
 #pragma unroll
-        for (int cc = 0; cc < ACT_MAX_HQ / 8; ++cc) {
-            if (cc >= hq / 8) break;
-            const int tc = hh * hq + cc * 8;                         // TMEM column (local)
-            const int i0 = static_cast<int>(rank) * head_half + tc;  // global ticker
-            uint32_t hv[8];
-            __syncwarp();
-            tmem_ld8(trow + (static_cast<uint32_t>(L) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
-            tmem_ld_wait();
-            if (valid && i0 <= a.n && a.val_out && a.n < i0 + 8) {
-                // critic: head row n over the same trunk (R#22)
-                float vh = 0.0f;
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                    if (i0 + jj == a.n) vh = __uint_as_float(hv[jj]);
-                a.val_out[e] = vh + bias[tc + (a.n - i0)];
+            for (int q = 0; q < ACT_MAX_HQ; ++q) {
+                const int i = static_cast<int>(rank) * head_half + hh * hq + q;
+                zr[q] = (q < hq && valid && i < a.n && !a.deterministic) ? a.znoise[static_cast<int64_t>(i) * a.N + e]
+                                                                          : 0.0f;
             }
-            if (valid && i0 < a.n && !a.value_only) {
-                float raw[8], mu[8];
-                int16_t ai8[8];
+            named_bar_sync(1, 256);
+            int boff = 0;
+            for (int l = 0; l < a.n_layers - 1; ++l) {
+                const int g = it * a.n_layers + l;
+                const uint32_t hpar = static_cast<uint32_t>(it * (a.n_layers - 1) + l) & 1u;
+                mbar_wait(accum_b, static_cast<uint32_t>(g) & 1u);   // both CTAs done reading h_l
+                tc_fence_after();
+                if (tr && it == 0 && etid == 0) tr[4 + 4 * l] = clock64();
+                // h_{l+1} atom by atom (64 columns = 8 warps x 32 columns x 128 rows), so the next
+                // layer's MMAs and the DSMEM copy of each atom start as soon as it is written
+                const int na = hid_half / 64;
+                for (int j = 0; j < na; ++j) {
+                    const int tc = j * 64 + hh * 32;                      // TMEM column (local)
+                    uint32_t v[32];
+                    tmem_ld32(trow + (static_cast<uint32_t>(g) & 1u) * tbuf + static_cast<uint32_t>(tc), v);
+                    tmem_ld_wait();
+                    const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
+                    uint32_t pk[16];
+                    epi_pack(v, b4, a.act, pk);
+                    const int atom_g = static_cast<int>(rank) * na + j;           // global atom of h_{l+1}
+                    const uint32_t atom = act_s + static_cast<uint32_t>(atom_g) * 16384u;
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    mu[jj] = __uint_as_float(hv[jj]) + bias[tc + jj];
-                    raw[jj] = mu[jj];
-                }
-                // one ticker: noise z ~ N(0,1) for (env, step, ticker) generated by the previous env-step
-                // launch, raw = mu + sigma z, log-prob term, tanh on the SFU, integer map in float64
-                auto sample = [&](int jj) {
-                    const float z = zr[cc * 8 + jj];
-                    const float ls = log_std[tc + jj];
-                    bad |= !isfinite(mu[jj]);
-                    raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
-                    logp += (-0.5f * z * z - ls) - half_ln_2pi;
-                    const float u = tanh_sfu(raw[jj]);
-                    const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
-                    ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
-                    a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
-                };
-                // chunk-uniform branch: straight-line code for the full 8-ticker chunks
-                if (i0 + 8 <= a.n) {
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) sample(jj);
-                } else {
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj)
-                        if (i0 + jj < a.n) sample(jj);
-                }
-                if (a.dbg_aint) {
-                    for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
-                        a.dbg_aint[static_cast<int64_t>(e) * a.n + i0 + jj] = ai8[jj];
-                }
-                float* arow = a.act_out + static_cast<int64_t>(e) * a.n + i0;
-                float* mrow = a.mu_out ? a.mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;
-                if (vec && i0 + 8 <= a.n) {
-                    reinterpret_cast<float4*>(arow)[0] = make_float4(raw[0], raw[1], raw[2], raw[3]);
-                    reinterpret_cast<float4*>(arow)[1] = make_float4(raw[4], raw[5], raw[6], raw[7]);
-                    if (mrow) {
-                        reinterpret_cast<float4*>(mrow)[0] = make_float4(mu[0], mu[1], mu[2], mu[3]);
-                        reinterpret_cast<float4*>(mrow)[1] = make_float4(mu[4], mu[5], mu[6], mu[7]);
+                    for (int q = 0; q < 4; ++q)
+                        st_shared_v4(atom + sw128_offset(static_cast<uint32_t>(r), static_cast<uint32_t>(hh * 4 + q)),
+                                     pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    fence_proxy_async_smem();
+                    tc_fence_before();
+                    mbar_arrive(ownrdy_b + 8u * j);
+                    if (etid == 0) {
+                        // the whole atom is written: ship it to the same offset in the peer
+                        mbar_wait(ownrdy_b + 8u * j, hpar);
+                        bulk_s2peer(mapa_shared(atom, peer), atom, 16384u, mapa_shared(peerrdy_b + 8u * j, peer));
                     }
-                } else {
-#pragma unroll
+                }
+                boff += hid_half;
+                if (tr && it == 0 && etid == 0) tr[5 + 4 * l] = clock64();
+            }
+            // ----- head: this CTA's tickers [rank*head_half, ...), this warp's quarter of them
+            const int L = a.n_layers - 1;
+            const int gL = it * a.n_layers + L;
+            mbar_wait(accum_b, static_cast<uint32_t>(gL) & 1u);
+            tc_fence_after();
+            if (tr && it == 0 && etid == 0) tr[24] = clock64();
+            const float* bias = bias_s + boff;
+            const float* log_std = bias_s + boff + head_half;
+            const float* sigma = bias_s + boff + 2 * head_half;
+            float logp = 0.0f;
+            bool bad = false;
+            const float half_ln_2pi = 0.918938533204672742f;
+            const bool vec = (a.n % 4) == 0;
+            const int i00 = static_cast<int>(rank) * head_half;
+    #pragma unroll
+            for (int cc = 0; cc < ACT_MAX_HQ / 8; ++cc) {
+                if (cc >= hq / 8) break;
+                const int tc = hh * hq + cc * 8;                         // TMEM column (local)
+                const int i0 = i00 + tc;                                 // global ticker
+                uint32_t hv[8];
+                __syncwarp();
+                tmem_ld8(trow + (static_cast<uint32_t>(gL) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
+                tmem_ld_wait();
+                if (valid && i0 <= a.n && a.val_out && a.n < i0 + 8) {
+                    // critic: head row n over the same trunk (R#22)
+                    float vh = 0.0f;
+    #pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        if (i0 + jj == a.n) vh = __uint_as_float(hv[jj]);
+                    a.val_out[e] = vh + bias[tc + (a.n - i0)];
+                }
+                if (valid && i0 < a.n && !a.value_only) {
+                    float raw[8], mu[8];
+                    int16_t ai8[8];
+    #pragma unroll
                     for (int jj = 0; jj < 8; ++jj) {
-                        if (i0 + jj < a.n) {
-                            arow[jj] = raw[jj];
-                            if (mrow) mrow[jj] = mu[jj];
+                        mu[jj] = __uint_as_float(hv[jj]) + bias[tc + jj];
+                        raw[jj] = mu[jj];
+                    }
+                    // one ticker: noise z ~ N(0,1) for (env, step, ticker) generated by the previous env-step
+                    // launch, raw = mu + sigma z, log-prob term, tanh on the SFU, integer map in float64
+                    auto sample = [&](int jj) {
+                        const float z = zr[cc * 8 + jj];
+                        const float ls = log_std[tc + jj];
+                        bad |= !isfinite(mu[jj]);
+                        raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
+                        logp += (-0.5f * z * z - ls) - half_ln_2pi;
+                        const float u = tanh_sfu(raw[jj]);
+                        const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
+                        ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
+                        a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
+                    };
+                    // chunk-uniform branch: straight-line code for the full 8-ticker chunks
+                    if (i0 + 8 <= a.n) {
+    #pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) sample(jj);
+                    } else {
+    #pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (i0 + jj < a.n) sample(jj);
+                    }
+                    if (a.dbg_aint) {
+                        for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
+                            a.dbg_aint[static_cast<int64_t>(e) * a.n + i0 + jj] = ai8[jj];
+                    }
+                    float* arow = a.act_out + static_cast<int64_t>(e) * a.n + i0;
+                    float* mrow = a.mu_out ? a.mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;
+                    if (vec && i0 + 8 <= a.n) {
+                        reinterpret_cast<float4*>(arow)[0] = make_float4(raw[0], raw[1], raw[2], raw[3]);
+                        reinterpret_cast<float4*>(arow)[1] = make_float4(raw[4], raw[5], raw[6], raw[7]);
+                        if (mrow) {
+                            reinterpret_cast<float4*>(mrow)[0] = make_float4(mu[0], mu[1], mu[2], mu[3]);
+                            reinterpret_cast<float4*>(mrow)[1] = make_float4(mu[4], mu[5], mu[6], mu[7]);
+                        }
+                    } else {
+    #pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            if (i0 + jj < a.n) {
+                                arow[jj] = raw[jj];
+                                if (mrow) mrow[jj] = mu[jj];
+                            }
                         }
                     }
                 }
             }
+            if (bad && valid) atomicOr(a.err, 1u);
+            if (tr && it == 0 && etid == 0) tr[25] = clock64();
+            // log-prob partial of (rank, hh) for row r -> CTA 0's buffer (it & 1) [rank*2 + hh][r]; CTA 1 first
+            // makes sure CTA 0 has consumed the tile that last used this buffer (two tiles ago)
+            const uint32_t pb = static_cast<uint32_t>(it) & 1u;
+            float* logp_s = logp_s0 + pb * 512;
+            if (rank == 1 && it >= 2) mbar_wait_cluster(logpfree_b + 8u * pb, static_cast<uint32_t>((it - 2) >> 1) & 1u);
+            st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), cr & ~1u), logp);
+            mbar_arrive_remote(mapa_shared(logp_b, cr & ~1u));   // release: the partial is visible with the arrival
+            if (rank == 0) {
+                mbar_wait_cluster(logp_b, static_cast<uint32_t>(it) & 1u);
+                if (hh == 0 && valid && a.logp_out)
+                    a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
+                named_bar_sync(2, 256);
+                if (etid == 0) mbar_arrive_remote(mapa_shared(logpfree_b + 8u * pb, peer));
+            }
         }
-        if (bad && valid) atomicOr(a.err, 1u);
-        if (tr && etid == 0) tr[25] = clock64();
-        // log-prob partial of (rank, hh) for row r -> CTA 0's logp_s[rank*2 + hh][r]
-        st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), cr & ~1u), logp);
     }
 
     tc_fence_before();
-    cluster_sync_all();      // logp partials visible in CTA 0; all peer DSMEM traffic finished
-    if (warp >= 2 && rank == 0) {
-        const int ew = warp - 2;
-        const int quad = warp & 3;
-        const int r = quad * 32 + lane;
-        const int e = env0 + r;
-        if ((ew >> 2) == 0 && r < rows_valid && e < a.N && a.logp_out)
-            a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
-    }
+    cluster_sync_all();      // every cross-CTA arrival and DSMEM copy of the launch is complete
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, tcols);

@@ -250,6 +250,8 @@ struct pod_env {
     std::vector<GraphEntry> graphs;
     uint64_t use_clock;
     bool use_graphs;
+    int persist;                // persistent actor clusters (POD_PERSIST=0 turns it off)
+    int sm_count;
     int profile;                // 0 = off, k = bracket every k-th step
     unsigned long long* trace;  // diagnostics: actor clock64 stamps of the last launch
     unsigned long long* env_trace;
@@ -370,6 +372,14 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     e->env_trace = nullptr;
     const char* ng = getenv("POD_NO_GRAPH");
     e->use_graphs = !(ng && ng[0] == '1');
+    {
+        const char* ps = getenv("POD_PERSIST");
+        e->persist = !(ps && ps[0] == '0');
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (e->sm_count < 2) e->sm_count = 2;
+    }
     cudaError_t ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_starts), sizeof(int32_t) * e->n_tiles);
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
     for (int g = 0; g < POD_MAX_GROUPS && ce == cudaSuccess; ++g) {
@@ -556,7 +566,11 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
         // every agent has an even number of full M-tiles and so does this launch
         aa.mc = (!p.pair && e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
-        lc.gridDim = dim3(static_cast<unsigned>(2 * mtiles));
+        aa.mtiles = mtiles;
+        // persistent clusters (one per SM pair) loop over the M-tiles: the next tile's obs and first
+        // weight stages load while the current tile's head runs (multi-wave batches)
+        const int ncl = (!aa.mc && !p.pair && e->persist) ? std::min(mtiles, e->sm_count / 2) : mtiles;
+        lc.gridDim = dim3(static_cast<unsigned>(2 * ncl));
         lc.blockDim = dim3(ACT_THREADS);
         lc.dynamicSmemBytes = p.actor_smem;
         lc.stream = s;

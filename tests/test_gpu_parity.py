@@ -648,3 +648,31 @@ def test_shape_sweep(n, f, N, nh, hid, act, agents, h_max, cost):
     o = c.oracle_env()
     out = o.rollout(T, "replay", a_rep=tr.dbg_aint.cpu().numpy(), want=("obs", "rew", "done", "hold", "cash"))
     assert_env_exact(tr, out, c.obs_dim)
+
+
+@pytest.mark.parametrize("agents", [1, 3])
+def test_persistent_actor_bit_identical(agents, monkeypatch):
+    """Multi-wave batch (more M-tiles than SM pairs: each persistent cluster runs several tiles, and with
+    several agents switches agents between tiles): every output equals the one-tile-per-cluster launch."""
+    N = 128 * 90 * agents   # 90 M-tiles per agent > 74 clusters
+    outs = []
+    for ps in ("0", "1"):
+        monkeypatch.setenv("POD_PERSIST", ps)
+        c = Case(n=30, f=3, T_data=400, N=N, H=40, n_agents=agents, seed=70)
+        aws, params, actor = _actor(c, 2, 128, n_agents=agents)
+        tr = api.Trajectory.allocate(3, c.N, c.n, c.k_pad, debug=True, critic=True)
+        c.env.reset(c.starts)
+        c.env.rollout(3, tr, actor=actor)
+        c.env.check()
+        outs.append(tr)
+    for name in ("obs", "act", "logp", "mu", "val", "rew", "done", "dbg_hold", "dbg_cash"):
+        assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
+    # and the persistent result itself against the oracle on sampled rows
+    obs_g = bf16_to_f64(outs[1].obs)[..., : c.obs_dim]
+    mu_g = outs[1].mu.cpu().numpy().astype(np.float64)
+    per = N // agents
+    for a in range(agents):
+        rows = np.arange(a * per, (a + 1) * per, 997)
+        w = oracle.actor_flat(aws[a].W, aws[a].b, aws[a].log_std)
+        for t in range(3):
+            mu_check(mu_g[t, rows], oracle.actor_mu(w, obs_g[t, rows], 2, 128, 30))
