@@ -206,8 +206,8 @@ def run_reference(args, w, rank, world):
     tot = sum(times)
     value = n_envs * Ts * args.steps / tot
     sample = (f"{n_envs} envs x {Ts} steps of workload {w.name} per step (market truncated to {T_data} rows; "
-              f"actor {w.n_hidden}x{w.hidden} float64, "
-              f"env step, GAE, fitness, select), {cores} OpenMP threads")
+              f"actor {w.n_hidden}x{w.hidden} + critic float64, "
+              f"env step, GAE on the critic values + normalisation, fitness, select), {cores} OpenMP threads")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -433,9 +433,11 @@ def main():
             n_s = max(cores, n_s // cores * cores)
             tt = oracle_step_sample(w, market, wf, n_s, Ts, cores, env_starts, wcr)
             cpu = {"value": n_s * Ts / tt, "unit": UNIT, "cores": cores, "kind": "oracle",
-                   "sample": f"{n_s} envs x {Ts} steps of {w.name} (float64 actor {w.n_hidden}x{w.hidden} + env "
-                             f"step + GAE + fitness + select), OpenMP over envs, {tt:.1f} s"}
-        launches_per_step = 1 + 2 * T + 1 + 1 + 1 + 1   # obs0, T x (actor, env), V(s_T) pass, step bump, gae, fitness
+                   "sample": f"{n_s} envs x {Ts} steps of {w.name} (float64 actor {w.n_hidden}x{w.hidden} + critic + "
+                             f"env step + GAE on the critic values + normalisation + fitness + select), OpenMP over "
+                             f"envs, {tt:.1f} s"}
+        # obs0, T x (actor, env), V(s_T) pass, step bump, GAE scan + normalisation, fitness
+        launches_per_step = 1 + 2 * T + 1 + 1 + 2 + 1
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
