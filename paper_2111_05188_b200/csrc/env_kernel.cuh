@@ -344,9 +344,16 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                     const float4 z = normals4(a.seed, static_cast<uint32_t>(a.env_offset + ee), step, static_cast<uint32_t>(qd));
                     const float zz[4] = {z.x, z.y, z.z, z.w};
                     float* zp = a.znoise + static_cast<int64_t>(4 * qd) * N + ee;
+                    if (4 * qd + 4 <= n) {   // full quad: four unconditional row stores
+                        zp[0] = zz[0];
+                        zp[N] = zz[1];
+                        zp[2 * N] = zz[2];
+                        zp[3 * N] = zz[3];
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (4 * qd + j < n) zp[static_cast<int64_t>(j) * N] = zz[j];
+                        for (int j = 0; j < 4; ++j)
+                            if (4 * qd + j < n) zp[static_cast<int64_t>(j) * N] = zz[j];
+                    }
                 }
             }
         }
@@ -364,14 +371,19 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                     for (int i = i0; i < i1; ++i)
                         ph = __dadd_rn(ph, __dmul_rn(p_164[i], static_cast<double>(hold_s[i * 32 + lane])));
                 } else {
-                    for (int i = i0 + (warp - 2); i < i1; i += 2) {
+                    // holdings out (one coalesced row per ticker; the row pointer steps by 2 N) and the
+                    // per-env holdings entries of s_{t+1}
+                    const int ib = i0 + (warp - 2);
+                    int32_t* hrow = a.hold + static_cast<int64_t>(ib) * N + e;
+                    const int64_t N2 = 2 * N;
+                    const int hkeep = done ? 0 : 1;
+                    for (int i = ib; i < i1; i += 2, hrow += N2) {
                         const int h = hold_s[i * 32 + lane];
-                        if (active) {
-                            a.hold[i * N + e] = done ? 0 : h;
-                            if (a.dbg_hold) a.dbg_hold[static_cast<int64_t>(e) * n + i] = h;
-                        }
-                        my[1 + i] = done ? 0 : f2bf(static_cast<float>(h) * p_1[i] * inv_c0);
+                        if (active) *hrow = h * hkeep;
+                        my[1 + i] = f2bf(static_cast<float>(h * hkeep) * p_1[i] * inv_c0);
                     }
+                    if (a.dbg_hold && active)
+                        for (int i = ib; i < i1; i += 2) a.dbg_hold[static_cast<int64_t>(e) * n + i] = hold_s[i * 32 + lane];
                 }
             }
             if (warp == 1) ph_s[lane] = ph;
