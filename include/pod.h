@@ -311,8 +311,9 @@ pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, i
  *   rho = exp(logp_theta(raw | s) - logp_old),
  *   L = -mean[min(rho A, clip(rho, 1-eps, 1+eps) A)] - c_ent H(pi)
  *       + c_v mean[(V(s) - R)^2],   H(pi) = sum_i (log sigma_i + (1 + ln 2 pi)/2),
- * the gradient of L (float32 forward + backward through the bf16-rollout MLP's
- * float32 master copy; GEMMs on cuBLAS) and one Adam step (bias-corrected,
+ * the gradient of L (forward + backward with bf16 x bf16 -> float32 tensor-core
+ * GEMMs on cuBLAS: the weights are the bf16 rollout slab, kept equal to the
+ * rounded float32 master after every step) and one Adam step (bias-corrected,
  * step t = adam_t + j + 1):  m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
  *   theta <- theta - lr (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps).
  * Afterwards the agent's rollout slab `params` (pod_actor_layout; agent 0 of

@@ -9,19 +9,22 @@
 namespace pod {
 
 struct PpoWs {
-    size_t x0, h, zh, d0, d1, act, lpo, adv, ret, grad, total;
+    size_t x0, h, zf, zh, d0, d1, b0, b1, act, lpo, adv, ret, grad, total;
 };
 
 inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, int B, int n) {
     auto up = [](size_t x) { return (x + 255) / 256 * 256; };
     PpoWs w{};
     size_t o = 0;
-    w.x0 = o;  o += up(sizeof(float) * B * L.k_pad);
-    w.h = o;   o += up(sizeof(float) * static_cast<size_t>(B) * hidden * n_hidden);
-    w.zh = o;  o += up(sizeof(float) * static_cast<size_t>(B) * L.n_out_pad);
     const size_t dmax = static_cast<size_t>(B) * (hidden > L.n_out_pad ? hidden : L.n_out_pad);
-    w.d0 = o;  o += up(sizeof(float) * dmax);
+    w.x0 = o;  o += up(2 * static_cast<size_t>(B) * L.k_pad);                       // bf16 minibatch obs
+    w.h = o;   o += up(2 * static_cast<size_t>(B) * hidden * n_hidden);             // bf16 activations
+    w.zf = o;  o += up(sizeof(float) * static_cast<size_t>(B) * hidden);            // f32 GEMM output
+    w.zh = o;  o += up(sizeof(float) * static_cast<size_t>(B) * L.n_out_pad);       // f32 head output
+    w.d0 = o;  o += up(sizeof(float) * dmax);                                       // f32 deltas
     w.d1 = o;  o += up(sizeof(float) * dmax);
+    w.b0 = o;  o += up(2 * dmax);                                                   // their bf16 copies
+    w.b1 = o;  o += up(2 * dmax);
     w.act = o; o += up(sizeof(float) * static_cast<size_t>(B) * n);
     w.lpo = o; o += up(sizeof(float) * B);
     w.adv = o; o += up(sizeof(float) * B);
@@ -38,7 +41,6 @@ inline cublasHandle_t ppo_cublas() {
     cudaGetDevice(&d);
     if (!h || d != dev) {
         if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-        cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);   // float32 GEMMs, no TF32
         dev = d;
     }
     return h;
@@ -97,16 +99,22 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate failed");
     POD_CUBLAS(cublasSetStream(cb, s));
     char* w = static_cast<char*>(ws);
-    float* x0 = reinterpret_cast<float*>(w + W.x0);
-    float* hbuf = reinterpret_cast<float*>(w + W.h);
+    __nv_bfloat16* x0 = reinterpret_cast<__nv_bfloat16*>(w + W.x0);
+    __nv_bfloat16* hbuf = reinterpret_cast<__nv_bfloat16*>(w + W.h);
+    float* zf = reinterpret_cast<float*>(w + W.zf);
     float* zh = reinterpret_cast<float*>(w + W.zh);
     float* d0 = reinterpret_cast<float*>(w + W.d0);
     float* d1 = reinterpret_cast<float*>(w + W.d1);
+    __nv_bfloat16* b0 = reinterpret_cast<__nv_bfloat16*>(w + W.b0);
+    __nv_bfloat16* b1 = reinterpret_cast<__nv_bfloat16*>(w + W.b1);
     float* act_b = reinterpret_cast<float*>(w + W.act);
     float* lpo_b = reinterpret_cast<float*>(w + W.lpo);
     float* adv_b = reinterpret_cast<float*>(w + W.adv);
     float* ret_b = reinterpret_cast<float*>(w + W.ret);
     float* grad = reinterpret_cast<float*>(w + W.grad);
+    const __nv_bfloat16* wslab[POD_MAX_HIDDEN_LAYERS + 1];
+    for (int l = 0; l < L.n_layers; ++l)
+        wslab[l] = reinterpret_cast<const __nv_bfloat16*>(static_cast<const char*>(params) + L.w_offset[l]);
     // flat offsets (elements) of W_l, b_l, log_std: pod_fuse_pods order
     int64_t woff[POD_MAX_HIDDEN_LAYERS + 1], boff[POD_MAX_HIDDEN_LAYERS + 1];
     int64_t f = 0;
@@ -119,57 +127,8 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         f += L.w_rows[l];
     }
     const int64_t lsoff = f;
-    const float one = 1.0f, zero = 0.0f;
-    const int B = batch;
-    const unsigned eg = 148 * 4;
-    for (int j = 0; j < n_minibatches; ++j) {
-        ppo_gather_kernel<<<B, 128, 0, s>>>(obs, act_raw, logp_old, adv, ret, perm + static_cast<int64_t>(j) * B, B,
-                                            L.k_pad, n, x0, act_b, lpo_b, adv_b, ret_b);
-        // forward: X_{l+1} = act(X_l W_l^T + b_l); head without activation
-        const float* xin = x0;
-        for (int l = 0; l < L.n_layers; ++l) {
-            const int rows = L.w_rows[l], cols = L.w_cols[l];
-            const bool head = l == L.n_layers - 1;
-            float* out = head ? zh : hbuf + static_cast<int64_t>(l) * B * hidden;
-            POD_CUBLAS(cublasSgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, rows, B, cols, &one, master + woff[l], cols, xin, cols,
-                                   &zero, out, rows));
-            ppo_bias_act_kernel<<<eg, 256, 0, s>>>(out, master + boff[l], B, rows, head ? -1 : act);
-            xin = out;
-        }
-        // head loss and dL/d(head output) -> d0 [B][n_out_pad]; gradient vector cleared first
-        POD_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * L.n_elems, s));
-        PpoHead hh{B, n, L.n_out_pad, hp->ratio_clip, hp->entropy_coef, hp->value_coef, act_b, lpo_b, adv_b, ret_b,
-                   zh, master + lsoff, d0, grad + lsoff, losses};
-        ppo_head_kernel<<<(B + 127) / 128, 128, 0, s>>>(hh);
-        ppo_entropy_kernel<<<1, 128, 0, s>>>(master + lsoff, n, hp->entropy_coef, grad + lsoff, losses);
-        // backward: dW_l = delta_l^T X_l, db_l = colsum(delta_l), delta_{l-1} = (delta_l W_l) * act'(X_l)
-        float* dcur = d0;
-        float* dnext = d1;
-        for (int l = L.n_layers - 1; l >= 0; --l) {
-            const int rows = L.w_rows[l], cols = L.w_cols[l];
-            const float* xl = l == 0 ? x0 : hbuf + static_cast<int64_t>(l - 1) * B * hidden;
-            POD_CUBLAS(cublasSgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, cols, rows, B, &one, xl, cols, dcur, rows, &zero,
-                                   grad + woff[l], cols));
-            ppo_colsum_kernel<<<(rows + 127) / 128, 128, 0, s>>>(dcur, B, rows, grad + boff[l]);
-            if (l > 0) {
-                POD_CUBLAS(cublasSgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, cols, B, rows, &one, master + woff[l], cols, dcur,
-                                       rows, &zero, dnext, cols));
-                ppo_act_grad_kernel<<<eg, 256, 0, s>>>(dnext, xl, static_cast<int64_t>(B) * cols, act);
-                float* t = dcur;
-                dcur = dnext;
-                dnext = t;
-            }
-        }
-        const int64_t step = adam_t + j + 1;
-        const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta1), static_cast<double>(step)));
-        const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta2), static_cast<double>(step)));
-        if (grad_out && j == n_minibatches - 1)
-            POD_CUDA(cudaMemcpyAsync(grad_out, grad, sizeof(float) * L.n_elems, cudaMemcpyDeviceToDevice, s));
-        ppo_adam_kernel<<<eg, 256, 0, s>>>(master, adam_m, adam_v, grad, static_cast<int64_t>(L.n_elems),
-                                           hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps, c1, c2);
-        POD_CUDA(cudaGetLastError());
-    }
-    // refresh the rollout slab (agent 0) from the master copy: the fusion narrowing with K = 1, tau = 1
+    // slab refresh from the master copy after every Adam step (the GEMMs read the bf16 slab): the fusion
+    // narrowing with K = 1, tau = 1
     FuseArgs fa{};
     {
         uint64_t fl = 0;
@@ -195,7 +154,70 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         fa.tau = 1.0f;
     }
     const int64_t g8 = fa.n_elems / 8;
-    fuse_blend_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>((g8 + 255) / 256, 8 * 148)), 1), 256, 0, s>>>(fa);
-    POD_CUDA(cudaGetLastError());
+    const dim3 ngrid(static_cast<unsigned>(std::min<int64_t>((g8 + 255) / 256, 8 * 148)), 1);
+    const float one = 1.0f, zero = 0.0f;
+    const int B = batch;
+    const unsigned eg = 148 * 4;
+    for (int j = 0; j < n_minibatches; ++j) {
+        ppo_gather_kernel<<<B, 128, 0, s>>>(obs, act_raw, logp_old, adv, ret, perm + static_cast<int64_t>(j) * B, B,
+                                            L.k_pad, n, reinterpret_cast<uint16_t*>(x0), act_b, lpo_b, adv_b, ret_b);
+        // forward: X_{l+1} = act(X_l W_l^T + b_l) (bf16 x bf16 -> f32 GEMM, bias + activation -> bf16)
+        const __nv_bfloat16* xin = x0;
+        for (int l = 0; l < L.n_layers; ++l) {
+            const int rows = L.w_rows[l], cols = L.w_cols[l];
+            const bool head = l == L.n_layers - 1;
+            float* out = head ? zh : zf;
+            POD_CUBLAS(cublasGemmEx(cb, CUBLAS_OP_T, CUBLAS_OP_N, rows, B, cols, &one, wslab[l], CUDA_R_16BF, cols, xin,
+                                    CUDA_R_16BF, cols, &zero, out, CUDA_R_32F, rows, CUBLAS_COMPUTE_32F,
+                                    CUBLAS_GEMM_DEFAULT));
+            __nv_bfloat16* hout = head ? nullptr : hbuf + static_cast<int64_t>(l) * B * hidden;
+            ppo_bias_act_kernel<<<eg, 256, 0, s>>>(out, master + boff[l], B, rows, head ? -1 : act, hout);
+            xin = hout;
+        }
+        // head loss and dL/d(head output) -> d0 / b0 [B][n_out_pad]; gradient vector cleared first
+        POD_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * L.n_elems, s));
+        PpoHead hh{B, n, L.n_out_pad, hp->ratio_clip, hp->entropy_coef, hp->value_coef, act_b, lpo_b, adv_b, ret_b,
+                   zh, master + lsoff, d0, b0, grad + lsoff, losses};
+        ppo_head_kernel<<<(B + 127) / 128, 128, 0, s>>>(hh);
+        ppo_entropy_kernel<<<1, 128, 0, s>>>(master + lsoff, n, hp->entropy_coef, grad + lsoff, losses);
+        // backward: dW_l = delta_l^T X_l, db_l = colsum(delta_l), delta_{l-1} = (delta_l W_l) * act'(X_l)
+        float* dcur = d0;
+        float* dnext = d1;
+        __nv_bfloat16* bcur = b0;
+        __nv_bfloat16* bnext = b1;
+        for (int l = L.n_layers - 1; l >= 0; --l) {
+            const int rows = L.w_rows[l], cols = L.w_cols[l];
+            const __nv_bfloat16* xl = l == 0 ? x0 : hbuf + static_cast<int64_t>(l - 1) * B * hidden;
+            POD_CUBLAS(cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_T, cols, rows, B, &one, xl, CUDA_R_16BF, cols, bcur,
+                                    CUDA_R_16BF, rows, &zero, grad + woff[l], CUDA_R_32F, cols, CUBLAS_COMPUTE_32F,
+                                    CUBLAS_GEMM_DEFAULT));
+            ppo_colsum_kernel<<<(rows + 127) / 128, 128, 0, s>>>(dcur, B, rows, grad + boff[l]);
+            if (l > 0) {
+                POD_CUBLAS(cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, cols, B, rows, &one, wslab[l], CUDA_R_16BF, cols,
+                                        bcur, CUDA_R_16BF, rows, &zero, dnext, CUDA_R_32F, cols, CUBLAS_COMPUTE_32F,
+                                        CUBLAS_GEMM_DEFAULT));
+                ppo_act_grad_kernel<<<eg, 256, 0, s>>>(dnext, xl, static_cast<int64_t>(B) * cols, act, bnext);
+                float* t = dcur;
+                dcur = dnext;
+                dnext = t;
+                __nv_bfloat16* tb = bcur;
+                bcur = bnext;
+                bnext = tb;
+            }
+        }
+        const int64_t step = adam_t + j + 1;
+        const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta1), static_cast<double>(step)));
+        const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta2), static_cast<double>(step)));
+        if (grad_out && j == n_minibatches - 1)
+            POD_CUDA(cudaMemcpyAsync(grad_out, grad, sizeof(float) * L.n_elems, cudaMemcpyDeviceToDevice, s));
+        ppo_adam_kernel<<<eg, 256, 0, s>>>(master, adam_m, adam_v, grad, static_cast<int64_t>(L.n_elems),
+                                           hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps, c1, c2);
+        fuse_blend_kernel<<<ngrid, 256, 0, s>>>(fa);
+        POD_CUDA(cudaGetLastError());
+    }
+    if (n_minibatches == 0) {
+        fuse_blend_kernel<<<ngrid, 256, 0, s>>>(fa);
+        POD_CUDA(cudaGetLastError());
+    }
     return POD_OK;
 }

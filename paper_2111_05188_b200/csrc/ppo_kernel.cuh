@@ -10,9 +10,11 @@
 //   dL/dmu_i      = -(1/B) [s1 <= s2] A rho z_i / sigma_i
 //   dL/dlog sig_i = -(1/B) sum_b [s1 <= s2] A rho (z_i^2 - 1) - c_ent
 //   dL/dV         = (2 c_v / B) (V - R)
-// The layer GEMMs (forward X W^T, backward delta^T X and delta W) run on cuBLAS in float32; these
-// kernels are the gather, bias + activation, head loss, activation derivative, bias reduction and
-// the Adam step.  Activations are kept post-nonlinearity: ReLU' = [h > 0], tanh' = 1 - h^2.
+// The layer GEMMs (forward X W^T, backward delta^T X and delta W) are bf16 x bf16 -> float32 tensor-core
+// GEMMs (cuBLAS, as the rollout's actor: bf16 weights = the rollout slab, bf16 activations); these
+// kernels are the gather, bias + activation, head loss, activation derivative (each writing the float32
+// value and its bf16 copy for the next GEMM), bias reduction and the Adam step on the float32 master.
+// Activations are kept post-nonlinearity: ReLU' = [h > 0], tanh' = 1 - h^2.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -30,20 +32,22 @@ struct PpoHead {
     const float* zh;         // [B][n_out_pad] head output (mu in 0..n-1, V in n)
     const float* log_std;    // [n] (master)
     float* delta;            // [B][n_out_pad] dL/d head output
+    __nv_bfloat16* delta_bf; // [B][n_out_pad] its bf16 copy (GEMM operand)
     float* g_log_std;        // [n] accumulated (atomic)
     double* losses;          // [4]
 };
 
-// gather the minibatch rows perm[0..B) of the flattened buffer; obs widened from bf16
+// gather the minibatch rows perm[0..B) of the flattened buffer (obs rows stay bf16: the first GEMM's operand)
 __global__ void ppo_gather_kernel(const uint16_t* __restrict__ obs, const float* __restrict__ act,
                                   const float* __restrict__ lpo, const float* __restrict__ adv,
                                   const float* __restrict__ ret, const int32_t* __restrict__ perm, int B, int k_pad,
-                                  int n, float* __restrict__ x0, float* __restrict__ act_b, float* __restrict__ lpo_b,
+                                  int n, uint16_t* __restrict__ x0, float* __restrict__ act_b, float* __restrict__ lpo_b,
                                   float* __restrict__ adv_b, float* __restrict__ ret_b) {
     const int r = blockIdx.x;
     const int64_t src = perm[r];
-    for (int c = threadIdx.x; c < k_pad; c += blockDim.x)
-        x0[static_cast<int64_t>(r) * k_pad + c] = __uint_as_float(static_cast<uint32_t>(obs[src * k_pad + c]) << 16);
+    const uint4* s4 = reinterpret_cast<const uint4*>(obs + src * k_pad);
+    uint4* d4 = reinterpret_cast<uint4*>(x0 + static_cast<int64_t>(r) * k_pad);
+    for (int c = threadIdx.x; c < k_pad / 8; c += blockDim.x) d4[c] = s4[c];   // bf16 rows, 16 B at a time
     for (int c = threadIdx.x; c < n; c += blockDim.x) act_b[static_cast<int64_t>(r) * n + c] = act[src * n + c];
     if (threadIdx.x == 0) {
         lpo_b[r] = lpo[src];
@@ -52,15 +56,18 @@ __global__ void ppo_gather_kernel(const uint16_t* __restrict__ obs, const float*
     }
 }
 
-// Z[B][N] (from the GEMM) += b, then the activation in place (act 0 ReLU, 1 tanh, -1 none)
-__global__ void ppo_bias_act_kernel(float* __restrict__ z, const float* __restrict__ b, int64_t B, int N, int act) {
+// Z[B][N] (from the GEMM) + b, then the activation (act 0 ReLU, 1 tanh, -1 none): into z in place
+// (head) or, when h is given, as the bf16 activation of the next layer
+__global__ void ppo_bias_act_kernel(float* __restrict__ z, const float* __restrict__ b, int64_t B, int N, int act,
+                                    __nv_bfloat16* __restrict__ h) {
     const int64_t total = B * N;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         float v = z[i] + b[i % N];
         if (act == 0) v = fmaxf(v, 0.0f);
         else if (act == 1) v = tanhf(v);
-        z[i] = v;
+        if (h) h[i] = __float2bfloat16_rn(v);
+        else z[i] = v;
     }
 }
 
@@ -94,12 +101,17 @@ __global__ void __launch_bounds__(128) ppo_head_kernel(const PpoHead h) {
             const float isig = expf(-h.log_std[i]);
             const float z = (raw[i] - mu[i]) * isig;
             d[i] = coef * z * isig;                            // dlogp/dmu_i = z_i / sigma_i
+            h.delta_bf[static_cast<int64_t>(b) * h.n_out_pad + i] = __float2bfloat16_rn(d[i]);
             if (coef != 0.0f) atomicAdd(&g_ls[i], coef * (z * z - 1.0f));
         }
         const float V = mu[h.n];
         const float R = h.ret[b];
         d[h.n] = 2.0f * h.c_v * (V - R) * inv_b;
-        for (int i = h.n + 1; i < h.n_out_pad; ++i) d[i] = 0.0f;
+        h.delta_bf[static_cast<int64_t>(b) * h.n_out_pad + h.n] = __float2bfloat16_rn(d[h.n]);
+        for (int i = h.n + 1; i < h.n_out_pad; ++i) {
+            d[i] = 0.0f;
+            h.delta_bf[static_cast<int64_t>(b) * h.n_out_pad + i] = __float2bfloat16_rn(0.0f);
+        }
         vl = static_cast<double>(V - R) * static_cast<double>(V - R);
     }
     red[0][threadIdx.x] = obj;
@@ -131,12 +143,15 @@ __global__ void ppo_entropy_kernel(const float* __restrict__ log_std, int n, flo
     if ((threadIdx.x & 31) == 0) atomicAdd(&losses[2], s);
 }
 
-// delta = dX * act'(H) in place on dX (H the layer's post-activation output)
-__global__ void ppo_act_grad_kernel(float* __restrict__ dx, const float* __restrict__ hact, int64_t total, int act) {
+// delta = dX * act'(H) in place on dX (H the layer's bf16 post-activation output), plus its bf16 copy
+__global__ void ppo_act_grad_kernel(float* __restrict__ dx, const __nv_bfloat16* __restrict__ hact, int64_t total,
+                                    int act, __nv_bfloat16* __restrict__ dbf) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const float h = hact[i];
-        dx[i] *= act == 0 ? (h > 0.0f ? 1.0f : 0.0f) : (1.0f - h * h);
+        const float h = __bfloat162float(hact[i]);
+        const float d = dx[i] * (act == 0 ? (h > 0.0f ? 1.0f : 0.0f) : (1.0f - h * h));
+        dx[i] = d;
+        dbf[i] = __float2bfloat16_rn(d);
     }
 }
 

@@ -552,13 +552,18 @@ def test_ppo_update_parity(act):
         segs.append((o, o + L.w_rows[l]))
         o += L.w_rows[l]
     segs.append((o, o + L.n_out_pad))
+    # the learner's GEMMs take bf16 operands (weights = the bf16 slab, activations and deltas rounded to
+    # bf16) with float32 accumulation, against the float64 oracle: a bf16-level bar per segment
     for a0, a1 in segs:
         ref = g_o[a0:a1]
         scale = np.abs(ref).max() + 1e-12
-        assert np.linalg.norm(g_g[a0:a1] - ref) <= 2e-4 * np.linalg.norm(ref) + 1e-7 * scale * math.sqrt(a1 - a0), (a0, a1)
-        assert np.all(np.abs(g_g[a0:a1] - ref) <= 2e-3 * scale + 1e-7), (a0, a1)
+        rel = np.linalg.norm(g_g[a0:a1] - ref) / (np.linalg.norm(ref) + 1e-30)
+        assert rel <= 2e-2, (a0, a1, rel)
+        assert np.all(np.abs(g_g[a0:a1] - ref) <= 5e-2 * scale + 1e-7), (a0, a1, np.abs(g_g[a0:a1] - ref).max() / scale)
     ls = losses.cpu().numpy()
-    assert ls[0] == pytest.approx(sobj, rel=1e-4, abs=1e-3) and ls[1] == pytest.approx(svl, rel=1e-4)
+    # bf16 forward: each rho carries ~1e-2 of relative error (as the rollout's own log-probs do)
+    A_abs = float(np.abs(A[rows].cpu().numpy()).sum())
+    assert abs(ls[0] - sobj) <= 2e-2 * A_abs and ls[1] == pytest.approx(svl, rel=5e-2)
     assert ls[2] == pytest.approx(H, rel=1e-6) and ls[3] == B
     # Adam, first step, on the device gradient
     th1, _, _ = oracle.adam_step(theta0, np.zeros_like(theta0), np.zeros_like(theta0), g_g, 1, lr)
