@@ -1,6 +1,8 @@
 // pod_ppo.cuh — host side of pod_ppo_update (included by pod_api.cu; kernels in ppo_kernel.cuh).
-// Forward/backward GEMMs are plain float32 library GEMMs (cuBLAS, column-major view of the
-// row-major [rows][cols] matrices); every other step runs in this library's kernels.
+// Forward/backward GEMMs are bf16 x bf16 -> float32 library GEMMs (cuBLAS tensor cores, column-major view
+// of the row-major [rows][cols] matrices); every other step runs in this library's kernels.  The whole
+// minibatch loop (~28 launches per minibatch) is captured once into a CUDA graph per argument set and
+// replayed; only the Adam step counter changes between calls and it is read from device memory.
 #pragma once
 #include <cublas_v2.h>
 
@@ -9,7 +11,7 @@
 namespace pod {
 
 struct PpoWs {
-    size_t x0, h, zf, zh, d0, d1, b0, b1, act, lpo, adv, ret, grad, total;
+    size_t x0, h, zf, zh, d0, b0, b1, act, lpo, adv, ret, grad, step, total;
 };
 
 inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, int B, int n) {
@@ -21,8 +23,7 @@ inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, 
     w.h = o;   o += up(2 * static_cast<size_t>(B) * hidden * n_hidden);             // bf16 activations
     w.zf = o;  o += up(sizeof(float) * static_cast<size_t>(B) * hidden);            // f32 GEMM output
     w.zh = o;  o += up(sizeof(float) * static_cast<size_t>(B) * L.n_out_pad);       // f32 head output
-    w.d0 = o;  o += up(sizeof(float) * dmax);                                       // f32 deltas
-    w.d1 = o;  o += up(sizeof(float) * dmax);
+    w.d0 = o;  o += up(sizeof(float) * dmax);                                       // f32 dX GEMM output
     w.b0 = o;  o += up(2 * dmax);                                                   // their bf16 copies
     w.b1 = o;  o += up(2 * dmax);
     w.act = o; o += up(sizeof(float) * static_cast<size_t>(B) * n);
@@ -30,20 +31,56 @@ inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, 
     w.adv = o; o += up(sizeof(float) * B);
     w.ret = o; o += up(sizeof(float) * B);
     w.grad = o; o += up(sizeof(float) * L.n_elems);
+    w.step = o; o += 256;                                                            // int64 Adam step base
     w.total = o;
     return w;
 }
 
+// one cuBLAS handle per thread and device, with an explicit workspace (no allocation under graph capture)
 inline cublasHandle_t ppo_cublas() {
     static thread_local cublasHandle_t h = nullptr;
     static thread_local int dev = -1;
+    static thread_local void* cws = nullptr;
     int d = 0;
     cudaGetDevice(&d);
     if (!h || d != dev) {
         if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+        constexpr size_t kWs = 32u << 20;
+        if (cudaMalloc(&cws, kWs) != cudaSuccess) return nullptr;
+        if (cublasSetWorkspace(h, cws, kWs) != CUBLAS_STATUS_SUCCESS) return nullptr;
         dev = d;
     }
     return h;
+}
+
+// captured minibatch loops, keyed on every argument but adam_t and the stream
+struct PpoGraphKey {
+    const void* p[16];
+    int64_t M, k_pad, n_elems;
+    int32_t cfg_n, n_hidden, hidden, act, batch, n_mb, dev;
+    pod_ppo_hparams hp;
+    size_t param_bytes, ws_bytes;
+    bool operator==(const PpoGraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct PpoGraph {
+    PpoGraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t used;
+};
+inline std::vector<PpoGraph>& ppo_graphs() {
+    static thread_local std::vector<PpoGraph> g;
+    return g;
+}
+inline cudaStream_t ppo_cap_stream() {
+    static thread_local cudaStream_t cs = nullptr;
+    static thread_local int dev = -1;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!cs || d != dev) {
+        if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        dev = d;
+    }
+    return cs;
 }
 
 }  // namespace pod
@@ -90,21 +127,21 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     const PpoWs W = ppo_ws_layout(L, n_hidden, hidden, batch, n);
     if (ws_bytes < W.total) return pod_fail(POD_ERR_ARG, "workspace needs %zu bytes", W.total);
     if (reinterpret_cast<uintptr_t>(ws) % 256 != 0 || reinterpret_cast<uintptr_t>(master) % 16 != 0 ||
+        reinterpret_cast<uintptr_t>(adam_m) % 16 != 0 || reinterpret_cast<uintptr_t>(adam_v) % 16 != 0 ||
         reinterpret_cast<uintptr_t>(params) % 16 != 0)
-        return pod_fail(POD_ERR_ARG, "ws must be 256-byte aligned, master and params 16-byte aligned");
+        return pod_fail(POD_ERR_ARG, "ws must be 256-byte aligned, master, adam_m, adam_v and params 16-byte aligned");
     st = pod_require_sm100();
     if (st) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaStream_t user_s = static_cast<cudaStream_t>(stream);
     cublasHandle_t cb = ppo_cublas();
-    if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate failed");
-    POD_CUBLAS(cublasSetStream(cb, s));
+    if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate / workspace failed");
     char* w = static_cast<char*>(ws);
+    int64_t* step_slot = reinterpret_cast<int64_t*>(w + W.step);
     __nv_bfloat16* x0 = reinterpret_cast<__nv_bfloat16*>(w + W.x0);
     __nv_bfloat16* hbuf = reinterpret_cast<__nv_bfloat16*>(w + W.h);
     float* zf = reinterpret_cast<float*>(w + W.zf);
     float* zh = reinterpret_cast<float*>(w + W.zh);
     float* d0 = reinterpret_cast<float*>(w + W.d0);
-    float* d1 = reinterpret_cast<float*>(w + W.d1);
     __nv_bfloat16* b0 = reinterpret_cast<__nv_bfloat16*>(w + W.b0);
     __nv_bfloat16* b1 = reinterpret_cast<__nv_bfloat16*>(w + W.b1);
     float* act_b = reinterpret_cast<float*>(w + W.act);
@@ -158,6 +195,10 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     const float one = 1.0f, zero = 0.0f;
     const int B = batch;
     const unsigned eg = 148 * 4;
+    const unsigned ag_rows = static_cast<unsigned>((B + PPO_AG_ROWS - 1) / PPO_AG_ROWS);   // <= 2^31 / 16
+    // the minibatch loop, enqueued on stream s (captured below, or eager with POD_PPO_GRAPH=0)
+    auto enqueue = [&](cudaStream_t s) -> pod_status {
+    POD_CUBLAS(cublasSetStream(cb, s));
     for (int j = 0; j < n_minibatches; ++j) {
         ppo_gather_kernel<<<B, 128, 0, s>>>(obs, act_raw, logp_old, adv, ret, perm + static_cast<int64_t>(j) * B, B,
                                             L.k_pad, n, reinterpret_cast<uint16_t*>(x0), act_b, lpo_b, adv_b, ret_b);
@@ -171,18 +212,18 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
                                     CUDA_R_16BF, cols, &zero, out, CUDA_R_32F, rows, CUBLAS_COMPUTE_32F,
                                     CUBLAS_GEMM_DEFAULT));
             __nv_bfloat16* hout = head ? nullptr : hbuf + static_cast<int64_t>(l) * B * hidden;
-            ppo_bias_act_kernel<<<eg, 256, 0, s>>>(out, master + boff[l], B, rows, head ? -1 : act, hout);
+            ppo_bias_act_kernel<<<dim3((rows / 4 + 127) / 128, std::min(B, 65535)), 128, 0, s>>>(out, master + boff[l], B, rows,
+                                                                                head ? -1 : act, hout);
             xin = hout;
         }
-        // head loss and dL/d(head output) -> d0 / b0 [B][n_out_pad]; gradient vector cleared first
+        // head loss and dL/d(head output) -> b0 [B][n_out_pad] (bf16) and the head bias gradient; gradient
+        // vector cleared first
         POD_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * L.n_elems, s));
         PpoHead hh{B, n, L.n_out_pad, hp->ratio_clip, hp->entropy_coef, hp->value_coef, act_b, lpo_b, adv_b, ret_b,
-                   zh, master + lsoff, d0, b0, grad + lsoff, losses};
-        ppo_head_kernel<<<(B + 127) / 128, 128, 0, s>>>(hh);
-        ppo_entropy_kernel<<<1, 128, 0, s>>>(master + lsoff, n, hp->entropy_coef, grad + lsoff, losses);
-        // backward: dW_l = delta_l^T X_l, db_l = colsum(delta_l), delta_{l-1} = (delta_l W_l) * act'(X_l)
-        float* dcur = d0;
-        float* dnext = d1;
+                   zh, master + lsoff, b0, grad + boff[L.n_layers - 1], grad + lsoff, losses};
+        ppo_head_kernel<<<(B + PPO_HEAD_WARPS - 1) / PPO_HEAD_WARPS, 32 * PPO_HEAD_WARPS, 0, s>>>(hh);
+        // backward: dW_l = delta_l^T X_l, delta_{l-1} = (delta_l W_l) * act'(X_l) with db_{l-1} = colsum
+        // (delta_{l-1}) fused into the activation-derivative kernel
         __nv_bfloat16* bcur = b0;
         __nv_bfloat16* bnext = b1;
         for (int l = L.n_layers - 1; l >= 0; --l) {
@@ -191,27 +232,21 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
             POD_CUBLAS(cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_T, cols, rows, B, &one, xl, CUDA_R_16BF, cols, bcur,
                                     CUDA_R_16BF, rows, &zero, grad + woff[l], CUDA_R_32F, cols, CUBLAS_COMPUTE_32F,
                                     CUBLAS_GEMM_DEFAULT));
-            ppo_colsum_kernel<<<(rows + 127) / 128, 128, 0, s>>>(dcur, B, rows, grad + boff[l]);
             if (l > 0) {
                 POD_CUBLAS(cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, cols, B, rows, &one, wslab[l], CUDA_R_16BF, cols,
-                                        bcur, CUDA_R_16BF, rows, &zero, dnext, CUDA_R_32F, cols, CUBLAS_COMPUTE_32F,
+                                        bcur, CUDA_R_16BF, rows, &zero, d0, CUDA_R_32F, cols, CUBLAS_COMPUTE_32F,
                                         CUBLAS_GEMM_DEFAULT));
-                ppo_act_grad_kernel<<<eg, 256, 0, s>>>(dnext, xl, static_cast<int64_t>(B) * cols, act, bnext);
-                float* t = dcur;
-                dcur = dnext;
-                dnext = t;
+                ppo_act_grad_kernel<<<dim3((cols / 2 + 127) / 128, ag_rows), 128, 0, s>>>(
+                    d0, xl, B, cols, act, bnext, grad + boff[l - 1]);
                 __nv_bfloat16* tb = bcur;
                 bcur = bnext;
                 bnext = tb;
             }
         }
-        const int64_t step = adam_t + j + 1;
-        const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta1), static_cast<double>(step)));
-        const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(hp->adam_beta2), static_cast<double>(step)));
         if (grad_out && j == n_minibatches - 1)
             POD_CUDA(cudaMemcpyAsync(grad_out, grad, sizeof(float) * L.n_elems, cudaMemcpyDeviceToDevice, s));
         ppo_adam_kernel<<<eg, 256, 0, s>>>(master, adam_m, adam_v, grad, static_cast<int64_t>(L.n_elems),
-                                           hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps, c1, c2);
+                                           hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps, step_slot, j);
         fuse_blend_kernel<<<ngrid, 256, 0, s>>>(fa);
         POD_CUDA(cudaGetLastError());
     }
@@ -219,5 +254,65 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         fuse_blend_kernel<<<ngrid, 256, 0, s>>>(fa);
         POD_CUDA(cudaGetLastError());
     }
+    return POD_OK;
+    };
+    ppo_set_step_kernel<<<1, 1, 0, user_s>>>(step_slot, adam_t);
+    POD_CUDA(cudaGetLastError());
+    static const bool use_graph = [] {
+        const char* e = std::getenv("POD_PPO_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    if (!use_graph) return enqueue(user_s);
+    PpoGraphKey key;
+    std::memset(&key, 0, sizeof(key));
+    const void* kp[16] = {master, adam_m, adam_v, params, obs, act_raw, logp_old, adv, ret, perm, losses, grad_out, ws,
+                          nullptr, nullptr, nullptr};
+    std::memcpy(key.p, kp, sizeof(kp));
+    key.M = M;
+    key.k_pad = L.k_pad;
+    key.n_elems = static_cast<int64_t>(L.n_elems);
+    key.cfg_n = n;
+    key.n_hidden = n_hidden;
+    key.hidden = hidden;
+    key.act = act;
+    key.batch = batch;
+    key.n_mb = n_minibatches;
+    cudaGetDevice(&key.dev);
+    key.hp = *hp;
+    key.param_bytes = param_bytes;
+    key.ws_bytes = ws_bytes;
+    static thread_local uint64_t ppo_clock = 0;
+    auto& cache = ppo_graphs();
+    PpoGraph* hit = nullptr;
+    for (auto& g : cache)
+        if (g.key == key) hit = &g;
+    if (!hit) {
+        cudaStream_t cs = ppo_cap_stream();
+        if (!cs) return pod_fail(POD_ERR_CUDA, "capture stream creation failed");
+        cudaGraph_t graph;
+        POD_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        pod_status est = enqueue(cs);
+        cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (est) {
+            if (ce == cudaSuccess) cudaGraphDestroy(graph);
+            return est;
+        }
+        if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "PPO graph capture: %s", cudaGetErrorString(ce));
+        cudaGraphExec_t exec;
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "PPO graph instantiate: %s", cudaGetErrorString(ce));
+        if (cache.size() >= 4) {   // evict the least recently used
+            size_t victim = 0;
+            for (size_t i = 1; i < cache.size(); ++i)
+                if (cache[i].used < cache[victim].used) victim = i;
+            cudaGraphExecDestroy(cache[victim].exec);
+            cache.erase(cache.begin() + static_cast<long>(victim));
+        }
+        cache.push_back(PpoGraph{key, exec, 0});
+        hit = &cache.back();
+    }
+    hit->used = ++ppo_clock;
+    POD_CUDA(cudaGraphLaunch(hit->exec, user_s));
     return POD_OK;
 }

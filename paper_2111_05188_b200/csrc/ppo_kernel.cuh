@@ -31,8 +31,8 @@ struct PpoHead {
     const float* ret;        // [B]
     const float* zh;         // [B][n_out_pad] head output (mu in 0..n-1, V in n)
     const float* log_std;    // [n] (master)
-    float* delta;            // [B][n_out_pad] dL/d head output
-    __nv_bfloat16* delta_bf; // [B][n_out_pad] its bf16 copy (GEMM operand)
+    __nv_bfloat16* delta_bf; // [B][n_out_pad] dL/d head output, bf16 (the backward GEMMs' operand)
+    float* g_bias;           // [n_out_pad] head bias gradient = column sums of the float32 delta (atomic)
     float* g_log_std;        // [n] accumulated (atomic)
     double* losses;          // [4]
 };
@@ -57,27 +57,59 @@ __global__ void ppo_gather_kernel(const uint16_t* __restrict__ obs, const float*
 }
 
 // Z[B][N] (from the GEMM) + b, then the activation (act 0 ReLU, 1 tanh, -1 none): into z in place
-// (head) or, when h is given, as the bf16 activation of the next layer
+// (head) or, when h is given, as the bf16 activation of the next layer.  Block = one row (grid-strided
+// over rows), thread = 4 consecutive columns (N is a multiple of 32).
 __global__ void ppo_bias_act_kernel(float* __restrict__ z, const float* __restrict__ b, int64_t B, int N, int act,
                                     __nv_bfloat16* __restrict__ h) {
-    const int64_t total = B * N;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-        float v = z[i] + b[i % N];
-        if (act == 0) v = fmaxf(v, 0.0f);
-        else if (act == 1) v = tanhf(v);
-        if (h) h[i] = __float2bfloat16_rn(v);
-        else z[i] = v;
+    const int c = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (c >= N) return;
+    for (int64_t r = blockIdx.y; r < B; r += gridDim.y) {
+    const int64_t i = r * N + c;
+    float4 v = *reinterpret_cast<const float4*>(z + i);
+    const float4 bc = *reinterpret_cast<const float4*>(b + c);
+    v.x += bc.x;
+    v.y += bc.y;
+    v.z += bc.z;
+    v.w += bc.w;
+    if (act == 0) {
+        v.x = fmaxf(v.x, 0.0f);
+        v.y = fmaxf(v.y, 0.0f);
+        v.z = fmaxf(v.z, 0.0f);
+        v.w = fmaxf(v.w, 0.0f);
+    } else if (act == 1) {
+        v.x = tanhf(v.x);
+        v.y = tanhf(v.y);
+        v.z = tanhf(v.z);
+        v.w = tanhf(v.w);
+    }
+    if (h) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(h + i) = pk;
+    } else {
+        *reinterpret_cast<float4*>(z + i) = v;
+    }
     }
 }
 
-// one thread per sample: head loss and dL/d(head output); log-std gradient and loss sums reduced per block
-__global__ void __launch_bounds__(128) ppo_head_kernel(const PpoHead h) {
+// one warp per sample (lanes over tickers): head loss and dL/d(head output); the log-std gradient and the
+// loss sums are reduced per block in shared memory, then one atomic each
+// (n_out_pad <= 128, checked at layout time).  Block 0 also adds the entropy term of the log-std gradient,
+// -c_ent, and the entropy value sum_i (log sigma_i + (1 + ln 2 pi) / 2).
+constexpr int PPO_HEAD_WARPS = 8;
+__global__ void __launch_bounds__(32 * PPO_HEAD_WARPS) ppo_head_kernel(const PpoHead h) {
     __shared__ float g_ls[128];
-    __shared__ double red[3][128];
-    for (int i = threadIdx.x; i < h.n && i < 128; i += blockDim.x) g_ls[i] = 0.0f;
+    __shared__ float g_b[128];
+    __shared__ double red[4][PPO_HEAD_WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+        g_ls[i] = 0.0f;
+        g_b[i] = 0.0f;
+    }
     __syncthreads();
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.x * PPO_HEAD_WARPS + warp;
     const float inv_b = 1.0f / static_cast<float>(h.B);
     const float half_ln_2pi = 0.918938533204672742f;
     double obj = 0.0, vl = 0.0;
@@ -85,10 +117,12 @@ __global__ void __launch_bounds__(128) ppo_head_kernel(const PpoHead h) {
         const float* mu = h.zh + static_cast<int64_t>(b) * h.n_out_pad;
         const float* raw = h.act + static_cast<int64_t>(b) * h.n;
         float logp = 0.0f;
-        for (int i = 0; i < h.n; ++i) {
+        for (int i = lane; i < h.n; i += 32) {
             const float z = (raw[i] - mu[i]) * expf(-h.log_std[i]);
             logp += -0.5f * z * z - h.log_std[i] - half_ln_2pi;
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) logp += __shfl_xor_sync(0xffffffffu, logp, o);
         const float A = h.adv[b];
         const float rho = expf(logp - h.logp_old[b]);
         const float s1 = rho * A;
@@ -96,87 +130,117 @@ __global__ void __launch_bounds__(128) ppo_head_kernel(const PpoHead h) {
         const bool active = s1 <= s2;
         obj = static_cast<double>(active ? s1 : s2);
         const float coef = active ? -A * rho * inv_b : 0.0f;   // dL/dlogp of this sample
-        float* d = h.delta + static_cast<int64_t>(b) * h.n_out_pad;
-        for (int i = 0; i < h.n; ++i) {
-            const float isig = expf(-h.log_std[i]);
-            const float z = (raw[i] - mu[i]) * isig;
-            d[i] = coef * z * isig;                            // dlogp/dmu_i = z_i / sigma_i
-            h.delta_bf[static_cast<int64_t>(b) * h.n_out_pad + i] = __float2bfloat16_rn(d[i]);
-            if (coef != 0.0f) atomicAdd(&g_ls[i], coef * (z * z - 1.0f));
-        }
+        __nv_bfloat16* dbf = h.delta_bf + static_cast<int64_t>(b) * h.n_out_pad;
         const float V = mu[h.n];
         const float R = h.ret[b];
-        d[h.n] = 2.0f * h.c_v * (V - R) * inv_b;
-        h.delta_bf[static_cast<int64_t>(b) * h.n_out_pad + h.n] = __float2bfloat16_rn(d[h.n]);
-        for (int i = h.n + 1; i < h.n_out_pad; ++i) {
-            d[i] = 0.0f;
-            h.delta_bf[static_cast<int64_t>(b) * h.n_out_pad + i] = __float2bfloat16_rn(0.0f);
+        for (int i = lane; i < h.n_out_pad; i += 32) {
+            float di = 0.0f;
+            if (i < h.n) {
+                const float isig = expf(-h.log_std[i]);
+                const float z = (raw[i] - mu[i]) * isig;
+                di = coef * z * isig;                          // dlogp/dmu_i = z_i / sigma_i
+                if (coef != 0.0f) atomicAdd(&g_ls[i], coef * (z * z - 1.0f));
+            } else if (i == h.n) {
+                di = 2.0f * h.c_v * (V - R) * inv_b;
+            }
+            if (di != 0.0f) atomicAdd(&g_b[i], di);
+            dbf[i] = __float2bfloat16_rn(di);
         }
         vl = static_cast<double>(V - R) * static_cast<double>(V - R);
     }
-    red[0][threadIdx.x] = obj;
-    red[1][threadIdx.x] = vl;
-    red[2][threadIdx.x] = b < h.B ? 1.0 : 0.0;
+    double ent = 0.0;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < h.n; i += blockDim.x) {
+            atomicAdd(&g_ls[i], -h.c_ent);
+            ent += static_cast<double>(h.log_std[i]) + 1.4189385332046727418;   // (1 + ln 2 pi) / 2
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ent += __shfl_xor_sync(0xffffffffu, ent, o);
+    if (lane == 0) {
+        red[0][warp] = obj;
+        red[1][warp] = vl;
+        red[2][warp] = b < h.B ? 1.0 : 0.0;
+        red[3][warp] = ent;
+    }
     __syncthreads();
-    for (int o = 64; o > 0; o >>= 1) {
-        if (threadIdx.x < o)
-            for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + o];
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
-        atomicAdd(&h.losses[0], red[0][0]);
-        atomicAdd(&h.losses[1], red[1][0]);
-        atomicAdd(&h.losses[3], red[2][0]);
+        double s0 = 0.0, s1v = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int k = 0; k < PPO_HEAD_WARPS; ++k) {
+            s0 += red[0][k];
+            s1v += red[1][k];
+            s2 += red[2][k];
+            s3 += red[3][k];
+        }
+        atomicAdd(&h.losses[0], s0);
+        atomicAdd(&h.losses[1], s1v);
+        atomicAdd(&h.losses[3], s2);
+        if (blockIdx.x == 0) atomicAdd(&h.losses[2], s3);
     }
-    for (int i = threadIdx.x; i < h.n && i < 128; i += blockDim.x) atomicAdd(&h.g_log_std[i], g_ls[i]);
+    for (int i = threadIdx.x; i < h.n; i += blockDim.x) atomicAdd(&h.g_log_std[i], g_ls[i]);
+    for (int i = threadIdx.x; i < h.n_out_pad; i += blockDim.x)
+        if (g_b[i] != 0.0f) atomicAdd(&h.g_bias[i], g_b[i]);
 }
 
-// entropy term of the log-std gradient (once per minibatch) and the entropy value
-__global__ void ppo_entropy_kernel(const float* __restrict__ log_std, int n, float c_ent, float* __restrict__ g_log_std,
-                                   double* __restrict__ losses) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        g_log_std[i] += -c_ent;
-        s += static_cast<double>(log_std[i]) + 1.4189385332046727418;   // (1 + ln 2 pi) / 2
-    }
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&losses[2], s);
-}
-
-// delta = dX * act'(H) in place on dX (H the layer's bf16 post-activation output), plus its bf16 copy
-__global__ void ppo_act_grad_kernel(float* __restrict__ dx, const __nv_bfloat16* __restrict__ hact, int64_t total,
-                                    int act, __nv_bfloat16* __restrict__ dbf) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const float h = __bfloat162float(hact[i]);
-        const float d = dx[i] * (act == 0 ? (h > 0.0f ? 1.0f : 0.0f) : (1.0f - h * h));
-        dx[i] = d;
-        dbf[i] = __float2bfloat16_rn(d);
-    }
-}
-
-// db[N] = sum over the B rows of delta[B][N] (thread per column, coalesced rows)
-__global__ void ppo_colsum_kernel(const float* __restrict__ delta, int B, int N, float* __restrict__ db) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+// delta = dX * act'(H) (dX the float32 GEMM output, H the layer's bf16 post-activation output), written as
+// the bf16 operand of the next GEMMs, with the layer's bias gradient db[c] += sum over the block's rows of
+// delta[r][c] fused in (one atomic per column per block).  Block = 128 threads x 2 columns, PPO_AG_ROWS
+// rows; N is a multiple of 32.
+constexpr int PPO_AG_ROWS = 16;
+__global__ void ppo_act_grad_kernel(const float* __restrict__ dx, const __nv_bfloat16* __restrict__ hact, int B, int N,
+                                    int act, __nv_bfloat16* __restrict__ dbf, float* __restrict__ db) {
+    const int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (c >= N) return;
-    float s = 0.0f;
-    for (int r = 0; r < B; ++r) s += delta[static_cast<int64_t>(r) * N + c];
-    db[c] = s;
+    const int r0 = blockIdx.y * PPO_AG_ROWS;
+    float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 8
+    for (int k = 0; k < PPO_AG_ROWS; ++k) {
+        const int r = r0 + k;
+        if (r < B) {
+            const int64_t i = static_cast<int64_t>(r) * N + c;
+            const float2 g = *reinterpret_cast<const float2*>(dx + i);
+            const float2 hv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(hact + i));
+            const float d0 = g.x * (act == 0 ? (hv.x > 0.0f ? 1.0f : 0.0f) : (1.0f - hv.x * hv.x));
+            const float d1 = g.y * (act == 0 ? (hv.y > 0.0f ? 1.0f : 0.0f) : (1.0f - hv.y * hv.y));
+            *reinterpret_cast<__nv_bfloat162*>(dbf + i) = __floats2bfloat162_rn(d0, d1);
+            s0 += d0;
+            s1 += d1;
+        }
+    }
+    if (s0 != 0.0f) atomicAdd(&db[c], s0);
+    if (s1 != 0.0f) atomicAdd(&db[c + 1], s1);
 }
 
-// Adam (bias-corrected) over the flat parameter vector
+// Adam (bias-corrected) over the flat parameter vector; the step number is *step_base + j + 1, read from
+// device memory so that one captured graph serves every call (c1 = 1 - b1^step, c2 = 1 - b2^step)
 __global__ void ppo_adam_kernel(float* __restrict__ theta, float* __restrict__ m, float* __restrict__ v,
                                 const float* __restrict__ g, int64_t count, float lr, float b1, float b2, float eps,
-                                float c1, float c2) {
+                                const int64_t* __restrict__ step_base, int j) {
+    const double step = static_cast<double>(*step_base + j + 1);
+    const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(b1), step));
+    const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(b2), step));
+    auto upd = [&](float& th, float& mi, float& vi, float gi) {
+        mi = b1 * mi + (1.0f - b1) * gi;
+        vi = b2 * vi + (1.0f - b2) * gi * gi;
+        th -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    };
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
-        const float gi = g[i];
-        const float mi = b1 * m[i] + (1.0f - b1) * gi;
-        const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
-        m[i] = mi;
-        v[i] = vi;
-        theta[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t c4 = count / 4;   // all four arrays are 16-byte aligned (checked on the host)
+    for (int64_t q = t0; q < c4; q += stride) {
+        float4 th = reinterpret_cast<float4*>(theta)[q], mi = reinterpret_cast<float4*>(m)[q];
+        float4 vi = reinterpret_cast<float4*>(v)[q];
+        const float4 gi = reinterpret_cast<const float4*>(g)[q];
+        upd(th.x, mi.x, vi.x, gi.x);
+        upd(th.y, mi.y, vi.y, gi.y);
+        upd(th.z, mi.z, vi.z, gi.z);
+        upd(th.w, mi.w, vi.w, gi.w);
+        reinterpret_cast<float4*>(theta)[q] = th;
+        reinterpret_cast<float4*>(m)[q] = mi;
+        reinterpret_cast<float4*>(v)[q] = vi;
     }
+    for (int64_t i = 4 * c4 + t0; i < count; i += stride) upd(theta[i], m[i], v[i], g[i]);
 }
+
+__global__ void ppo_set_step_kernel(int64_t* __restrict__ slot, int64_t adam_t) { *slot = adam_t; }
 
 }  // namespace pod

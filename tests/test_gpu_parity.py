@@ -602,6 +602,42 @@ def test_ppo_learner_improves_surrogate():
     assert torch.isfinite(learner.master).all()
 
 
+def test_ppo_graph_replay_step_counter():
+    """The minibatch loop is a cached CUDA graph replayed across calls; only the Adam step counter differs
+    between calls (read from device memory).  Two calls of one minibatch through the same buffers (the
+    second a replay at adam_t = 1) equal one call of two minibatches: a stale bias correction
+    (1 - beta^step) on the replay would move the parameters by ~2x."""
+    c = Case(n=30, f=3, T_data=400, N=256, H=100, seed=53)
+    aws, params_a, actor = _actor(c, 2, 128)
+    params_b = params_a.clone()
+    T, B = 8, 512
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, critic=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    adv, ret = api.pod_gae(tr.rew, tr.val[:T].contiguous(), tr.done, tr.val[T].contiguous(), 0.99, 0.95,
+                           normalize=True)
+    M = T * c.N
+    args = (tr.obs[:T].reshape(M, c.k_pad), tr.act.reshape(M, c.n), tr.logp.reshape(M), adv.reshape(M), ret.reshape(M))
+    perm = torch.from_numpy(np.random.default_rng(9).permutation(M)[: 2 * B].astype(np.int32)).cuda()
+    la = api.PPOLearner(c.cfg, 2, 128, params_a, batch=B, learning_rate=1e-3)
+    lb = api.PPOLearner(c.cfg, 2, 128, params_b, batch=B, learning_rate=1e-3)
+    m0 = la.master.cpu().numpy()
+    buf = torch.empty(B, dtype=torch.int32, device="cuda")
+    for k in range(2):
+        buf.copy_(perm[k * B:(k + 1) * B])
+        la.update(*args, buf)
+    lb.update(*args, perm)
+    torch.cuda.synchronize()
+    ma, mb = la.master.cpu().numpy(), lb.master.cpu().numpy()
+    assert np.isfinite(ma).all() and np.abs(mb - m0).max() > 1e-4
+    # float atomics (bias and log-std reductions) make the gradient sums order-dependent, and Adam turns a
+    # near-zero gradient into a +-lr step: compare per element at 1 % of lr and allow a 1 % tail (a stale
+    # bias correction moves essentially every updated element by ~1/3 of lr)
+    moved = np.abs(mb - m0) > 0
+    off = np.abs(ma - mb) > 1e-2 * 1e-3
+    assert off[moved].mean() < 0.01, off[moved].mean()
+
+
 # ----------------------------------------------------------------- shape sweep (edge configurations)
 @pytest.mark.parametrize("n,f,N,nh,hid,act,agents,h_max,cost", [
     (1, 3, 1, 1, 128, 0, 1, 100, 0.002),      # one stock, one env (a 1-lane ragged tile)
