@@ -512,14 +512,14 @@ def test_equity_curve_exact_and_backtest_metrics():
     assert np.all(mf[[0, 1, 2, 4]] == 0.0) and np.all(np.isnan(mf[3]))
 
 
-@pytest.mark.parametrize("act", [0, 1])
-def test_ppo_update_parity(act):
+@pytest.mark.parametrize("act,B", [(0, 512), (1, 512), (0, 1001)])
+def test_ppo_update_parity(act, B):
     """R#26: one PPO minibatch on the device buffers of a rollout (critic values, normalised GAE):
     the float32 gradient (cuBLAS GEMMs + this library's kernels) vs the float64 oracle's analytic
     gradient at the same parameters on the same rows; the loss sums; the Adam step; the refreshed slab."""
     c = Case(n=30, f=3, T_data=400, N=256, H=100, seed=51)
     aws, params, actor = _actor(c, 2, 128, act=act)
-    T, B = 8, 512
+    T = 8   # B = 1001: ragged in every kernel's row blocking (8-sample head blocks, 16-row bias blocks)
     tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, critic=True)
     c.env.reset(c.starts)
     c.env.rollout(T, tr, actor=actor)
