@@ -85,11 +85,14 @@ struct ActorArgs {
     float* val_out;      // [N] critic V(s_t) = head row n (R#22), or null
     uint32_t* err;
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
+    int32_t kpb_head;            // K blocks per ring stage of the head layer (1: one 3-D box per stage)
 };
 
 struct ActorMaps {
     CUtensorMap obs;                     // 2-D bf16 [rows][k_pad], box {64, 128}
-    CUtensorMap w[ACT_MAX_LAYERS];       // 3-D bf16 [agents][out][in], box {64, BN_l, 1}
+    // 3-D bf16 [agents][out][in], box {32, BN_l, 1}; a narrow head (kpb_head > 1): 4-D view
+    // [agents][in / 32][out][32], box {32, BN_L, kpb_head, 1} — kpb_head K blocks per ring stage, one TMA
+    CUtensorMap w[ACT_MAX_LAYERS];
 };
 
 // column split of layer l: this CTA's half (rows of W_l) and the ring tile height
@@ -97,6 +100,18 @@ __host__ __device__ inline int actor_layer_out(int l, int n_layers, int hidden, 
     return l == n_layers - 1 ? n_out_pad : hidden;
 }
 __host__ __device__ inline int actor_bn(int half) { return half < ACT_BN ? half : ACT_BN; }
+// K blocks (32 wide) per ring stage of a narrow head (bn < 256 weight rows: 64 at C3): kpb blocks per 16 KB
+// stage in one 4-D TMA box keep as many bytes in flight as a wide layer's stage (the weight stream is
+// latency-bound: ~1.5K cycles per TMA round trip under load, five stages; 4 KB stages ran the C3 head at
+// ~2.2K cycles per stage).  The largest divisor of KB / 2 (own-half-first rotation) with kpb bn <= 256.
+inline int actor_kpb_head(int KB, int bn) {
+    const int kb = KB / 2;
+    int cap = ACT_BN / bn;
+    if (cap > kb) cap = kb;
+    if (cap < 1) cap = 1;
+    while (kb % cap) --cap;
+    return cap;
+}
 constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
 
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
@@ -249,6 +264,23 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     const int bn = actor_bn(half);
                     const int KB = K / ACT_BK;                                          // 32-wide K blocks
                     const int kbo = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);   // own half of h_l first
+                    if (__builtin_expect(l == a.n_layers - 1 && a.kpb_head > 1, 0)) {
+                        // narrow head: kpb_head K blocks per stage, one 4-D box (half == bn here)
+                        const int kp = a.kpb_head, ns = KB / kp;
+                        for (int j = 0; j < ns; ++j) {
+                            const int ks = (j + static_cast<int>(rank) * (ns / 2)) % ns;
+                            mbar_wait(empty_b + 8u * stage, phase ^ 1u);
+                            mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn * kp) * (ACT_BK * 2));
+                            tma_load_4d(ring_s + stage * stage_bytes, &maps.w[l], 0, static_cast<int>(rank) * half,
+                                        ks * kp, tl.agent, full_b + 8u * stage);
+                            ++seq;
+                            if (++stage == ACT_STAGES) {
+                                stage = 0;
+                                phase ^= 1u;
+                            }
+                        }
+                        continue;
+                    }
                     for (int c = 0; c < half / bn; ++c) {
                         for (int j = 0; j < KB; ++j) {
                             const int kb = (j + kbo) % KB;
@@ -299,6 +331,41 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     const int kbo = l == 0 ? 0 : static_cast<int>(rank) * na * 2;   // own atoms of h_l first
                     // phase of the atom barriers: one completion per hidden epilogue, over tiles
                     const uint32_t par = static_cast<uint32_t>(it * (a.n_layers - 1) + l - 1) & 1u;
+                    if (__builtin_expect(l == a.n_layers - 1 && a.kpb_head > 1, 0)) {
+                        // narrow head: kpb_head K blocks per stage (sub-tiles of bn x 64 B, consecutive)
+                        const int kp = a.kpb_head;
+                        const uint32_t sub16 = static_cast<uint32_t>(bn) * (ACT_BK * 2) >> 4;
+                        const uint32_t dt = tmem + (static_cast<uint32_t>(g) & 1u) * tbuf;
+                        for (int j0 = 0; j0 < KB; j0 += kp) {
+                            for (int q = 0; q < kp; ++q) {
+                                const int j = j0 + q;
+                                const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
+                                if ((j & 1) == 0) {
+                                    const int ja = j >> 1;
+                                    if (ja < na) {
+                                        mbar_wait(ownrdy_b + 8u * ja, par);
+                                    } else {
+                                        mbar_arrive_expect_tx(peerrdy_b + 8u * (ja - na), 16384u);
+                                        mbar_wait(peerrdy_b + 8u * (ja - na), par);
+                                    }
+                                    tc_fence_after();
+                                }
+                                if (q == 0) {
+                                    mbar_wait(full_b + 8u * stage, phase);
+                                    tc_fence_after();
+                                }
+                                const uint64_t ad = adesc0 + (((kb >> 1) * 16384u + (kb & 1) * 64u) >> 4);
+                                const uint64_t bd = bdesc0 + ((stage * stage_bytes) >> 4) + static_cast<uint32_t>(q) * sub16;
+                                mma_bf16(dt, ad, bd, idesc, j != 0);
+                                mma_bf16(dt, ad + 2, bd + 2, idesc, 1u);
+                            }
+                            mma_commit(empty_b + 8u * stage);
+                            if (++stage == ACT_STAGES) {
+                                stage = 0;
+                                phase ^= 1u;
+                            }
+                        }
+                    } else
                     for (int c = 0; c < half / bn; ++c) {
                         for (int j = 0; j < KB; ++j) {
                             const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;

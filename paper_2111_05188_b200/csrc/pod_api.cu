@@ -101,8 +101,8 @@ static pod_status encode_bf16(CUtensorMap* m, const void* base, int rank, const 
                               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return pod_fail(POD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-    cuuint64_t d[3], s[2];
-    cuuint32_t b[3], es[3] = {1, 1, 1};
+    cuuint64_t d[4], s[3];
+    cuuint32_t b[4], es[4] = {1, 1, 1, 1};
     for (int i = 0; i < rank; ++i) {
         d[i] = dims[i];
         b[i] = box[i];
@@ -715,15 +715,32 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             const char* pp = getenv("POD_PAIR");
             p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1' && !tr->val;   // pair kernel: no critic output
         }
+        const char* kpe = getenv("POD_KPB_HEAD");   // experiments: POD_KPB_HEAD=0 keeps one box per stage
+        const bool kpb_off = kpe && kpe[0] == '0';
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
             const int bn = p.pair ? rows / 4 : actor_bn(rows / 2);   // pair: each CTA stages half of its column half
-            const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
-                                      static_cast<uint64_t>(e->cfg.n_agents)};
-            const uint64_t str[2] = {static_cast<uint64_t>(L.w_cols[l]) * 2, actor->param_bytes};
-            const uint32_t box[3] = {ACT_BK, static_cast<uint32_t>(bn), 1};
-            st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 3, dims, str, box,
-                             CU_TENSOR_MAP_SWIZZLE_64B);
+            const int KB = L.w_cols[l] / ACT_BK;
+            const bool head = l == L.n_layers - 1;
+            // narrow head: several K blocks per ring stage (not with the multicast / pair variants)
+            const int kph = (head && !p.pair && !e->mc_ok && !kpb_off) ? actor_kpb_head(KB, bn) : 1;
+            if (head) p.aa.kpb_head = kph;
+            if (kph == 1) {
+                const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
+                                          static_cast<uint64_t>(e->cfg.n_agents)};
+                const uint64_t str[2] = {static_cast<uint64_t>(L.w_cols[l]) * 2, actor->param_bytes};
+                const uint32_t box[3] = {ACT_BK, static_cast<uint32_t>(bn), 1};
+                st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 3, dims, str,
+                                 box, CU_TENSOR_MAP_SWIZZLE_64B);
+            } else {
+                // [agents][K block][out][32]: the K-block stride is 64 bytes inside each weight row
+                const uint64_t dims[4] = {static_cast<uint64_t>(ACT_BK), static_cast<uint64_t>(rows),
+                                          static_cast<uint64_t>(KB), static_cast<uint64_t>(e->cfg.n_agents)};
+                const uint64_t str[3] = {static_cast<uint64_t>(L.w_cols[l]) * 2, ACT_BK * 2, actor->param_bytes};
+                const uint32_t box[4] = {ACT_BK, static_cast<uint32_t>(bn), static_cast<uint32_t>(kph), 1};
+                st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 4, dims, str,
+                                 box, CU_TENSOR_MAP_SWIZZLE_64B);
+            }
             if (st) return st;
         }
         ActorArgs& aa = p.aa;
