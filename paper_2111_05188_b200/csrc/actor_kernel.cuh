@@ -85,13 +85,13 @@ struct ActorArgs {
     float* val_out;      // [N] critic V(s_t) = head row n (R#22), or null
     uint32_t* err;
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
-    int32_t kpb_head;            // K blocks per ring stage of the head layer (1: one 3-D box per stage)
+    uint32_t kpb_pack;           // K blocks per ring stage of layer l in bits [5l, 5l+5) (0/1: one 3-D box)
 };
 
 struct ActorMaps {
     CUtensorMap obs;                     // 2-D bf16 [rows][k_pad], box {64, 128}
-    // 3-D bf16 [agents][out][in], box {32, BN_l, 1}; a narrow head (kpb_head > 1): 4-D view
-    // [agents][in / 32][out][32], box {32, BN_L, kpb_head, 1} — kpb_head K blocks per ring stage, one TMA
+    // 3-D bf16 [agents][out][in], box {32, BN_l, 1}; a narrow layer (kpb > 1): 4-D view
+    // [agents][in / 32][out][32], box {32, BN_l, kpb, 1} — kpb K blocks per ring stage, one TMA
     CUtensorMap w[ACT_MAX_LAYERS];
 };
 
@@ -100,14 +100,16 @@ __host__ __device__ inline int actor_layer_out(int l, int n_layers, int hidden, 
     return l == n_layers - 1 ? n_out_pad : hidden;
 }
 __host__ __device__ inline int actor_bn(int half) { return half < ACT_BN ? half : ACT_BN; }
-// K blocks (32 wide) per ring stage of a narrow head (bn < 256 weight rows: 64 at C3): kpb blocks per 16 KB
-// stage in one 4-D TMA box keep as many bytes in flight as a wide layer's stage (the weight stream is
-// latency-bound: ~1.5K cycles per TMA round trip under load, five stages; 4 KB stages ran the C3 head at
-// ~2.2K cycles per stage).  The largest divisor of KB / 2 (own-half-first rotation) with kpb bn <= 256.
-inline int actor_kpb_head(int KB, int bn) {
-    const int kb = KB / 2;
+// K blocks (32 wide) per ring stage of a narrow layer (bn < 256 weight rows: the C3 head, every C2 layer):
+// kpb blocks per 16 KB stage in one 4-D TMA box keep as many bytes in flight as a wide layer's stage (the
+// weight stream is latency-bound: ~1.5K cycles per TMA round trip under load, five stages; 4 KB stages
+// ran the C3 head at ~2.2K cycles per stage).  The largest divisor of KB (of KB / 2 under the
+// own-half-first rotation of layers l > 0) with kpb bn <= 256; at most 31 (5-bit field).
+inline int actor_kpb(int KB, int bn, bool rotated) {
+    const int kb = rotated ? KB / 2 : KB;
     int cap = ACT_BN / bn;
     if (cap > kb) cap = kb;
+    if (cap > 31) cap = 31;
     if (cap < 1) cap = 1;
     while (kb % cap) --cap;
     return cap;
@@ -264,11 +266,13 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     const int bn = actor_bn(half);
                     const int KB = K / ACT_BK;                                          // 32-wide K blocks
                     const int kbo = l == 0 ? 0 : static_cast<int>(rank) * (KB / 2);   // own half of h_l first
-                    if (__builtin_expect(l == a.n_layers - 1 && a.kpb_head > 1, 0)) {
-                        // narrow head: kpb_head K blocks per stage, one 4-D box (half == bn here)
-                        const int kp = a.kpb_head, ns = KB / kp;
+                    const int kp = static_cast<int>((a.kpb_pack >> (5 * l)) & 31u);
+                    if (__builtin_expect(kp > 1, 0)) {
+                        // narrow layer: kp K blocks per stage, one 4-D box (half == bn here)
+                        const int ns = KB / kp;
+                        const int kso = l == 0 ? 0 : static_cast<int>(rank) * (ns / 2);
                         for (int j = 0; j < ns; ++j) {
-                            const int ks = (j + static_cast<int>(rank) * (ns / 2)) % ns;
+                            const int ks = (j + kso) % ns;
                             mbar_wait(empty_b + 8u * stage, phase ^ 1u);
                             mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn * kp) * (ACT_BK * 2));
                             tma_load_4d(ring_s + stage * stage_bytes, &maps.w[l], 0, static_cast<int>(rank) * half,
@@ -331,16 +335,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     const int kbo = l == 0 ? 0 : static_cast<int>(rank) * na * 2;   // own atoms of h_l first
                     // phase of the atom barriers: one completion per hidden epilogue, over tiles
                     const uint32_t par = static_cast<uint32_t>(it * (a.n_layers - 1) + l - 1) & 1u;
-                    if (__builtin_expect(l == a.n_layers - 1 && a.kpb_head > 1, 0)) {
-                        // narrow head: kpb_head K blocks per stage (sub-tiles of bn x 64 B, consecutive)
-                        const int kp = a.kpb_head;
+                    const int kp = static_cast<int>((a.kpb_pack >> (5 * l)) & 31u);
+                    if (__builtin_expect(kp > 1, 0)) {
+                        // narrow layer: kp K blocks per stage (sub-tiles of bn x 64 B, consecutive)
                         const uint32_t sub16 = static_cast<uint32_t>(bn) * (ACT_BK * 2) >> 4;
                         const uint32_t dt = tmem + (static_cast<uint32_t>(g) & 1u) * tbuf;
                         for (int j0 = 0; j0 < KB; j0 += kp) {
                             for (int q = 0; q < kp; ++q) {
                                 const int j = j0 + q;
                                 const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
-                                if ((j & 1) == 0) {
+                                if (l > 0 && (j & 1) == 0) {
                                     const int ja = j >> 1;
                                     if (ja < na) {
                                         mbar_wait(ownrdy_b + 8u * ja, par);

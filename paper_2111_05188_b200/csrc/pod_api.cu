@@ -715,16 +715,15 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             const char* pp = getenv("POD_PAIR");
             p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1' && !tr->val;   // pair kernel: no critic output
         }
-        const char* kpe = getenv("POD_KPB_HEAD");   // experiments: POD_KPB_HEAD=0 keeps one box per stage
+        const char* kpe = getenv("POD_KPB");   // experiments: POD_KPB=0 keeps one box per stage
         const bool kpb_off = kpe && kpe[0] == '0';
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
             const int bn = p.pair ? rows / 4 : actor_bn(rows / 2);   // pair: each CTA stages half of its column half
             const int KB = L.w_cols[l] / ACT_BK;
-            const bool head = l == L.n_layers - 1;
-            // narrow head: several K blocks per ring stage (not with the multicast / pair variants)
-            const int kph = (head && !p.pair && !e->mc_ok && !kpb_off) ? actor_kpb_head(KB, bn) : 1;
-            if (head) p.aa.kpb_head = kph;
+            // narrow layers: several K blocks per ring stage (not with the multicast / pair variants)
+            const int kph = (bn < ACT_BN && !p.pair && !e->mc_ok && !kpb_off) ? actor_kpb(KB, bn, l > 0) : 1;
+            p.aa.kpb_pack |= static_cast<uint32_t>(kph) << (5 * l);
             if (kph == 1) {
                 const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
                                           static_cast<uint64_t>(e->cfg.n_agents)};
