@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     tc_fence_before();
     cluster_sync_all();          // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
+    // the env-step grid that follows may be scheduled now (its blocks stage their inputs on free SMs and
+    // wait for this grid's completion before reading the actions); a no-op without a dependent
+    if (threadIdx.x == 0) pdl_launch_dependents();
     const uint32_t tmem = *tslot;
     unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 64 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = clock64();

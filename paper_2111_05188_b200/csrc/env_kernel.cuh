@@ -81,6 +81,7 @@ struct EnvArgs {
     double* dbg_cash;         // [N] slice or null
     double* equity;           // [N] slice of step t: v_{t+1} before any reset, or null
     uint32_t* err;
+    int32_t pdl;              // 1: launched as a programmatic dependent of the actor (see the kernel)
 };
 
 struct EnvMaps {
@@ -155,12 +156,16 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
         for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(chunk_bar + 8u * c, 32);
         if (!tma) fence_mbar_init();
     }
+    // Launched as a programmatic dependent of the actor (when a.pdl): everything up to the actions
+    // (holdings, ledger state, market rows, tile constants) is loaded while the actor grid is still
+    // running; griddepcontrol.wait precedes the first read of the actor's outputs (the actions) and the
+    // first write the actor could observe (the next step's noise).
     if (tma && tid == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(n) * (stepping ? 192u : 128u));
         tma_load_2d(smem_u32(hold_s), &maps.hold, tile * 32, 0, bar);
-        if (stepping) tma_load_2d(smem_u32(aint_s), &maps.aint, tile * 32, 0, bar);
+        if (stepping && !a.pdl) tma_load_2d(smem_u32(aint_s), &maps.aint, tile * 32, 0, bar);
     }
     // per-env ledger state (warp 0 owns the ledger)
     double cash0 = 0.0, v0 = 0.0, disc0 = 0.0;
@@ -181,7 +186,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     if (need_hold && !tma) {   // ragged tile: cooperative plain loads
         for (int i = warp; i < n; i += 4) {
             hold_s[i * 32 + lane] = active ? a.hold[i * N + e] : 0;
-            if (stepping) aint_s[i * 32 + lane] = active ? a.aint[i * N + e] : 0;
+            if (stepping && !a.pdl) aint_s[i * 32 + lane] = active ? a.aint[i * N + e] : 0;
         }
     }
     // ---- 2. market rows: every thread issues all of its loads before using any
@@ -226,6 +231,14 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             tmpl[c] = f2bf(p / p_0[i]);
         } else if (c >= a.obs_dim || c < 1 + n) {
             tmpl[c] = 0;
+        }
+    }
+    if (a.pdl) {
+        pdl_wait();
+        if (stepping) {
+            if (tma && tid == 0) tma_load_2d(smem_u32(aint_s), &maps.aint, tile * 32, 0, bar);
+            if (!tma)
+                for (int i = warp; i < n; i += 4) aint_s[i * 32 + lane] = active ? a.aint[i * N + e] : 0;
         }
     }
     if (tma) mbar_wait(bar, 0);

@@ -251,6 +251,7 @@ struct pod_env {
     uint64_t use_clock;
     bool use_graphs;
     int persist;                // persistent actor clusters (POD_PERSIST=0 turns it off)
+    int pdl;                    // env step as a programmatic dependent of the actor (POD_PDL=0 turns it off)
     int sm_count;
     int profile;                // 0 = off, k = bracket every k-th step
     unsigned long long* trace;  // diagnostics: actor clock64 stamps of the last launch
@@ -375,6 +376,8 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     {
         const char* ps = getenv("POD_PERSIST");
         e->persist = !(ps && ps[0] == '0');
+        const char* pd = getenv("POD_PDL");
+        e->pdl = !(pd && pd[0] == '0');
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -559,6 +562,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
                                      cudaEventRecordExternal);
     };
     const int sampling = (!p.injected && !p.aa.deterministic) ? 1 : 0;
+    int actor_ctas = 0;   // CTAs of the last actor launch (SMs it occupies)
     auto launch_actor = [&](ActorArgs& aa) {
         // one 2-CTA cluster per 128-env tile (column split of every layer)
         cudaLaunchConfig_t lc{};
@@ -571,6 +575,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         // weight stages load while the current tile's head runs (multi-wave batches)
         const int ncl = (!aa.mc && !p.pair && e->persist) ? std::min(mtiles, e->sm_count / 2) : mtiles;
         lc.gridDim = dim3(static_cast<unsigned>(2 * ncl));
+        actor_ctas = 2 * ncl * ((aa.mc || p.pair) ? 2 : 1);
         lc.blockDim = dim3(ACT_THREADS);
         lc.dynamicSmemBytes = p.actor_smem;
         lc.stream = s;
@@ -623,7 +628,32 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         a.equity = tr->equity ? tr->equity + static_cast<int64_t>(t) * N : nullptr;
         a.gen_noise = (sampling && t + 1 < T) ? 1 : 0;   // noise for the actor launch of step t+1
         a.noise_t = t + 1;
-        env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+        // Programmatic dependent of the actor launch just before (not across a profiling event node):
+        // its blocks are scheduled as SMs free up, the first ones on the SMs the actor leaves idle.
+        // Used when that helps: a dense launch (>= 7 tiles per SM: the launch latency is hidden as actor
+        // CTAs exit) or a small one whose tiles fit two per idle SM (C2); not when a few idle SMs would
+        // collect a dense, slow cluster of tiles ahead of the rest (C3: 20 idle SMs, 256 tiles).
+        const int tiles = t1 - t0;
+        const int idle_sms = std::max(0, e->sm_count - actor_ctas);
+        const bool dense = tiles >= 7 * e->sm_count;
+        const bool roomy = 2 * idle_sms >= tiles;
+        const bool pdl = e->pdl && !p.injected && (dense || roomy) && !(prof && t % prof->stride == 0);
+        if (pdl) {
+            a.pdl = 1;
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(static_cast<unsigned>(t1 - t0));
+            lc.blockDim = dim3(ENV_THREADS);
+            lc.dynamicSmemBytes = static_cast<size_t>(env_smem(e));
+            lc.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            cudaLaunchKernelEx(&lc, env_step_kernel, e->env_maps, a);
+        } else {
+            env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+        }
         mark(t, 3);
     }
     if (!p.injected && tr->val) {
