@@ -396,8 +396,7 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
-        ce = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  env_smem_bytes(ENV_MAX_STOCKS, ENV_MAX_KPAD));
+        ce = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(gae_smem_bytes()));
@@ -503,7 +502,11 @@ static EnvArgs env_args(const pod_env* e, int mode) {
 
 static inline int env_blocks(const pod_env* e) { return e->n_tiles; }
 static inline size_t env_smem(const pod_env* e) {
-    return static_cast<size_t>(env_smem_bytes(e->cfg.n_stocks, e->k_pad));
+    static const size_t over = [] {   // experiments: POD_ENV_SMEM=<bytes> raises the request (fewer tiles per SM)
+        const char* v = getenv("POD_ENV_SMEM");
+        return v ? static_cast<size_t>(atol(v)) : 0;
+    }();
+    return std::max(static_cast<size_t>(env_smem_bytes(e->cfg.n_stocks, e->k_pad)), over);
 }
 
 static uint64_t splitmix64(uint64_t& x) {
