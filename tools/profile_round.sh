@@ -7,6 +7,7 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt
 timeout 900 python bench.py > $OUT/bench_c3.json 2> $OUT/bench_c3.err; echo "C3 exit $?"
 timeout 600 python bench.py --config C2 > $OUT/bench_c2.json 2> $OUT/bench_c2.err; echo "C2 exit $?"
+timeout 600 python bench.py --config C4 --no-cpu-baseline > $OUT/bench_c4.json 2> $OUT/bench_c4.err; echo "C4 exit $?"
 timeout 900 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "C5 exit $?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "REF exit $?"
 CMD="python bench.py --T 8 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --profile-stride 0 --tdata 100000"
