@@ -328,9 +328,10 @@ pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, i
  *   pod_ppo_workspace_size (the last 256 bytes hold the device Adam step base).
  * The minibatch loop is captured into a CUDA graph on the first call with a
  * given argument set (all pointers, sizes and hyper-parameters; adam_t and the
- * stream excepted) and replayed by later calls (library-owned, 4 per thread,
+ * stream excepted) and replayed by later calls (library-owned, 16 per thread,
  * least recently used evicted); the calling thread's first call also creates
- * its cuBLAS handle and a 32 MiB cuBLAS workspace (the only allocations).
+ * its cuBLAS handle (the only allocation).  cuBLAS scratch lives in `ws`, so
+ * learners with distinct buffers may run concurrently on different streams.
  * POD_PPO_GRAPH=0 launches eagerly instead.  Stream-ordered.  Errors: ARG, SHAPE, UNSUPPORTED, CUDA. */
 pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, int32_t act,
                           const pod_ppo_hparams* hp, float* master, float* adam_m, float* adam_v, int64_t adam_t,

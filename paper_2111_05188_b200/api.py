@@ -301,7 +301,11 @@ class PPOLearner:
         """obs bf16 [M, k_pad], act_raw f32 [M, n], logp_old/adv/ret f32 [M], perm i32 [n_mb * batch]."""
         M = obs.shape[0]
         n_mb = perm.numel() // self.batch
-        self.losses.zero_()
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                self.losses.zero_()
+        else:
+            self.losses.zero_()
         check(load().pod_ppo_update(C.byref(self.cfg), self.n_hidden, self.hidden, self.act, C.byref(self.hp),
                                     _ptr(self.master), _ptr(self.m), _ptr(self.v), self.t, _ptr(self.params),
                                     self.params.shape[1], _ptr(obs), _ptr(act_raw), _ptr(logp_old), _ptr(adv),

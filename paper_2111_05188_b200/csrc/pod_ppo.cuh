@@ -10,8 +10,11 @@
 
 namespace pod {
 
+constexpr size_t kPpoCublasWs = 32u << 20;
+constexpr size_t kPpoGraphCache = 16;   // captured minibatch loops kept per thread (e.g. one per pod learner)
+
 struct PpoWs {
-    size_t x0, h, zf, zh, d0, b0, b1, act, lpo, adv, ret, grad, step, total;
+    size_t x0, h, zf, zh, d0, b0, b1, act, lpo, adv, ret, grad, step, cublas, total;
 };
 
 inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, int B, int n) {
@@ -32,22 +35,21 @@ inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, 
     w.ret = o; o += up(sizeof(float) * B);
     w.grad = o; o += up(sizeof(float) * L.n_elems);
     w.step = o; o += 256;                                                            // int64 Adam step base
+    w.cublas = o; o += kPpoCublasWs;                     // this call's cuBLAS workspace (concurrent learners)
     w.total = o;
     return w;
 }
 
-// one cuBLAS handle per thread and device, with an explicit workspace (no allocation under graph capture)
+// one cuBLAS handle per thread and device; each call points it at the workspace inside its own `ws`
+// (no allocation under graph capture, and learners replayed concurrently on different streams do not
+// share cuBLAS scratch)
 inline cublasHandle_t ppo_cublas() {
     static thread_local cublasHandle_t h = nullptr;
     static thread_local int dev = -1;
-    static thread_local void* cws = nullptr;
     int d = 0;
     cudaGetDevice(&d);
     if (!h || d != dev) {
         if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-        constexpr size_t kWs = 32u << 20;
-        if (cudaMalloc(&cws, kWs) != cudaSuccess) return nullptr;
-        if (cublasSetWorkspace(h, cws, kWs) != CUBLAS_STATUS_SUCCESS) return nullptr;
         dev = d;
     }
     return h;
@@ -134,7 +136,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     if (st) return st;
     cudaStream_t user_s = static_cast<cudaStream_t>(stream);
     cublasHandle_t cb = ppo_cublas();
-    if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate / workspace failed");
+    if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate failed");
     char* w = static_cast<char*>(ws);
     int64_t* step_slot = reinterpret_cast<int64_t*>(w + W.step);
     __nv_bfloat16* x0 = reinterpret_cast<__nv_bfloat16*>(w + W.x0);
@@ -199,6 +201,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     // the minibatch loop, enqueued on stream s (captured below, or eager with POD_PPO_GRAPH=0)
     auto enqueue = [&](cudaStream_t s) -> pod_status {
     POD_CUBLAS(cublasSetStream(cb, s));
+    POD_CUBLAS(cublasSetWorkspace(cb, w + W.cublas, kPpoCublasWs));
     for (int j = 0; j < n_minibatches; ++j) {
         ppo_gather_kernel<<<B, 128, 0, s>>>(obs, act_raw, logp_old, adv, ret, perm + static_cast<int64_t>(j) * B, B,
                                             L.k_pad, n, reinterpret_cast<uint16_t*>(x0), act_b, lpo_b, adv_b, ret_b);
@@ -302,7 +305,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         ce = cudaGraphInstantiate(&exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "PPO graph instantiate: %s", cudaGetErrorString(ce));
-        if (cache.size() >= 4) {   // evict the least recently used
+        if (cache.size() >= kPpoGraphCache) {   // evict the least recently used
             size_t victim = 0;
             for (size_t i = 1; i < cache.size(); ++i)
                 if (cache[i].used < cache[victim].used) victim = i;

@@ -638,6 +638,49 @@ def test_ppo_graph_replay_step_counter():
     assert off[moved].mean() < 0.01, off[moved].mean()
 
 
+def test_ppo_concurrent_learners_on_streams():
+    """Two learners (distinct buffers, own cuBLAS scratch inside their workspaces) replayed concurrently on
+    two streams reach the same parameters as each run alone (float atomics in the reductions: float32-level
+    agreement; any sharing of scratch between the concurrent graphs would show as gross differences)."""
+    c = Case(n=30, f=3, T_data=400, N=256, H=100, seed=54)
+    aws, params, actor = _actor(c, 2, 128)
+    T, B = 8, 512
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, critic=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    adv, ret = api.pod_gae(tr.rew, tr.val[:T].contiguous(), tr.done, tr.val[T].contiguous(), 0.99, 0.95,
+                           normalize=True)
+    M = T * c.N
+    args = (tr.obs[:T].reshape(M, c.k_pad), tr.act.reshape(M, c.n), tr.logp.reshape(M), adv.reshape(M), ret.reshape(M))
+    perms = [torch.from_numpy(np.random.default_rng(20 + k).permutation(M)[: 4 * B].astype(np.int32)).cuda()
+             for k in range(2)]
+
+    def learners():
+        return [api.PPOLearner(c.cfg, 2, 128, params.clone(), batch=B, learning_rate=1e-3) for _ in range(2)]
+
+    solo = learners()
+    for k in range(2):
+        solo[k].update(*args, perms[k])
+        torch.cuda.synchronize()
+    conc = learners()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    main = torch.cuda.current_stream()
+    for rep in range(2):   # the second round replays the captured graphs concurrently
+        for k in range(2):
+            streams[k].wait_stream(main)
+            conc[k].update(*args, perms[k], stream=streams[k])
+        for k in range(2):
+            main.wait_stream(streams[k])
+        if rep == 0:
+            for k in range(2):
+                solo[k].update(*args, perms[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        a, b = conc[k].master.cpu().numpy(), solo[k].master.cpu().numpy()
+        assert np.isfinite(a).all()
+        assert (np.abs(a - b) > 1e-2 * 1e-3).mean() < 0.01
+
+
 # ----------------------------------------------------------------- shape sweep (edge configurations)
 @pytest.mark.parametrize("n,f,N,nh,hid,act,agents,h_max,cost", [
     (1, 3, 1, 1, 128, 0, 1, 100, 0.002),      # one stock, one env (a 1-lane ragged tile)

@@ -19,5 +19,5 @@ for K in actor_forward env_step gae; do
   ncu --set full --clock-control none --import-source on -k regex:$K -s $SKIP -c 1 -o $OUT/prof_$K $CMD > $OUT/ncu_$K.log 2>&1
   echo "ncu $K exit $?"
 done
-timeout 300 python tools/bench_ppo.py > $OUT/ppo_bench.json 2> $OUT/ppo_bench.err; echo "ppo exit $?"
+timeout 300 python tools/bench_ppo.py --pods 8 > $OUT/ppo_bench.json 2> $OUT/ppo_bench.err; echo "ppo exit $?"
 timeout 300 python tools/bench_fuse.py > $OUT/fuse_bench.json 2> $OUT/fuse_bench.err; echo "fuse exit $?"
