@@ -67,7 +67,7 @@ struct ActorArgs {
     int32_t obs_row0;        // row of obs[t][0] in the obs tensor map = t * N
     int32_t mtile0;          // first 128-env M-tile of this launch (env groups)
     int32_t mtiles;          // M-tiles of this launch; cluster c processes mtile0 + c, + c + nclusters, ...
-    int32_t mc;              // 1: 4-CTA clusters (2 M-tiles) share weight tiles by TMA multicast
+    int32_t mc;              // 0, or G = 2 / 4: clusters of 2G CTAs (G M-tiles) share weight tiles by TMA multicast
     int32_t value_only;      // 1: only the critic V (head row n) is written (bootstrap pass over obs[T])
     uint64_t seed;
     int64_t env_offset;
@@ -167,7 +167,11 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t peer = cr ^ 1u;                      // same M-tile, other column half
     const uint32_t partner = cr ^ 2u;                   // other M-tile, same column half (a.mc)
     const uint16_t pair_mask = static_cast<uint16_t>((1u << cr) | (1u << peer));
-    const uint16_t share_mask = static_cast<uint16_t>((1u << cr) | (1u << partner));
+    uint16_t share_mask = static_cast<uint16_t>((1u << cr) | (1u << partner));
+    if (a.mc > 2) {   // every CTA of this column half in the cluster
+        share_mask = 0;
+        for (int gq = 0; gq < a.mc; ++gq) share_mask |= static_cast<uint16_t>(1u << (2 * gq + rank));
+    }
     const int ka = (a.k_pad > a.hidden ? a.k_pad : a.hidden) / 64;   // activation atoms
     const uint32_t act_s = base_u32;                                  // ka * 16 KB
     const uint32_t ring_s = act_s + ka * 16384u;
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
         if (lane == 0) {
             for (int s = 0; s < ACT_STAGES; ++s) {
                 mbar_init(full_b + 8u * s, 1);
-                mbar_init(empty_b + 8u * s, a.mc ? 2 : 1);   // both consumers of a shared tile
+                mbar_init(empty_b + 8u * s, a.mc ? a.mc : 1);   // every consumer of a shared tile
             }
             mbar_init(obs_b, 1);
             mbar_init(accum_b, 2);        // one multicast commit from each CTA of the pair
@@ -296,8 +300,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                             if (!a.mc) {
                                 tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
                                             static_cast<int>(rank) * half + c * bn, tl.agent, full_b + 8u * stage);
-                            } else if ((seq & 1) == static_cast<int>(cr >> 1)) {
-                                // alternate tiles: this CTA fetches it for itself and its partner
+                            } else if ((seq & (a.mc - 1)) == static_cast<int>(cr >> 1)) {
+                                // round robin over the M-tiles: this CTA fetches the stage for all of them
                                 tma_load_3d_mc(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
                                                static_cast<int>(rank) * half + c * bn, tl.agent, full_b + 8u * stage,
                                                share_mask);

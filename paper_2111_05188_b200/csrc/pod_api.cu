@@ -355,8 +355,9 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         if (e->per_agent % 128 != 0) G = 1;
         // weight-tile multicast across 2 M-tiles: measured no faster (the fills are limited by
         // shared-memory bandwidth under SS-mode MMAs, not by L2), so opt-in only
-        const char* mcs = getenv("POD_MULTICAST");
-        e->mc_ok = (e->per_agent % 256 == 0 && mcs && mcs[0] == '1') ? 1 : 0;
+        const char* mcs = getenv("POD_MULTICAST");   // 1 or 2: pairs of M-tiles, 4: quads (8-CTA clusters)
+        const int mcg = mcs ? (atoi(mcs) == 4 ? 4 : (atoi(mcs) >= 1 ? 2 : 0)) : 0;
+        e->mc_ok = (mcg && e->per_agent % (128 * mcg) == 0) ? mcg : 0;
         // boundaries in units of M-tile pairs when agents fill pairs (the 2-SM actor needs them)
         const int unit = (e->per_agent % 256 == 0) ? 2 : 1;
         const int units = (mt + unit - 1) / unit;
@@ -572,19 +573,19 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
         // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
         // every agent has an even number of full M-tiles and so does this launch
-        aa.mc = (!p.pair && e->mc_ok && mtiles % 2 == 0 && m0 % 2 == 0) ? 1 : 0;
+        aa.mc = (!p.pair && e->mc_ok && mtiles % e->mc_ok == 0 && m0 % e->mc_ok == 0) ? e->mc_ok : 0;
         aa.mtiles = mtiles;
         // persistent clusters (one per SM pair) loop over the M-tiles: the next tile's obs and first
         // weight stages load while the current tile's head runs (multi-wave batches)
         const int ncl = (!aa.mc && !p.pair && e->persist) ? std::min(mtiles, e->sm_count / 2) : mtiles;
         lc.gridDim = dim3(static_cast<unsigned>(2 * ncl));
-        actor_ctas = 2 * ncl * ((aa.mc || p.pair) ? 2 : 1);
+        actor_ctas = 2 * ncl;
         lc.blockDim = dim3(ACT_THREADS);
         lc.dynamicSmemBytes = p.actor_smem;
         lc.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (aa.mc || p.pair) ? 4 : 2;
+        at[0].val.clusterDim.x = aa.mc ? 2 * aa.mc : (p.pair ? 4 : 2);
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
