@@ -641,7 +641,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         const int idle_sms = std::max(0, e->sm_count - actor_ctas);
         const bool dense = tiles >= 7 * e->sm_count;
         const bool roomy = 2 * idle_sms >= tiles;
-        const bool pdl = e->pdl && !p.injected && (dense || roomy) && !(prof && t % prof->stride == 0);
+        const bool pdl = e->pdl && e->groups == 1 && !p.injected && (dense || roomy) && !(prof && t % prof->stride == 0);
         if (pdl) {
             a.pdl = 1;
             cudaLaunchConfig_t lc{};
