@@ -299,14 +299,24 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 const int i1 = i0 + CH < n ? i0 + CH : n;
                 const double cash_c0 = cash;
                 bool unsure = false;
+                // one-deep prefetch: ticker i+1's shared-memory operands are loaded before ticker i's
+                // holdings store (which would otherwise keep the compiler from hoisting them)
+                int ai_n = aint_s[i0 * 32 + lane], h_n = hold_s[i0 * 32 + lane];
+                double un_n = unit_s[i0], rc_n = rcp_s[i0];
 #pragma unroll 4
                 for (int i = i0; i < i1; ++i) {
-                    const int ai = aint_s[i * 32 + lane];
-                    int h = hold_s[i * 32 + lane];
+                    const int ai = ai_n;
+                    int h = h_n;
+                    const double unit = un_n, rcp = rc_n;
+                    if (i + 1 < i1) {
+                        ai_n = aint_s[(i + 1) * 32 + lane];
+                        h_n = hold_s[(i + 1) * 32 + lane];
+                        un_n = unit_s[i + 1];
+                        rc_n = rcp_s[i + 1];
+                    }
                     if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
-                    const double unit = unit_s[i];
                     const double ad = static_cast<double>(ai > 0 ? ai : 0);
-                    const double y = __dmul_rn(cash, rcp_s[i]);
+                    const double y = __dmul_rn(cash, rcp);
                     const double fl = floor(y);
                     const double qd = fl < ad ? fl : ad;
                     const double cost = __dmul_rn(qd, unit);
