@@ -16,6 +16,7 @@
 
 #include "actor_kernel.cuh"
 #include "actor_pair_kernel.cuh"
+#include "actor_wide_kernel.cuh"
 #include "env_kernel.cuh"
 #include "fuse_kernel.cuh"
 #include "metrics_kernel.cuh"
@@ -397,6 +398,8 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(actor_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -545,6 +548,7 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
 struct RolloutPlan {
     bool injected;
     bool pair;          // 4-CTA clusters with the 2-SM MMA (per-agent env count a multiple of 256)
+    bool wide;          // 2-CTA clusters with the 2-SM MMA, no column split (actor_wide_kernel.cuh)
     ActorMaps maps;
     ActorArgs aa;
     size_t actor_smem;
@@ -578,8 +582,8 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         // persistent clusters (one per SM pair) loop over the M-tiles: the next tile's obs and first
         // weight stages load while the current tile's head runs (multi-wave batches)
         const int ncl = (!aa.mc && !p.pair && e->persist) ? std::min(mtiles, e->sm_count / 2) : mtiles;
-        lc.gridDim = dim3(static_cast<unsigned>(2 * ncl));
-        actor_ctas = 2 * ncl;
+        lc.gridDim = dim3(static_cast<unsigned>(p.wide ? mtiles : 2 * ncl));   // wide: one CTA per M-tile
+        actor_ctas = static_cast<int>(lc.gridDim.x);
         lc.blockDim = dim3(ACT_THREADS);
         lc.dynamicSmemBytes = p.actor_smem;
         lc.stream = s;
@@ -590,7 +594,9 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        if (p.pair)
+        if (p.wide)
+            cudaLaunchKernelEx(&lc, actor_wide_kernel, p.maps, aa);
+        else if (p.pair)
             cudaLaunchKernelEx(&lc, actor_pair_kernel, p.maps, aa);
         else
             cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
@@ -748,15 +754,19 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             // epilogue/synchronisation currently costs more than it saves (measured)
             const char* pp = getenv("POD_PAIR");
             p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1' && !tr->val;   // pair kernel: no critic output
+            const char* pw = getenv("POD_WIDE");
+            p.wide = !p.pair && !e->mc_ok && e->groups == 1 && pw && pw[0] == '1' &&
+                     actor_wide_ok(e->per_agent, actor->n_hidden, actor->hidden, L.n_out_pad);
         }
         const char* kpe = getenv("POD_KPB");   // experiments: POD_KPB=0 keeps one box per stage
         const bool kpb_off = kpe && kpe[0] == '0';
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
-            const int bn = p.pair ? rows / 4 : actor_bn(rows / 2);   // pair: each CTA stages half of its column half
+            // pair: each CTA stages half of its column half; wide: half of each <= 256-row chunk
+            const int bn = p.pair ? rows / 4 : (p.wide ? actor_wide_cw(rows) / 2 : actor_bn(rows / 2));
             const int KB = L.w_cols[l] / ACT_BK;
             // narrow layers: several K blocks per ring stage (not with the multicast / pair variants)
-            const int kph = (bn < ACT_BN && !p.pair && !e->mc_ok && !kpb_off) ? actor_kpb(KB, bn, l > 0) : 1;
+            const int kph = (bn < ACT_BN && !p.pair && !p.wide && !e->mc_ok && !kpb_off) ? actor_kpb(KB, bn, l > 0) : 1;
             p.aa.kpb_pack |= static_cast<uint32_t>(kph) << (5 * l);
             if (kph == 1) {
                 const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
@@ -799,7 +809,9 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         aa.znoise = e->znoise;
         aa.err = e->err;
         aa.trace = e->trace;
-        p.actor_smem = p.pair ? actor_pair_smem_bytes(L.k_pad, actor->hidden) : actor_smem_bytes(L.k_pad, actor->hidden);
+        p.actor_smem = p.wide   ? actor_wide_smem_bytes(L.k_pad, actor->hidden)
+                       : p.pair ? actor_pair_smem_bytes(L.k_pad, actor->hidden)
+                                : actor_smem_bytes(L.k_pad, actor->hidden);
         if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
     }
     if (!e->use_graphs) {
