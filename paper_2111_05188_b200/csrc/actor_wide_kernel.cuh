@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 const int KB = K / ACT_BK;
                 const uint32_t par = static_cast<uint32_t>(l - 1) & 1u;
                 // h_l atoms whose TMEM columns (of layer l-1) the first chunk overwrites
-                const int first = (cw / 64 < na) ? cw / 64 : na;
+                const int first = ((cw + 63) / 64 < na) ? (cw + 63) / 64 : na;   // >= 1 (narrow heads too)
                 if (tr) tr[2 + 4 * l] = clock64();
                 for (int c = 0; c < out / cw; ++c) {
                     for (int j = 0; j < KB; ++j) {

@@ -9,6 +9,8 @@ against the oracle's Philox/Box–Muller and map.
 """
 import math
 
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -679,6 +681,31 @@ def test_ppo_concurrent_learners_on_streams():
         a, b = conc[k].master.cpu().numpy(), solo[k].master.cpu().numpy()
         assert np.isfinite(a).all()
         assert (np.abs(a - b) > 1e-2 * 1e-3).mean() < 0.01
+
+
+@pytest.mark.parametrize("hidden", [512, 128])
+def test_wide_actor_matches_column_split(tmp_path, hidden):
+    """The opt-in 2-SM wide actor (POD_WIDE=1, actor_wide_kernel) against the default column-split actor
+    on the same seeded step (each process reads the switch at plan time): mu and V agree to bf16-level
+    accumulation differences (different K order inside the float32 accumulators), logp likewise.  The
+    narrow head (n_out_pad = 32 < one 64-column atom) once raced its first atom: caught here."""
+    import os
+    import subprocess
+
+    outs = {}
+    for flag in ("0", "1"):
+        path = tmp_path / f"wide{flag}.npz"
+        env = dict(os.environ, POD_WIDE=flag)
+        subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "wide_actor_run.py"), str(path),
+                        str(hidden)],
+                       check=True, env=env, cwd=os.path.dirname(os.path.dirname(__file__)), timeout=300)
+        outs[flag] = np.load(path)
+    for k in ("mu", "val"):
+        a, b = outs["0"][k].astype(np.float64), outs["1"][k].astype(np.float64)
+        scale = np.abs(a).max() + 1e-12
+        assert np.abs(a - b).max() <= 1e-2 * scale, (k, np.abs(a - b).max() / scale)
+    la, lb = outs["0"]["logp"].astype(np.float64), outs["1"]["logp"].astype(np.float64)
+    assert np.abs(la - lb).max() <= 1e-4 * np.abs(la).max()
 
 
 # ----------------------------------------------------------------- shape sweep (edge configurations)
