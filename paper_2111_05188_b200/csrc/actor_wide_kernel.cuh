@@ -186,6 +186,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 if (tr) tr[3 + 4 * l] = clock64();
                 mma_commit_cta2_mc(accum_b, pair_mask);
             }
+        } else if (lane == 0) {
+            // non-leader: forward "atom j of h_l written here" to the leader's MMA issuer, so no epilogue
+            // thread blocks on the whole-CTA barrier
+            for (int l = 1; l < a.n_layers; ++l) {
+                const uint32_t par = static_cast<uint32_t>(l - 1) & 1u;
+                for (int j = 0; j < na; ++j) {
+                    mbar_wait(ownrdy_b + 8u * j, par);
+                    mbar_arrive_remote(mapa_shared(ownpair_b + 8u * j, 0));
+                }
+            }
         }
         __syncwarp();
     } else {
@@ -229,11 +239,15 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             mbar_wait_cluster(accum_b, static_cast<uint32_t>(l) & 1u);   // the pair's MMAs of layer l are done
             tc_fence_after();
             if (tr && etid == 0) tr[4 + 4 * l] = clock64();
+            // TMEM loads one atom ahead: atom j+1's tcgen05.ld is in flight while atom j is packed
+            // and stored (tcgen05.wait::ld waits for every outstanding load, so it is issued after the
+            // wait for atom j)
+            uint32_t v[32], vn[32];
+            tmem_ld32(trow + static_cast<uint32_t>(hh * 32), v);
             for (int j = 0; j < na; ++j) {
                 const int tc = j * 64 + hh * 32;
-                uint32_t v[32];
-                tmem_ld32(trow + static_cast<uint32_t>(tc), v);
                 tmem_ld_wait();
+                if (j + 1 < na) tmem_ld32(trow + static_cast<uint32_t>(tc + 64), vn);
                 const float4* b4 = reinterpret_cast<const float4*>(bias_s + boff + tc);
                 uint32_t pk[16];
                 epi_pack(v, b4, a.act, pk);
@@ -245,11 +259,10 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 fence_proxy_async_smem();
                 tc_fence_before();
                 mbar_arrive(ownrdy_b + 8u * j);
-                if (etid == 0 && !is_leader) {
-                    mbar_wait(ownrdy_b + 8u * j, static_cast<uint32_t>(l) & 1u);
-                    mbar_arrive_remote(mapa_shared(ownpair_b + 8u * j, 0));
-                }
+#pragma unroll
+                for (int q = 0; q < 32; ++q) v[q] = vn[q];
             }
+            tmem_ld_wait();
             boff += a.hidden;
             if (tr && etid == 0) tr[5 + 4 * l] = clock64();
         }
