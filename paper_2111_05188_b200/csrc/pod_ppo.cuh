@@ -196,12 +196,13 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     const dim3 ngrid(static_cast<unsigned>(std::min<int64_t>((g8 + 255) / 256, 8 * 148)), 1);
     const float one = 1.0f, zero = 0.0f;
     const int B = batch;
-    const unsigned eg = 148 * 4;
     const unsigned ag_rows = static_cast<unsigned>((B + PPO_AG_ROWS - 1) / PPO_AG_ROWS);   // <= 2^31 / 16
     // the minibatch loop, enqueued on stream s (captured below, or eager with POD_PPO_GRAPH=0)
     auto enqueue = [&](cudaStream_t s) -> pod_status {
     POD_CUBLAS(cublasSetStream(cb, s));
     POD_CUBLAS(cublasSetWorkspace(cb, w + W.cublas, kPpoCublasWs));
+    // the gradient vector is cleared once here, then by each minibatch's Adam step for the next
+    POD_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * L.n_elems, s));
     for (int j = 0; j < n_minibatches; ++j) {
         ppo_gather_kernel<<<B, 128, 0, s>>>(obs, act_raw, logp_old, adv, ret, perm + static_cast<int64_t>(j) * B, B,
                                             L.k_pad, n, reinterpret_cast<uint16_t*>(x0), act_b, lpo_b, adv_b, ret_b);
@@ -221,7 +222,6 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         }
         // head loss and dL/d(head output) -> b0 [B][n_out_pad] (bf16) and the head bias gradient; gradient
         // vector cleared first
-        POD_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * L.n_elems, s));
         PpoHead hh{B, n, L.n_out_pad, hp->ratio_clip, hp->entropy_coef, hp->value_coef, act_b, lpo_b, adv_b, ret_b,
                    zh, master + lsoff, b0, grad + boff[L.n_layers - 1], grad + lsoff, losses};
         ppo_head_kernel<<<(B + PPO_HEAD_WARPS - 1) / PPO_HEAD_WARPS, 32 * PPO_HEAD_WARPS, 0, s>>>(hh);
@@ -248,9 +248,9 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         }
         if (grad_out && j == n_minibatches - 1)
             POD_CUDA(cudaMemcpyAsync(grad_out, grad, sizeof(float) * L.n_elems, cudaMemcpyDeviceToDevice, s));
-        ppo_adam_kernel<<<eg, 256, 0, s>>>(master, adam_m, adam_v, grad, static_cast<int64_t>(L.n_elems),
-                                           hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps, step_slot, j);
-        fuse_blend_kernel<<<ngrid, 256, 0, s>>>(fa);
+        // Adam on the master, narrowed into the slab, gradient cleared for the next minibatch
+        ppo_adam_narrow_kernel<<<ngrid, 256, 0, s>>>(fa, adam_m, adam_v, grad, hp->learning_rate, hp->adam_beta1,
+                                                     hp->adam_beta2, hp->adam_eps, step_slot, j);
         POD_CUDA(cudaGetLastError());
     }
     if (n_minibatches == 0) {

@@ -20,6 +20,8 @@
 
 #include <cstdint>
 
+#include "fuse_kernel.cuh"
+
 namespace pod {
 
 struct PpoHead {
@@ -210,37 +212,51 @@ __global__ void ppo_act_grad_kernel(const float* __restrict__ dx, const __nv_bfl
     if (s1 != 0.0f) atomicAdd(&db[c + 1], s1);
 }
 
-// Adam (bias-corrected) over the flat parameter vector; the step number is *step_base + j + 1, read from
-// device memory so that one captured graph serves every call (c1 = 1 - b1^step, c2 = 1 - b2^step)
-__global__ void ppo_adam_kernel(float* __restrict__ theta, float* __restrict__ m, float* __restrict__ v,
-                                const float* __restrict__ g, int64_t count, float lr, float b1, float b2, float eps,
-                                const int64_t* __restrict__ step_base, int j) {
+__global__ void ppo_set_step_kernel(int64_t* __restrict__ slot, int64_t adam_t) { *slot = adam_t; }
+
+// Adam step on the float32 master (fa.work) fused with the narrowing of the result into the rollout slab
+// (bf16 RNE weights, f32 biases / log-std: the fusion's segment table with K = 1) and the clearing of the
+// gradient for the next minibatch; 8 consecutive elements per thread (segments are multiples of 8).
+__global__ void ppo_adam_narrow_kernel(const __grid_constant__ FuseArgs fa, float* __restrict__ m,
+                                       float* __restrict__ v, float* __restrict__ g, float lr, float b1, float b2,
+                                       float eps, const int64_t* __restrict__ step_base, int j) {
     const double step = static_cast<double>(*step_base + j + 1);
     const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(b1), step));
     const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(b2), step));
-    auto upd = [&](float& th, float& mi, float& vi, float gi) {
-        mi = b1 * mi + (1.0f - b1) * gi;
-        vi = b2 * vi + (1.0f - b2) * gi * gi;
-        th -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
-    };
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t c4 = count / 4;   // all four arrays are 16-byte aligned (checked on the host)
-    for (int64_t q = t0; q < c4; q += stride) {
-        float4 th = reinterpret_cast<float4*>(theta)[q], mi = reinterpret_cast<float4*>(m)[q];
-        float4 vi = reinterpret_cast<float4*>(v)[q];
-        const float4 gi = reinterpret_cast<const float4*>(g)[q];
-        upd(th.x, mi.x, vi.x, gi.x);
-        upd(th.y, mi.y, vi.y, gi.y);
-        upd(th.z, mi.z, vi.z, gi.z);
-        upd(th.w, mi.w, vi.w, gi.w);
-        reinterpret_cast<float4*>(theta)[q] = th;
-        reinterpret_cast<float4*>(m)[q] = mi;
-        reinterpret_cast<float4*>(v)[q] = vi;
+    const int64_t n8 = fa.n_elems / 8;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n8; q += stride) {
+        int64_t o;
+        const FuseSeg& sg = fa.seg[fuse_find(fa, 8 * q, &o)];
+        float th[8], mi[8], vi[8], gi[8];
+        float4* t4 = reinterpret_cast<float4*>(fa.work + 8 * q);
+        float4* m4 = reinterpret_cast<float4*>(m + 8 * q);
+        float4* v4 = reinterpret_cast<float4*>(v + 8 * q);
+        float4* g4 = reinterpret_cast<float4*>(g + 8 * q);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 a = t4[h], b = m4[h], c = v4[h], d = g4[h];
+            th[4 * h] = a.x; th[4 * h + 1] = a.y; th[4 * h + 2] = a.z; th[4 * h + 3] = a.w;
+            mi[4 * h] = b.x; mi[4 * h + 1] = b.y; mi[4 * h + 2] = b.z; mi[4 * h + 3] = b.w;
+            vi[4 * h] = c.x; vi[4 * h + 1] = c.y; vi[4 * h + 2] = c.z; vi[4 * h + 3] = c.w;
+            gi[4 * h] = d.x; gi[4 * h + 1] = d.y; gi[4 * h + 2] = d.z; gi[4 * h + 3] = d.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            mi[k] = b1 * mi[k] + (1.0f - b1) * gi[k];
+            vi[k] = b2 * vi[k] + (1.0f - b2) * gi[k] * gi[k];
+            th[k] -= lr * (mi[k] / c1) / (sqrtf(vi[k] / c2) + eps);
+        }
+        const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            t4[h] = make_float4(th[4 * h], th[4 * h + 1], th[4 * h + 2], th[4 * h + 3]);
+            m4[h] = make_float4(mi[4 * h], mi[4 * h + 1], mi[4 * h + 2], mi[4 * h + 3]);
+            v4[h] = make_float4(vi[4 * h], vi[4 * h + 1], vi[4 * h + 2], vi[4 * h + 3]);
+            g4[h] = zero;
+        }
+        fuse_store8(fa.params, sg, o, th);
     }
-    for (int64_t i = 4 * c4 + t0; i < count; i += stride) upd(theta[i], m[i], v[i], g[i]);
 }
-
-__global__ void ppo_set_step_kernel(int64_t* __restrict__ slot, int64_t adam_t) { *slot = adam_t; }
 
 }  // namespace pod
