@@ -334,6 +334,27 @@ def test_env_groups_bit_identical(monkeypatch):
             assert torch.equal(getattr(outs[0], name), getattr(other, name)), name
 
 
+@pytest.mark.parametrize("n,N,nh,hid", [(30, 512, 2, 128), (100, 36864, 3, 512)])
+def test_pdl_env_launch_bit_identical(n, N, nh, hid, monkeypatch):
+    """The env step launched as a programmatic dependent of the actor (griddepcontrol; default where it
+    pays: a small launch whose tiles fit the idle SMs, N = 512, or a dense one, >= 7 tiles per SM, N =
+    36864 at the C3 actor shape) is bit-identical to the plain stream order (POD_PDL=0), including the
+    critic values and the next-step noise the env step writes while the actor grid may still run."""
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("POD_PDL", flag)
+        c = Case(n=n, f=3, T_data=600, N=N, H=50, seed=14)
+        aws, params, actor = _actor(c, nh, hid)
+        tr = api.Trajectory.allocate(3, N, n, c.k_pad, debug=True, critic=True)
+        c.env.reset(c.starts)
+        c.env.rollout(3, tr, actor=actor)
+        c.env.check()
+        torch.cuda.synchronize()
+        outs.append(tr)
+    for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash", "dbg_aint", "val"):
+        assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
+
+
 @pytest.mark.parametrize("cost", [0.0, 0.25, 0.002])
 @pytest.mark.parametrize("kind", ["all_buy", "uniform", "buy_then_sell"])
 def test_exact_quotient_ties(kind, cost):
