@@ -535,13 +535,14 @@ def test_equity_curve_exact_and_backtest_metrics():
     assert np.all(mf[[0, 1, 2, 4]] == 0.0) and np.all(np.isnan(mf[3]))
 
 
-@pytest.mark.parametrize("act,B", [(0, 512), (1, 512), (0, 1001)])
-def test_ppo_update_parity(act, B):
+@pytest.mark.parametrize("act,B,n,nh,hid", [(0, 512, 30, 2, 128), (1, 512, 30, 2, 128), (0, 1001, 30, 2, 128),
+                                            (0, 512, 64, 1, 256), (1, 384, 30, 4, 128)])
+def test_ppo_update_parity(act, B, n, nh, hid):
     """R#26: one PPO minibatch on the device buffers of a rollout (critic values, normalised GAE):
     the float32 gradient (cuBLAS GEMMs + this library's kernels) vs the float64 oracle's analytic
     gradient at the same parameters on the same rows; the loss sums; the Adam step; the refreshed slab."""
-    c = Case(n=30, f=3, T_data=400, N=256, H=100, seed=51)
-    aws, params, actor = _actor(c, 2, 128, act=act)
+    c = Case(n=n, f=3, T_data=400, N=256, H=100, seed=51)   # n = 64: the critic row in a fresh pad block
+    aws, params, actor = _actor(c, nh, hid, act=act)
     T = 8   # B = 1001: ragged in every kernel's row blocking (8-sample head blocks, 16-row bias blocks)
     tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, critic=True)
     c.env.reset(c.starts)
@@ -555,13 +556,13 @@ def test_ppo_update_parity(act, B):
     A = adv.reshape(M)
     R = ret.reshape(M)
     lr = 1e-3
-    learner = api.PPOLearner(c.cfg, 2, 128, params, act=act, batch=B, learning_rate=lr)
+    learner = api.PPOLearner(c.cfg, nh, hid, params, act=act, batch=B, learning_rate=lr)
     theta0 = learner.master.cpu().numpy().astype(np.float64)
     rows = np.random.default_rng(3).permutation(M)[:B].astype(np.int32)
     g_gpu = torch.empty(learner.n_elems, dtype=torch.float32, device="cuda")
     losses = learner.update(obs, act_raw, lpo, A, R, torch.from_numpy(rows).cuda(), grad_out=g_gpu)
-    L = api.actor_layout(c.cfg, 2, 128)
-    dims = (L.k_pad, 128, 2, c.n, L.n_out_pad)
+    L = api.actor_layout(c.cfg, nh, hid)
+    dims = (L.k_pad, hid, nh, c.n, L.n_out_pad)
     _, g_o, (sobj, svl, H) = oracle.ppo_loss_grad(
         theta0, dims, bf16_to_f64(obs[rows]), act_raw[rows].cpu().numpy(), lpo[rows].cpu().numpy(),
         A[rows].cpu().numpy(), R[rows].cpu().numpy(), 0.25, 0.02, 0.5, act)
