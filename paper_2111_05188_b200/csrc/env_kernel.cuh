@@ -182,6 +182,17 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     const int64_t t = s + k;
     const bool done = stepping && ((k + 1 == a.horizon) || (t + 1 == a.T_data - 1));
     const int64_t t_obs = stepping ? (done ? s : t + 1) : t;   // market row of the next observation
+    if (stepping) {
+        // the next step reads close[t'+1] and feat[t'+1] (t' = this step's next row) for the first time:
+        // pull them into L2 now, so the next launch's dependent market loads do not go to HBM
+        const int64_t tn = t_obs + 1;
+        const int lc = (n * 4 + 127) / 128, lf = (a.f * n * 4 + 127) / 128;
+        if (tn < a.T_data && tid < lc + lf) {
+            const char* row = tid < lc ? reinterpret_cast<const char*>(a.close + tn * n) + tid * 128
+                                       : reinterpret_cast<const char*>(a.feat + tn * a.f * n) + (tid - lc) * 128;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+        }
+    }
 
     if (need_hold && !tma) {   // ragged tile: cooperative plain loads
         for (int i = warp; i < n; i += 4) {
