@@ -321,7 +321,8 @@ pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, i
  *   master, adam_m, adam_v [dev] f32 [layout.n_elems] (pod_fuse_pods order), in/out;
  *   obs [dev] bf16 [M][k_pad], act_raw f32 [M][n], logp_old, adv, ret f32 [M]
  *   (traj.obs rows 0..T-1, traj.act, traj.logp, normalised advantages, returns);
- *   perm [dev] i32 [n_minibatches * batch] row indices in [0, M);
+ *   perm [dev] i32 [n_minibatches * batch] row indices in [0, M) (may be NULL
+ *   when n_minibatches == 0: the call then only re-narrows master into params);
  *   losses [dev] f64 [4] accumulates (sum of the surrogate objective, sum of
  *   (V - R)^2, entropy per minibatch, rows); grad_out [dev] f32 [n_elems] or
  *   NULL: the last minibatch's gradient (diagnostics); ws >=

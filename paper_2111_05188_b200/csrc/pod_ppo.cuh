@@ -111,8 +111,8 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
                                      int64_t M, const int32_t* perm, int32_t batch, int32_t n_minibatches,
                                      double* losses, float* grad_out, void* ws, size_t ws_bytes, void* stream) {
     using namespace pod;
-    if (!hp || !master || !adam_m || !adam_v || !params || !obs || !act_raw || !logp_old || !adv || !ret || !perm ||
-        !losses || !ws)
+    if (!hp || !master || !adam_m || !adam_v || !params || !obs || !act_raw || !logp_old || !adv || !ret ||
+        (!perm && n_minibatches > 0) || !losses || !ws)
         return pod_fail(POD_ERR_ARG, "NULL argument");
     if (act != 0 && act != 1) return pod_fail(POD_ERR_ARG, "act must be 0 (ReLU) or 1 (tanh)");
     if (batch < 1 || n_minibatches < 0 || M < 1 || adam_t < 0) return pod_fail(POD_ERR_ARG, "bad batch / M / adam_t");

@@ -272,6 +272,37 @@ def test_error_paths():
     api.Env(cfg, c.close_d, c.feat_d)           # the clean market is accepted
 
 
+def test_degenerate_calls():
+    """Empty and degenerate inputs: a rollout of T = 0 steps and a GAE over an empty buffer are argument
+    errors (nothing launched); selection with k = P keeps every slot (identity plan, slabs untouched);
+    a PPO update with no minibatches only re-narrows the master into the slab it came from (unchanged)."""
+    c = Case(n=30, f=3, T_data=200, N=64, H=50, seed=31)
+    aws, params, actor = _actor(c, 2, 128, n_agents=2)
+    tr = api.Trajectory.allocate(1, 64, 30, c.k_pad)
+    c.env.reset(c.starts)
+    with pytest.raises(PodError) as ei:
+        c.env.rollout(0, tr, actor=actor)
+    assert ei.value.name == "POD_ERR_ARG"
+    z = torch.zeros((0, 64), dtype=torch.float32, device="cuda")
+    with pytest.raises(PodError) as ei:
+        api.pod_gae(z, z, torch.zeros((0, 64), dtype=torch.uint8, device="cuda"),
+                    torch.zeros(64, device="cuda"), 0.99, 0.95)
+    assert ei.value.name == "POD_ERR_ARG"
+    comm = api.Comm(1, 0, 2)
+    before = params.clone()
+    plan = comm.select_elite(torch.tensor([0.5, 0.25], dtype=torch.float64, device="cuda"), 2, params)
+    torch.cuda.synchronize()
+    assert plan.tolist() == [0, 1] and torch.equal(params, before)
+    comm.destroy()
+    learner = api.PPOLearner(c.cfg, 2, 128, params[:1], batch=64)
+    M = 64
+    empty_perm = torch.zeros(0, dtype=torch.int32, device="cuda")
+    learner.update(tr.obs[:1].reshape(M, c.k_pad), torch.zeros((M, 30), device="cuda"), torch.zeros(M, device="cuda"),
+                   torch.zeros(M, device="cuda"), torch.zeros(M, device="cuda"), empty_perm)
+    torch.cuda.synchronize()
+    assert torch.equal(params, before)
+
+
 # ----------------------------------------------------------------- full size (bench launch config)
 def test_full_size_c3_sampled_rows():
     """C3 launch configuration (8192 envs, n=100, 3x512, one agent) on sampled rows."""
