@@ -768,6 +768,7 @@ def test_wide_actor_matches_column_split(tmp_path, hidden):
     (30, 0, 96, 4, 128, 0, 1, 100, 0.0),      # no indicator channels, four hidden layers, zero cost
     (64, 3, 200, 1, 512, 1, 2, 7, 0.01),      # n % 32 == 0 (critic row in a fresh pad block), 2 agents, small h_max
     (5, 1, 33, 3, 128, 0, 1, 100, 0.002),     # one indicator channel, ragged second tile
+    (127, 0, 160, 2, 512, 0, 1, 1000, 0.002), # the most stocks (n_out_pad 128: the widest head), h_max 1000
 ])
 def test_shape_sweep(n, f, N, nh, hid, act, agents, h_max, cost):
     """Sampled rollout with critic on edge configurations: actor means and critic values vs the float64
