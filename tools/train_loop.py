@@ -49,6 +49,7 @@ def main():
     T = args.T
     tr = api.Trajectory.allocate(T, N, w.n_stocks, env.k_pad, critic=True)
     learners = [api.PPOLearner(cfg, w.n_hidden, w.hidden, params[s : s + 1], batch=1024) for s in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
     comm = api.Comm(1, 0, P)
     fit = torch.empty(P, dtype=torch.float64, device="cuda")
     prev = torch.empty((A, int(api.actor_layout(cfg, w.n_hidden, w.hidden).n_elems)), dtype=torch.float32,
@@ -62,7 +63,8 @@ def main():
         adv, ret = api.pod_gae(tr.rew, tr.val[:T].contiguous(), tr.done, tr.val[T].contiguous(), w.gamma, w.lam,
                                normalize=True)
         per = N // P
-        for s in range(P):
+        main = torch.cuda.current_stream()
+        for s in range(P):   # the pods' learners run concurrently, one stream each
             rows = torch.arange(s * per, (s + 1) * per, device="cuda")
             sel = (torch.arange(T, device="cuda")[:, None] * N + rows[None, :]).reshape(-1)
             M = sel.numel()
@@ -73,7 +75,12 @@ def main():
             r_s = ret.reshape(T * N)[sel].contiguous()
             n_mb = max(1, M // 1024)
             perm = torch.from_numpy(rng.permutation(M)[: n_mb * 1024].astype(np.int32)).cuda()
-            learners[s].update(obs, act, lpo, a_s, r_s, perm)
+            streams[s].wait_stream(main)
+            for t_ in (obs, act, lpo, a_s, r_s, perm):
+                t_.record_stream(streams[s])
+            learners[s].update(obs, act, lpo, a_s, r_s, perm, stream=streams[s])
+        for s in range(P):
+            main.wait_stream(streams[s])
         # ---- K-pod fusion (hard adoption of the mean, tau = 1)
         api.fuse_pods(cfg, w.n_hidden, w.hidden, params, K, tau=1.0, prev=prev)
         for s in range(P):   # learners continue from the fused parameters
