@@ -328,8 +328,9 @@ pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, i
  *   NULL: the last minibatch's gradient (diagnostics); ws >=
  *   pod_ppo_workspace_size (the last 256 bytes hold the device Adam step base).
  * The minibatch loop is captured into a CUDA graph on the first call with a
- * given argument set (all pointers, sizes and hyper-parameters; adam_t and the
- * stream excepted) and replayed by later calls (library-owned, 16 per thread,
+ * given set of pointers and sizes (adam_t, the hyper-parameters and the stream
+ * excepted: they are passed through device memory, so schedules replay the same
+ * graph) and replayed by later calls (library-owned, 16 per thread,
  * least recently used evicted); the calling thread's first call also creates
  * its cuBLAS handle (the only allocation).  cuBLAS scratch lives in `ws`, so
  * learners with distinct buffers may run concurrently on different streams.

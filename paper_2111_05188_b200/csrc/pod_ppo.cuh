@@ -1,8 +1,9 @@
 // pod_ppo.cuh — host side of pod_ppo_update (included by pod_api.cu; kernels in ppo_kernel.cuh).
 // Forward/backward GEMMs are bf16 x bf16 -> float32 library GEMMs (cuBLAS tensor cores, column-major view
 // of the row-major [rows][cols] matrices); every other step runs in this library's kernels.  The whole
-// minibatch loop (~28 launches per minibatch) is captured once into a CUDA graph per argument set and
-// replayed; only the Adam step counter changes between calls and it is read from device memory.
+// minibatch loop (19 launches per minibatch) is captured once into a CUDA graph per buffer set and
+// replayed; the Adam step counter and the hyper-parameters (schedules: learning rate, clip, entropy
+// coefficient) are written to device memory by one small kernel per call and read from there.
 #pragma once
 #include <cublas_v2.h>
 
@@ -55,12 +56,11 @@ inline cublasHandle_t ppo_cublas() {
     return h;
 }
 
-// captured minibatch loops, keyed on every argument but adam_t and the stream
+// captured minibatch loops, keyed on every pointer and size (not adam_t, the hyper-parameters or the stream)
 struct PpoGraphKey {
     const void* p[16];
     int64_t M, k_pad, n_elems;
     int32_t cfg_n, n_hidden, hidden, act, batch, n_mb, dev;
-    pod_ppo_hparams hp;
     size_t param_bytes, ws_bytes;
     bool operator==(const PpoGraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -138,7 +138,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     cublasHandle_t cb = ppo_cublas();
     if (!cb) return pod_fail(POD_ERR_CUDA, "cublasCreate failed");
     char* w = static_cast<char*>(ws);
-    int64_t* step_slot = reinterpret_cast<int64_t*>(w + W.step);
+    PpoDev* hpd = reinterpret_cast<PpoDev*>(w + W.step);   // step base + hyper-parameters of this call
     __nv_bfloat16* x0 = reinterpret_cast<__nv_bfloat16*>(w + W.x0);
     __nv_bfloat16* hbuf = reinterpret_cast<__nv_bfloat16*>(w + W.h);
     float* zf = reinterpret_cast<float*>(w + W.zf);
@@ -222,7 +222,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         }
         // head loss and dL/d(head output) -> b0 [B][n_out_pad] (bf16) and the head bias gradient; gradient
         // vector cleared first
-        PpoHead hh{B, n, L.n_out_pad, hp->ratio_clip, hp->entropy_coef, hp->value_coef, act_b, lpo_b, adv_b, ret_b,
+        PpoHead hh{B, n, L.n_out_pad, hpd, act_b, lpo_b, adv_b, ret_b,
                    zh, master + lsoff, b0, grad + boff[L.n_layers - 1], grad + lsoff, losses};
         ppo_head_kernel<<<(B + PPO_HEAD_WARPS - 1) / PPO_HEAD_WARPS, 32 * PPO_HEAD_WARPS, 0, s>>>(hh);
         // backward: dW_l = delta_l^T X_l, delta_{l-1} = (delta_l W_l) * act'(X_l) with db_{l-1} = colsum
@@ -249,8 +249,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
         if (grad_out && j == n_minibatches - 1)
             POD_CUDA(cudaMemcpyAsync(grad_out, grad, sizeof(float) * L.n_elems, cudaMemcpyDeviceToDevice, s));
         // Adam on the master, narrowed into the slab, gradient cleared for the next minibatch
-        ppo_adam_narrow_kernel<<<ngrid, 256, 0, s>>>(fa, adam_m, adam_v, grad, hp->learning_rate, hp->adam_beta1,
-                                                     hp->adam_beta2, hp->adam_eps, step_slot, j);
+        ppo_adam_narrow_kernel<<<ngrid, 256, 0, s>>>(fa, adam_m, adam_v, grad, hpd, j);
         POD_CUDA(cudaGetLastError());
     }
     if (n_minibatches == 0) {
@@ -259,7 +258,8 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     }
     return POD_OK;
     };
-    ppo_set_step_kernel<<<1, 1, 0, user_s>>>(step_slot, adam_t);
+    ppo_set_step_kernel<<<1, 1, 0, user_s>>>(hpd, adam_t, hp->ratio_clip, hp->entropy_coef, hp->value_coef,
+                                             hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps);
     POD_CUDA(cudaGetLastError());
     static const bool use_graph = [] {
         const char* e = std::getenv("POD_PPO_GRAPH");
@@ -281,7 +281,6 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     key.batch = batch;
     key.n_mb = n_minibatches;
     cudaGetDevice(&key.dev);
-    key.hp = *hp;
     key.param_bytes = param_bytes;
     key.ws_bytes = ws_bytes;
     static thread_local uint64_t ppo_clock = 0;

@@ -24,9 +24,16 @@
 
 namespace pod {
 
+// per-call values in device memory (written by ppo_set_step_kernel before the captured minibatch loop), so
+// one graph serves every call of a schedule: the Adam step base and the hyper-parameters
+struct PpoDev {
+    int64_t step_base;
+    float ratio_clip, entropy_coef, value_coef, lr, b1, b2, eps, pad;
+};
+
 struct PpoHead {
     int32_t B, n, n_out_pad;
-    float eps, c_ent, c_v;
+    const PpoDev* hpd;       // ratio clip, entropy and value coefficients
     const float* act;        // [B][n] raw actions of the minibatch
     const float* logp_old;   // [B]
     const float* adv;        // [B]
@@ -112,6 +119,7 @@ __global__ void __launch_bounds__(32 * PPO_HEAD_WARPS) ppo_head_kernel(const Ppo
     }
     __syncthreads();
     const int b = blockIdx.x * PPO_HEAD_WARPS + warp;
+    const float h_eps = h.hpd->ratio_clip, h_c_ent = h.hpd->entropy_coef, h_c_v = h.hpd->value_coef;
     const float inv_b = 1.0f / static_cast<float>(h.B);
     const float half_ln_2pi = 0.918938533204672742f;
     double obj = 0.0, vl = 0.0;
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(32 * PPO_HEAD_WARPS) ppo_head_kernel(const Ppo
         const float A = h.adv[b];
         const float rho = expf(logp - h.logp_old[b]);
         const float s1 = rho * A;
-        const float s2 = fminf(fmaxf(rho, 1.0f - h.eps), 1.0f + h.eps) * A;
+        const float s2 = fminf(fmaxf(rho, 1.0f - h_eps), 1.0f + h_eps) * A;
         const bool active = s1 <= s2;
         obj = static_cast<double>(active ? s1 : s2);
         const float coef = active ? -A * rho * inv_b : 0.0f;   // dL/dlogp of this sample
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(32 * PPO_HEAD_WARPS) ppo_head_kernel(const Ppo
                 di = coef * z * isig;                          // dlogp/dmu_i = z_i / sigma_i
                 if (coef != 0.0f) atomicAdd(&g_ls[i], coef * (z * z - 1.0f));
             } else if (i == h.n) {
-                di = 2.0f * h.c_v * (V - R) * inv_b;
+                di = 2.0f * h_c_v * (V - R) * inv_b;
             }
             if (di != 0.0f) atomicAdd(&g_b[i], di);
             dbf[i] = __float2bfloat16_rn(di);
@@ -153,7 +161,7 @@ __global__ void __launch_bounds__(32 * PPO_HEAD_WARPS) ppo_head_kernel(const Ppo
     double ent = 0.0;
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < h.n; i += blockDim.x) {
-            atomicAdd(&g_ls[i], -h.c_ent);
+            atomicAdd(&g_ls[i], -h_c_ent);
             ent += static_cast<double>(h.log_std[i]) + 1.4189385332046727418;   // (1 + ln 2 pi) / 2
         }
 #pragma unroll
@@ -212,15 +220,26 @@ __global__ void ppo_act_grad_kernel(const float* __restrict__ dx, const __nv_bfl
     if (s1 != 0.0f) atomicAdd(&db[c + 1], s1);
 }
 
-__global__ void ppo_set_step_kernel(int64_t* __restrict__ slot, int64_t adam_t) { *slot = adam_t; }
+__global__ void ppo_set_step_kernel(PpoDev* __restrict__ d, int64_t adam_t, float ratio_clip, float entropy_coef,
+                                    float value_coef, float lr, float b1, float b2, float eps) {
+    d->step_base = adam_t;
+    d->ratio_clip = ratio_clip;
+    d->entropy_coef = entropy_coef;
+    d->value_coef = value_coef;
+    d->lr = lr;
+    d->b1 = b1;
+    d->b2 = b2;
+    d->eps = eps;
+}
 
 // Adam step on the float32 master (fa.work) fused with the narrowing of the result into the rollout slab
 // (bf16 RNE weights, f32 biases / log-std: the fusion's segment table with K = 1) and the clearing of the
 // gradient for the next minibatch; 8 consecutive elements per thread (segments are multiples of 8).
 __global__ void ppo_adam_narrow_kernel(const __grid_constant__ FuseArgs fa, float* __restrict__ m,
-                                       float* __restrict__ v, float* __restrict__ g, float lr, float b1, float b2,
-                                       float eps, const int64_t* __restrict__ step_base, int j) {
-    const double step = static_cast<double>(*step_base + j + 1);
+                                       float* __restrict__ v, float* __restrict__ g, const PpoDev* __restrict__ d,
+                                       int j) {
+    const float lr = d->lr, b1 = d->b1, b2 = d->b2, eps = d->eps;
+    const double step = static_cast<double>(d->step_base + j + 1);
     const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(b1), step));
     const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(b2), step));
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;

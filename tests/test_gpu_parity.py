@@ -693,6 +693,43 @@ def test_ppo_graph_replay_step_counter():
     assert off[moved].mean() < 0.01, off[moved].mean()
 
 
+def test_ppo_hyperparameter_schedule_replays_graph():
+    """Hyper-parameters reach the captured minibatch loop through device memory: a learner whose
+    learning rate changes between calls (same buffers: a graph replay) takes exactly the step of a fresh
+    learner constructed with that rate (same state, same kernels, deterministic data) — a stale, baked-in
+    rate would give the first call's step."""
+    c = Case(n=30, f=3, T_data=400, N=256, H=100, seed=55)
+    aws, params, actor = _actor(c, 2, 128)
+    T, B = 8, 512
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, critic=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    adv, ret = api.pod_gae(tr.rew, tr.val[:T].contiguous(), tr.done, tr.val[T].contiguous(), 0.99, 0.95,
+                           normalize=True)
+    M = T * c.N
+    args = (tr.obs[:T].reshape(M, c.k_pad), tr.act.reshape(M, c.n), tr.logp.reshape(M), adv.reshape(M), ret.reshape(M))
+    perm = torch.from_numpy(np.random.default_rng(4).permutation(M)[:B].astype(np.int32)).cuda()
+    sched = api.PPOLearner(c.cfg, 2, 128, params.clone(), batch=B, learning_rate=1e-3, value_coef=0.0,
+                           entropy_coef=0.0)
+    sched.update(*args, perm)                       # capture at lr 1e-3
+    sched.hp.learning_rate = 5e-3
+    sched.m.zero_()
+    sched.v.zero_()
+    sched.t = 0
+    theta = sched.master.clone()
+    slab = sched.params.clone()                     # the GEMMs read the bf16 slab narrowed from theta
+    sched.update(*args, perm)                       # replay at lr 5e-3
+    fresh = api.PPOLearner(c.cfg, 2, 128, slab, batch=B, learning_rate=5e-3, value_coef=0.0, entropy_coef=0.0)
+    fresh.master.copy_(theta)
+    fresh.update(*args, perm)
+    torch.cuda.synchronize()
+    a, b = sched.master.cpu().numpy(), fresh.master.cpu().numpy()
+    moved = np.abs(b - theta.cpu().numpy()) > 0
+    assert moved.mean() > 0.5
+    # float atomics in the reductions: compare at 1 % of the step, allowing a 1 % tail
+    assert (np.abs(a - b) > 1e-2 * 5e-3)[moved].mean() < 0.01
+
+
 def test_ppo_concurrent_learners_on_streams():
     """Two learners (distinct buffers, own cuBLAS scratch inside their workspaces) replayed concurrently on
     two streams reach the same parameters as each run alone (float atomics in the reductions: float32-level
