@@ -296,6 +296,15 @@ class PPOLearner:
         self.ws = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
         self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
 
+    def set_hparams(self, **kw):
+        """Change hyper-parameters between updates (schedules): ratio_clip, entropy_coef, value_coef,
+        learning_rate, adam_beta1, adam_beta2, adam_eps.  They reach the captured minibatch loop through
+        device memory, so the next update replays the same graph."""
+        for k, v in kw.items():
+            if not hasattr(self.hp, k) or k == "reserved":
+                raise ValueError(f"unknown PPO hyper-parameter {k!r}")
+            setattr(self.hp, k, float(v))
+
     def update(self, obs: torch.Tensor, act_raw: torch.Tensor, logp_old: torch.Tensor, adv: torch.Tensor,
                ret: torch.Tensor, perm: torch.Tensor, grad_out: Optional[torch.Tensor] = None, stream=None):
         """obs bf16 [M, k_pad], act_raw f32 [M, n], logp_old/adv/ret f32 [M], perm i32 [n_mb * batch]."""

@@ -712,7 +712,7 @@ def test_ppo_hyperparameter_schedule_replays_graph():
     sched = api.PPOLearner(c.cfg, 2, 128, params.clone(), batch=B, learning_rate=1e-3, value_coef=0.0,
                            entropy_coef=0.0)
     sched.update(*args, perm)                       # capture at lr 1e-3
-    sched.hp.learning_rate = 5e-3
+    sched.set_hparams(learning_rate=5e-3)
     sched.m.zero_()
     sched.v.zero_()
     sched.t = 0
