@@ -408,10 +408,12 @@ def test_exact_quotient_ties(kind, cost):
     assert_env_exact(tr, out, env.obs_dim)
 
 
-def test_weight_multicast_bit_identical(monkeypatch):
-    """Opt-in 4-CTA clusters sharing weight tiles by TMA multicast give identical results."""
+@pytest.mark.parametrize("mcg", ["1", "4"])
+def test_weight_multicast_bit_identical(mcg, monkeypatch):
+    """Opt-in clusters sharing weight tiles by TMA multicast (POD_MULTICAST=1: two M-tiles in 4-CTA
+    clusters; 4: four M-tiles in 8-CTA clusters) give identical results."""
     outs = []
-    for mc in ("0", "1"):
+    for mc in ("0", mcg):
         monkeypatch.setenv("POD_MULTICAST", mc)
         c = Case(n=100, f=3, T_data=2000, N=512, H=300, seed=13, dt=1 / (252 * 390))
         aws, params, actor = _actor(c, 3, 512)
