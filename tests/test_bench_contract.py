@@ -25,3 +25,27 @@ def test_reference_arm_json_line():
     e = d["e2e"]
     assert e["value"] == d["value"] and e["unit"] == d["unit"]
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_json_line_on_gpu():
+    """The measured arm's line at a small config: the contract keys, the roofline of the dominant kernel,
+    e2e through the public API with host copies, the launch count and the clocks sample."""
+    out = subprocess.run([sys.executable, "bench.py", "--config", "C1", "--steps", "3", "--warmup", "3",
+                          "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900, check=True)
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor", "alu") and r["achieved"] > 0 and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and d["clocks"]["sm_mhz"] > 0
