@@ -30,7 +30,8 @@
 //     half is still in flight (per-rank K order: own half first);
 //   * head: each CTA samples its half of the tickers with noise z that the
 //     previous env-step launch generated in its otherwise idle warps; the per-row
-//     log-prob partials are combined in CTA 0 through DSMEM after a cluster barrier.
+//     log-prob partials go to a [4][N] scratch that the next env step sums in a fixed order (the
+//     DSMEM combine in CTA 0 remains for callers without the scratch).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -85,6 +86,7 @@ struct ActorArgs {
     float* val_out;      // [N] critic V(s_t) = head row n (R#22), or null
     uint32_t* err;
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
+    float* logp_parts;           // [4][N] log-prob partials (rank, half) for the env step to combine, or null
     uint32_t kpb_pack;           // K blocks per ring stage of layer l in bits [5l, 5l+5) (0/1: one 3-D box)
 };
 
@@ -583,17 +585,24 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             if (tr && it == 0 && etid == 0) tr[25] = clock64();
             // log-prob partial of (rank, hh) for row r -> CTA 0's buffer (it & 1) [rank*2 + hh][r]; CTA 1 first
             // makes sure CTA 0 has consumed the tile that last used this buffer (two tiles ago)
-            const uint32_t pb = static_cast<uint32_t>(it) & 1u;
-            float* logp_s = logp_s0 + pb * 512;
-            if (rank == 1 && it >= 2) mbar_wait_cluster(logpfree_b + 8u * pb, static_cast<uint32_t>((it - 2) >> 1) & 1u);
-            st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), cr & ~1u), logp);
-            mbar_arrive_remote(mapa_shared(logp_b, cr & ~1u));   // release: the partial is visible with the arrival
-            if (rank == 0) {
-                mbar_wait_cluster(logp_b, static_cast<uint32_t>(it) & 1u);
-                if (hh == 0 && valid && a.logp_out)
-                    a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
-                named_bar_sync(2, 256);
-                if (etid == 0) mbar_arrive_remote(mapa_shared(logpfree_b + 8u * pb, peer));
+            if (a.logp_parts) {
+                // the env step that follows combines the four partials ((p0 + p1) + p2) + p3: no
+                // cross-CTA exchange in this kernel's tail
+                if (valid && a.logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
+            } else {
+                const uint32_t pb = static_cast<uint32_t>(it) & 1u;
+                float* logp_s = logp_s0 + pb * 512;
+                if (rank == 1 && it >= 2)
+                    mbar_wait_cluster(logpfree_b + 8u * pb, static_cast<uint32_t>((it - 2) >> 1) & 1u);
+                st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), cr & ~1u), logp);
+                mbar_arrive_remote(mapa_shared(logp_b, cr & ~1u));   // release: the partial is visible with the arrival
+                if (rank == 0) {
+                    mbar_wait_cluster(logp_b, static_cast<uint32_t>(it) & 1u);
+                    if (hh == 0 && valid && a.logp_out)
+                        a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
+                    named_bar_sync(2, 256);
+                    if (etid == 0) mbar_arrive_remote(mapa_shared(logpfree_b + 8u * pb, peer));
+                }
             }
         }
     }

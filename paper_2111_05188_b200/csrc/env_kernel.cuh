@@ -82,6 +82,8 @@ struct EnvArgs {
     double* equity;           // [N] slice of step t: v_{t+1} before any reset, or null
     uint32_t* err;
     int32_t pdl;              // 1: launched as a programmatic dependent of the actor (see the kernel)
+    const float* logp_parts;  // [4][N] the actor's log-prob partials of this step, or null
+    float* logp_out;          // [N] slice of step t: ((p0 + p1) + p2) + p3 written here
 };
 
 struct EnvMaps {
@@ -255,6 +257,11 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     if (tma) mbar_wait(bar, 0);
     __syncthreads();
     if (trc && threadIdx.x == 0) trc[1] = clock64();
+    if (warp == 1 && stepping && a.logp_parts && a.logp_out && active) {
+        // the actor's four log-prob partials of this env, summed in the actor's own order
+        const float* pp = a.logp_parts + e;
+        a.logp_out[e] = ((pp[0] + pp[N]) + pp[2 * N]) + pp[3 * N];
+    }
 
     // ---- 4. the float64 ledger, warp 0, lane = env, in exactly the order of
     //         Eqs. 3-4 under R#3/R#4 (sells, then greedy buys, tickers ascending)

@@ -241,6 +241,7 @@ struct pod_env {
     // workspace carve
     int32_t* hold;
     int16_t* aint;
+    float* logp_parts;          // [4][N] K1's log-prob partials, combined by K2
     float* znoise;
     double *cash, *asset, *disc, *ep_ret, *tile_gpow;
     int32_t *tile_start, *tile_k;
@@ -262,7 +263,7 @@ struct pod_env {
 };
 
 struct WsLayout {
-    size_t hold, aint, znoise, cash, asset, disc, ep_ret, tile_start, tile_k, tile_gpow, step, err, total;
+    size_t hold, aint, znoise, logp_parts, cash, asset, disc, ep_ret, tile_start, tile_k, tile_gpow, step, err, total;
 };
 
 static WsLayout ws_layout(const pod_env_config* c) {
@@ -278,6 +279,7 @@ static WsLayout ws_layout(const pod_env_config* c) {
     w.hold = take(n * N * 4);
     w.aint = take(n * N * 2);
     w.znoise = take(n * N * 4);
+    w.logp_parts = take(4 * N * 4);
     w.cash = take(N * 8);
     w.asset = take(N * 8);
     w.disc = take(N * 8);
@@ -335,6 +337,7 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     char* b = static_cast<char*>(ws);
     e->hold = reinterpret_cast<int32_t*>(b + w.hold);
     e->aint = reinterpret_cast<int16_t*>(b + w.aint);
+    e->logp_parts = reinterpret_cast<float*>(b + w.logp_parts);
     e->znoise = reinterpret_cast<float*>(b + w.znoise);
     e->cash = reinterpret_cast<double*>(b + w.cash);
     e->asset = reinterpret_cast<double*>(b + w.asset);
@@ -621,6 +624,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             aa.mtile0 = m0;
             aa.act_out = tr->act + static_cast<int64_t>(t) * N * n;
             aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
+            aa.logp_parts = (p.pair || p.wide || !tr->logp) ? nullptr : e->logp_parts;
             aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
             aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
             aa.val_out = tr->val ? tr->val + static_cast<int64_t>(t) * N : nullptr;
@@ -636,6 +640,9 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         a.dbg_hold = tr->dbg_hold ? tr->dbg_hold + static_cast<int64_t>(t) * N * n : nullptr;
         a.dbg_cash = tr->dbg_cash ? tr->dbg_cash + static_cast<int64_t>(t) * N : nullptr;
         a.equity = tr->equity ? tr->equity + static_cast<int64_t>(t) * N : nullptr;
+        // the column-split actor leaves its log-prob partials to this step (the other variants write logp)
+        a.logp_parts = (!p.injected && !p.pair && !p.wide && tr->logp) ? e->logp_parts : nullptr;
+        a.logp_out = a.logp_parts ? tr->logp + static_cast<int64_t>(t) * N : nullptr;
         a.gen_noise = (sampling && t + 1 < T) ? 1 : 0;   // noise for the actor launch of step t+1
         a.noise_t = t + 1;
         // Programmatic dependent of the actor launch just before (not across a profiling event node):
