@@ -22,7 +22,8 @@
 // reassociate the cash sums and could flip a floor() at a near tie.  All four
 // warps then write the new holdings (coalesced 128-B rows), build the per-env
 // part of s_{t+1} and store the 32 observation rows with 16-B vector stores
-// (512 contiguous bytes per warp instruction).
+// (512 contiguous bytes per warp instruction).  Warp 1 also sums the actor's four log-prob partials
+// of each env into traj.logp (fixed order), and the idle warps draw the next step's actor noise.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
