@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t logp_b = obs_b + 88u;       // CTA 0: a tile's 4 x 128 log-prob partials written (512 arrivals)
     const uint32_t logpfree_b = obs_b + 96u;   // [2] CTA 1: CTA 0 has read partial buffer p (1 remote arrival)
     const uint32_t tslot_s = obs_b + 112u;
+    const uint32_t accl_b = obs_b + 120u;      // this CTA's MMAs of a layer are complete (local commit)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
     // persistent over M-tiles: cluster c (one CTA pair per M-tile) takes tiles mtile0 + c + it * nclusters
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             }
             mbar_init(obs_b, 1);
             mbar_init(accum_b, 2);        // one multicast commit from each CTA of the pair
+            mbar_init(accl_b, 1);
             mbar_init(actfree_b, 1);
             mbar_init(logp_b, 512);
             mbar_init(logpfree_b, 1);
@@ -412,7 +414,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         }
                     }
                     if (tr && it == 0) tr[3 + 4 * l] = clock64();
-                    mma_commit_mc(accum_b, pair_mask);
+                    mma_commit(accl_b);                  // this CTA's accumulator is complete
+                    mma_commit_mc(accum_b, pair_mask);   // ... and the pair has read h_l
                 }
                 mma_commit(actfree_b);   // the next tile's obs may overwrite act_s once these MMAs are done
             }
@@ -464,7 +467,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             for (int l = 0; l < a.n_layers - 1; ++l) {
                 const int g = it * a.n_layers + l;
                 const uint32_t hpar = static_cast<uint32_t>(it * (a.n_layers - 1) + l) & 1u;
-                mbar_wait(accum_b, static_cast<uint32_t>(g) & 1u);   // both CTAs done reading h_l
+                // this CTA's MMAs of layer l are done (its accumulator is final and its act_s is free for
+                // its own atoms); the peer's, before shipping atoms into its act_s (below)
+                mbar_wait(accl_b, static_cast<uint32_t>(g) & 1u);
                 tc_fence_after();
                 if (tr && it == 0 && etid == 0) tr[4 + 4 * l] = clock64();
                 // h_{l+1} atom by atom (64 columns = 8 warps x 32 columns x 128 rows), so the next
@@ -488,7 +493,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     tc_fence_before();
                     mbar_arrive(ownrdy_b + 8u * j);
                     if (etid == 0) {
-                        // the whole atom is written: ship it to the same offset in the peer
+                        // the whole atom is written: ship it to the same offset in the peer, once the
+                        // peer's MMAs are done reading its h_l
+                        if (j == 0) mbar_wait(accum_b, static_cast<uint32_t>(g) & 1u);
                         mbar_wait(ownrdy_b + 8u * j, hpar);
                         bulk_s2peer(mapa_shared(atom, peer), atom, 16384u, mapa_shared(peerrdy_b + 8u * j, peer));
                     }
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             // ----- head: this CTA's tickers [rank*head_half, ...), this warp's quarter of them
             const int L = a.n_layers - 1;
             const int gL = it * a.n_layers + L;
-            mbar_wait(accum_b, static_cast<uint32_t>(gL) & 1u);
+            mbar_wait(accl_b, static_cast<uint32_t>(gL) & 1u);
             tc_fence_after();
             if (tr && it == 0 && etid == 0) tr[24] = clock64();
             const float* bias = bias_s + boff;
