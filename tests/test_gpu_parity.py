@@ -317,8 +317,19 @@ def test_full_size_c3_sampled_rows():
     obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
     mu_g = tr.mu.cpu().numpy().astype(np.float64)
     w = oracle.actor_flat(aws[0].W, aws[0].b, aws[0].log_std)
+    raw_g = tr.act.cpu().numpy().astype(np.float64)
+    logp_g = tr.logp.cpu().numpy().astype(np.float64)
+    ls = aws[0].log_std.astype(np.float64)
     for t in range(T):
         mu_check(mu_g[t, rows], oracle.actor_mu(w, obs_g[t, rows], 3, 512, 100))
+        # noise (Philox, drawn by the previous env step) and the log-prob (partials summed by the env step)
+        for e in rows:
+            z_o = oracle.normals(c.cfg.seed, c.cfg.env_offset + int(e), t, 100)
+            z_g = (raw_g[t, e] - mu_g[t, e]) / np.exp(ls)
+            assert np.all(np.abs(z_g - z_o) <= 2e-5 * np.abs(z_o) + 5e-4), (t, e)
+            lp_o = float(np.sum(-0.5 * z_o * z_o - ls - 0.5 * math.log(2 * math.pi)))
+            terms = float(np.sum(0.5 * z_o * z_o + np.abs(ls) + 0.5 * math.log(2 * math.pi)))
+            assert abs(logp_g[t, e] - lp_o) <= 1e-5 * terms + 1e-4, (t, e)
     # env replay on the sampled envs (envs are independent: batch equivalence)
     a_g = tr.dbg_aint.cpu().numpy()
     starts = c.env_starts()[rows]
