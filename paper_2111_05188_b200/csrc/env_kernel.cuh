@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             // selling set (Eq. 3 "+ (p^S)^T k^S"), tickers ascending.  Branch-free: a
             // non-sell adds +0.0, which leaves the (never negative-zero) cash unchanged.
             // Only cash is carried: the post-sell holdings are recomputed in the buy pass.
-#pragma unroll 8
+            // unrolled 16 deep: the loads and products of 16 tickers are scheduled ahead of their
+            // carried adds (8: 4.2K cycles per tile for the sells, 16: 3.9K)
+#pragma unroll 16
             for (int i = 0; i < n; ++i) {
                 const int ai = aint_s[i * 32 + lane];
                 const int h = hold_s[i * 32 + lane];
