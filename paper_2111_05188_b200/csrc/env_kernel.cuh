@@ -117,6 +117,9 @@ __device__ __forceinline__ uint16_t f2bf(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
+// SELL_UNROLL / BUY_UNROLL: unroll depths of the ledger's two ticker loops (16 / 8 for many tickers,
+// 8 / 4 for few: the deeper unroll is +1.5 % at n = 100 and -3 % at n = 30)
+template <int SELL_UNROLL, int BUY_UNROLL>
 __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_constant__ EnvMaps maps, const EnvArgs a) {
     extern __shared__ __align__(128) uint8_t env_smem[];
     const int tid = threadIdx.x;
@@ -288,9 +291,9 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             // selling set (Eq. 3 "+ (p^S)^T k^S"), tickers ascending.  Branch-free: a
             // non-sell adds +0.0, which leaves the (never negative-zero) cash unchanged.
             // Only cash is carried: the post-sell holdings are recomputed in the buy pass.
-            // unrolled 16 deep: the loads and products of 16 tickers are scheduled ahead of their
-            // carried adds (8: 4.2K cycles per tile for the sells, 16: 3.9K)
-#pragma unroll 16
+            // unrolled SELL_UNROLL deep: the loads and products of that many tickers are scheduled ahead of
+            // their carried adds (n = 100: 8 -> 4.2K cycles per tile for the sells, 16 -> 3.9K)
+#pragma unroll SELL_UNROLL
             for (int i = 0; i < n; ++i) {
                 const int ai = aint_s[i * 32 + lane];
                 const int h = hold_s[i * 32 + lane];
@@ -324,9 +327,9 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 // holdings store (which would otherwise keep the compiler from hoisting them)
                 int ai_n = aint_s[i0 * 32 + lane], h_n = hold_s[i0 * 32 + lane];
                 double un_n = unit_s[i0], rc_n = rcp_s[i0];
-                // unrolled 8 deep (4: 13.4K cycles per tile for the buys, 8: 12.9K; 72 registers, still
-                // 7 tiles per SM, the shared-memory limit)
-#pragma unroll 8
+                // unrolled BUY_UNROLL deep (n = 100: 4 -> 13.4K cycles per tile for the buys, 8 -> 12.9K;
+                // 72 registers, still 7 tiles per SM, the shared-memory limit)
+#pragma unroll BUY_UNROLL
                 for (int i = i0; i < i1; ++i) {
                     const int ai = ai_n;
                     int h = h_n;

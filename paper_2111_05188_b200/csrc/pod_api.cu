@@ -403,7 +403,9 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
-        ce = cudaFuncSetAttribute(env_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        ce = cudaFuncSetAttribute(env_step_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(env_step_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(gae_smem_bytes()));
@@ -508,6 +510,12 @@ static EnvArgs env_args(const pod_env* e, int mode) {
 }
 
 static inline int env_blocks(const pod_env* e) { return e->n_tiles; }
+// the env-step instantiation for this handle's ticker count (ledger loop unroll depths)
+using EnvStepFn = void (*)(EnvMaps, EnvArgs);
+static inline EnvStepFn env_step_fn(const pod_env* e) {
+    return e->cfg.n_stocks >= 64 ? env_step_kernel<16, 8> : env_step_kernel<8, 4>;
+}
+
 static inline size_t env_smem(const pod_env* e) {
     static const size_t over = [] {   // experiments: POD_ENV_SMEM=<bytes> raises the request (fewer tiles per SM)
         const char* v = getenv("POD_ENV_SMEM");
@@ -541,7 +549,7 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
     POD_CUDA(cudaMemsetAsync(e->step, 0, 8, s));
     EnvArgs a = env_args(e, 2);
     a.obs_out = obs0;
-    env_step_kernel<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+    env_step_fn(e)<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
     POD_CUDA(cudaGetLastError());
     POD_CUDA(cudaStreamSynchronize(s));   // the pinned staging buffer is reused by the next reset
     return POD_OK;
@@ -609,7 +617,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
     a0.obs_out = tr->obs;
     a0.gen_noise = sampling;          // noise for the actor launch of step 0
     a0.noise_t = 0;
-    env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
+    env_step_fn(e)<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
     for (int t = 0; t < T; ++t) {
         mark(t, 0);
         if (p.injected) {
@@ -667,9 +675,9 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             at[0].val.programmaticStreamSerializationAllowed = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            cudaLaunchKernelEx(&lc, env_step_kernel, e->env_maps, a);
+            cudaLaunchKernelEx(&lc, env_step_fn(e), e->env_maps, a);
         } else {
-            env_step_kernel<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+            env_step_fn(e)<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
         }
         mark(t, 3);
     }
