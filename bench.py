@@ -143,6 +143,17 @@ def env_bytes_per_env(n, f, obs_dim):
     return 2 * n + 8 * n + 48 + 4 + 1 + 2 * obs_dim + (3 + f) * n * 4 / 32.0
 
 
+def env_bytes_per_env_survey(n, f, obs_dim):
+    """SURVEY.md §8(d)'s K2 byte model: a 2n + holdings r/w 8n + cash/asset r/w 32 + reward 4 + done 1 +
+    s_{t+1} 2 obs_dim per env-step, plus (n + n f) 4 B per tile of 32 envs (2,089 B at n = 100)."""
+    return 2 * n + 8 * n + 32 + 4 + 1 + 2 * obs_dim + (n + n * f) * 4 / 32.0
+
+
+def gae_bytes_survey(T, N):
+    """SURVEY.md §8(d)'s K3 byte model: 17 B per element (r, V, d read; A, R written) + 4 B per env."""
+    return 17.0 * T * N + 4.0 * N
+
+
 def gae_bytes(T, N):
     """r, V read 4+4, done 1, adv, ret written 4+4 per element; boot 4 per env; the per-buffer
     normalisation rereads and rewrites adv (+8 per element; R#23)."""
@@ -174,6 +185,29 @@ def oracle_step_sample(w, market, weights_flat, n_envs, T, nthreads, starts, cri
     J = oracle.fitness(env.ep_ret, 1)
     oracle.select_elite(J, 1)
     return time.perf_counter() - t0
+
+
+def c1_full_oracle(cores):
+    """configs[0] (C1) run in full by the oracle on the host: 16 envs x T = 64 steps of the whole step
+    (actor 2x128 + critic, env step, GAE, fitness, select), all cores and one thread."""
+    import numpy as np
+
+    import oracle
+    from paper_2111_05188_b200 import configs, synth
+
+    w1 = configs.preset("C1")
+    m1 = synth.make_market(w1.n_stocks, w1.T_data, w1.dt, w1.seed, n_feat=w1.n_feat)
+    aw = synth.make_actor(w1.obs_dim, w1.n_hidden, w1.hidden, w1.n_stocks, w1.seed * 1000)
+    wf = oracle.actor_flat(aw.W, aw.b, aw.log_std)
+    wcr = np.append(aw.w_v.astype(np.float64), aw.b_v)
+    st = np.repeat(synth.tile_starts(1, w1.T_data, w1.horizon, w1.seed + 1), 32)
+    out = {}
+    for th in (cores, 1):
+        tt = oracle_step_sample(w1, m1, wf, w1.n_envs, w1.T, th, st, wcr)
+        out["all_cores" if th == cores else "one_thread"] = {"value": w1.n_envs * w1.T / tt, "unit": UNIT,
+                                                              "cores": th, "seconds": tt}
+    out["sample"] = "C1 in full: 16 envs x 64 steps (whole step incl. actor 2x128 + critic, GAE, fitness, select)"
+    return out
 
 
 def run_reference(args, w, rank, world):
@@ -225,11 +259,32 @@ def workload_config(w, T=None, world=1):
             "l2": "inputs/outputs larger than L2 (trajectory writes per step >> 126 MB), no flush needed"}
 
 
+def relaunch_distributed(n: int) -> int:
+    """`--gpus N` without a torchrun environment: start N ranks of this same command under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, POD_BENCH_CHILD="1")
+    # the JSON line of rank 0 goes to the real stdout; everything else to stderr
+    r = subprocess.run(cmd, env=env, stdout=_JSON_FD, stderr=2)
+    return r.returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
     from paper_2111_05188_b200 import configs
 
     over = {}
@@ -295,28 +350,16 @@ def main():
     k_elite = args.elite_k or max(1, (P * world) // 2)
     stream = torch.cuda.current_stream()
     env.reset(starts)
-    env.profile(args.profile_stride)
-    ev_g0, ev_g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    acc = {"actor_ms": 0.0, "actor_n": 0, "env_ms": 0.0, "env_n": 0, "gae_ms": 0.0, "gae_n": 0}
+    env.profile(0)   # the headline is timed with no event nodes inside the rollout graph
 
-    def step(measure: bool):
+    def step():
         env.rollout(T, traj, actor=actor)
-        ev_g0.record(stream)
         api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret, normalize=True, stats=adv_stats)
-        ev_g1.record(stream)
         env.fitness(fit)
         comm.select_elite(fit, k_elite, params)
-        am, an, em, en = env.profile_read()
-        if measure:
-            acc["actor_ms"] += am
-            acc["actor_n"] += an
-            acc["env_ms"] += em
-            acc["env_n"] += en
-            acc["gae_ms"] += ev_g0.elapsed_time(ev_g1)
-            acc["gae_n"] += 1
 
     for _ in range(args.warmup):
-        step(False)
+        step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -327,7 +370,7 @@ def main():
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        step(True)
+        step()
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -342,6 +385,38 @@ def main():
     env_steps = world * N * T * args.steps
     value = env_steps / (ms_max / 1e3)
     env.check()
+
+    # ---- per-kernel durations: a separate pass of the same steps with CUDA events recorded inside the
+    # rollout graph around the actor / env-step launches of every k-th step (on the stream each launch runs
+    # on), and around the GAE launches; nothing of this pass enters `value`
+    acc = {"actor_ms": 0.0, "actor_n": 0, "env_ms": 0.0, "env_n": 0, "gae_ms": 0.0, "gae_n": 0, "step_ms": 0.0}
+    if args.profile_stride > 0:
+        env.profile(args.profile_stride)
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        env.rollout(T, traj, actor=actor)   # capture the profiled graph outside the timed pass
+        env.profile_read()
+        p0.record(stream)
+        for i in range(args.steps):
+            env.rollout(T, traj, actor=actor)
+            gev[i][0].record(stream)
+            api.pod_gae(traj.rew, val, traj.done, boot, w.gamma, w.lam, adv, ret, normalize=True, stats=adv_stats)
+            gev[i][1].record(stream)
+            env.fitness(fit)
+            comm.select_elite(fit, k_elite, params)
+            am, an, em, en = env.profile_read()
+            acc["actor_ms"] += am
+            acc["actor_n"] += an
+            acc["env_ms"] += em
+            acc["env_n"] += en
+        p1.record(stream)
+        torch.cuda.synchronize()
+        acc["step_ms"] = p0.elapsed_time(p1)
+        for g0, g1 in gev:
+            acc["gae_ms"] += g0.elapsed_time(g1)
+            acc["gae_n"] += 1
+        env.profile(0)
 
     # ---- end to end through the public API: pinned host inputs in, result out, every step
     e2e = None
@@ -380,41 +455,51 @@ def main():
                "d2h_bytes_per_step": int(bo)}
 
     if rank == 0:
-        # ---- per-kernel rooflines (algorithmic work / live CUDA-event duration)
+        # ---- per-kernel rooflines (algorithmic work per launch / live CUDA-event duration of the launch)
+        # tensor peak: the burst figure when the run held its clocks with no power cap (the kernel's own
+        # conditions), else the sustained one; both fractions are reported
+        capped = "sw_power_cap" in (ck.get("reasons") or []) or (
+            ck.get("sm_mhz") and ck.get("sm_max_mhz") and ck["sm_mhz"] < 0.95 * ck["sm_max_mhz"])
+        tpeak = peaks["bf16_tflops_sustained"] if capped else peaks["bf16_tflops"]
+        tpeak_kind = "sustained (power-capped clocks)" if capped else "burst (full clocks, no power cap)"
+        pstep = acc["step_ms"] if acc["step_ms"] > 0 else ms
         kern = {}
         if acc["actor_n"]:
             a_ms = acc["actor_ms"] / acc["actor_n"]
             flops = N * actor_flops_per_env(env.obs_dim, w.n_hidden, w.hidden, n)
             tf = flops / (a_ms / 1e3) / 1e12
-            kern["actor_mlp"] = {"bound": "tensor", "achieved": tf, "peak": peaks["bf16_tflops_sustained"],
-                                 "unit": "TFLOP/s", "frac": tf / peaks["bf16_tflops_sustained"],
+            kern["actor_mlp"] = {"bound": "tensor", "achieved": tf, "peak": tpeak, "peak_kind": tpeak_kind,
+                                 "unit": "TFLOP/s", "frac": tf / tpeak,
+                                 "frac_burst": tf / peaks["bf16_tflops"],
+                                 "frac_sustained": tf / peaks["bf16_tflops_sustained"],
+                                 "flop_per_env_step": actor_flops_per_env(env.obs_dim, w.n_hidden, w.hidden, n),
                                  "avg_launch_us_full_n": a_ms * 1e3, "launch_units_timed": acc["actor_n"],
-                                 "share_of_step": a_ms * T * args.steps / ms}
+                                 "share_of_step": a_ms * T * args.steps / pstep}
         if acc["env_n"]:
             e_ms = acc["env_ms"] / acc["env_n"]
-            by = N * env_bytes_per_env(n, w.n_feat, env.obs_dim)
-            gbs = by / (e_ms / 1e3) / 1e9
+            b_bench = env_bytes_per_env(n, w.n_feat, env.obs_dim)
+            b_survey = env_bytes_per_env_survey(n, w.n_feat, env.obs_dim)
+            gbs = N * b_bench / (e_ms / 1e3) / 1e9
             kern["env_step"] = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                "frac": gbs / peaks["hbm_gbs"], "avg_launch_us_full_n": e_ms * 1e3,
-                                "launch_units_timed": acc["env_n"], "share_of_step": e_ms * T * args.steps / ms}
+                                "frac": gbs / peaks["hbm_gbs"], "bytes_per_env_step": b_bench,
+                                "bytes_per_env_step_survey": b_survey,
+                                "frac_survey_bytes": N * b_survey / (e_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                "avg_launch_us_full_n": e_ms * 1e3,
+                                "launch_units_timed": acc["env_n"], "share_of_step": e_ms * T * args.steps / pstep}
         if acc["gae_n"]:
             g_ms = acc["gae_ms"] / acc["gae_n"]
             gbs = gae_bytes(T, N) / (g_ms / 1e3) / 1e9
             kern["gae"] = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                           "frac": gbs / peaks["hbm_gbs"], "avg_launch_us_full_n": g_ms * 1e3, "launch_units_timed": acc["gae_n"],
-                           "share_of_step": acc["gae_ms"] / ms}
-        # the event-bracketed steps run slower than the plain graph (the record nodes break the
-        # kernel-to-kernel launch path), so the bracketed actor + env durations overstate the rollout
-        # time: the rollout kernels' shares are their bracketed proportions of the rollout's part of
-        # the step (step minus GAE), and `achieved` keeps the bracketed (conservative) duration
-        if "actor_mlp" in kern and "env_step" in kern:
-            ra, re_ = kern["actor_mlp"], kern["env_step"]
-            roll = max(0.0, 1.0 - kern["gae"]["share_of_step"]) if "gae" in kern else 1.0
-            tot = ra["avg_launch_us_full_n"] + re_["avg_launch_us_full_n"]
-            infl = (ra["share_of_step"] + re_["share_of_step"]) / roll if roll > 0 else None
-            for k in (ra, re_):
-                k["share_of_step"] = roll * k["avg_launch_us_full_n"] / tot
-                k["bracket_inflation"] = infl
+                           "frac": gbs / peaks["hbm_gbs"], "bytes_per_element": 25,
+                           "bytes_per_element_survey": 17,
+                           "frac_survey_bytes": gae_bytes_survey(T, N) / (g_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                           "avg_launch_us_full_n": g_ms * 1e3, "launch_units_timed": acc["gae_n"],
+                           "share_of_step": acc["gae_ms"] / pstep}
+        # the event-bracketed steps of the profiled pass run slower than the plain graph (the record nodes
+        # break the kernel-to-kernel launch path), so `achieved` keeps the bracketed (conservative) duration
+        # and `bracket_inflation` = profiled-pass step time / headline step time
+        for k in kern.values():
+            k["bracket_inflation"] = pstep / ms if ms > 0 else None
         dom = max(kern, key=lambda k: kern[k]["share_of_step"]) if kern else None
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -429,6 +514,10 @@ def main():
             k = kern[dom]
             roofline = {"kernel": dom, "bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"],
                         "unit": k["unit"], "frac": k["frac"], "traffic": traffic, "peak_source": peaks["source"]}
+            if "peak_kind" in k:
+                roofline["peak_kind"] = k["peak_kind"]
+                roofline["frac_burst"] = k["frac_burst"]
+                roofline["frac_sustained"] = k["frac_sustained"]
         # ---- CPU baseline: the oracle as it stands, bounded sample, rank 0 at N=1 only
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -448,6 +537,13 @@ def main():
                    "sample": f"{n_s} envs x {Ts} steps of {w.name} (float64 actor {w.n_hidden}x{w.hidden} + critic + "
                              f"env step + GAE on the critic values + normalisation + fitness + select), OpenMP over "
                              f"envs, {tt:.1f} s"}
+            # the same oracle on one thread (a bounded sample of ~5 s)
+            n_1 = int(min(N, max(1, (5.0 / max(t1s * cores, 1e-9)) / Ts)))
+            t_1 = oracle_step_sample(w, market, wf, n_1, Ts, 1, env_starts, wcr)
+            cpu["single_thread"] = {"value": n_1 * Ts / t_1, "unit": UNIT, "cores": 1,
+                                    "sample": f"{n_1} envs x {Ts} steps of {w.name}, 1 thread, {t_1:.1f} s"}
+            # configs[0] (C1) in full: 16 envs x 64 steps, Dow-30 daily, actor 2x128 (the oracle-scale case)
+            cpu["c1_full"] = c1_full_oracle(cores)
         # obs0, T x (actor, env), V(s_T) pass, step bump, GAE scan + normalisation, fitness
         launches_per_step = 1 + 2 * T + 1 + 1 + 2 + 1
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

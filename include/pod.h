@@ -376,9 +376,13 @@ pod_status pod_early_stop(const double* history, int32_t len, int32_t patience, 
 pod_status pod_elite_plan(const double* fitness, int32_t P_total, int32_t k, int32_t* plan);
 
 /* One parameter-slab transfer of a plan, as seen from `rank`:
- * kind 0 = local device copy src_local -> dst_local, 1 = send slab src_local
- * to `peer`, 2 = receive into dst_local from `peer`.  Global agent g lives on
- * rank g / P_local at local index g % P_local. */
+ * kind 0 = local device copy src_local -> dst_local (before the exchange),
+ * 1 = send slab src_local to `peer`, 2 = receive into dst_local from `peer`,
+ * 3 = local device copy src_local -> dst_local after the exchange (fan-out of
+ * a slab this rank received from `peer`).  Global agent g lives on rank
+ * g / P_local at local index g % P_local.  An elite slab crosses to another
+ * rank at most once per destination rank (k = 1: one copy per rank, a
+ * broadcast), however many of that rank's slots take it. */
 typedef struct {
     int32_t kind;
     int32_t peer;
@@ -386,8 +390,9 @@ typedef struct {
     int32_t dst_local;
 } pod_transfer;
 
-/* Transfers `rank` must execute to realise `plan` (host only).  Sends and
- * receives between a pair of ranks appear in the same (ascending slot)
+/* Transfers `rank` must execute to realise `plan` (host only), in execution
+ * order: kinds 0, then the sends/receives (one NCCL group), then kind 3.  Sends
+ * and receives between a pair of ranks appear in the same (ascending slot)
  * order on both sides.  *n_ops gets the count; POD_ERR_ARG if max_ops is too
  * small or the plan is not a valid elite plan. */
 pod_status pod_elite_transfers(const int32_t* plan, int32_t P_total, int32_t P_local, int32_t rank,
@@ -407,7 +412,9 @@ pod_status pod_comm_destroy(pod_comm_t* comm);
  *      i32 [P_total];
  *   4. grouped ncclSend/ncclRecv (+ local cudaMemcpyAsync) moving elite
  *      parameter slabs into the eliminated slots of params [dev]
- *      [P_local][param_bytes] ("sending the network parameters").
+ *      [P_local][param_bytes] ("sending the network parameters"):
+ *      one transfer per (elite, destination rank), then local fan-out copies
+ *      (pod_elite_transfers).
  * Synchronous w.r.t. the plan (step 2), asynchronous for the slab moves.
  * Errors: ARG, NONFINITE, NCCL, CUDA. */
 pod_status pod_select_elite(pod_comm_t* comm, const double* fitness_local, int32_t P_local, int32_t k,

@@ -15,8 +15,6 @@
 #include <vector>
 
 #include "actor_kernel.cuh"
-#include "actor_pair_kernel.cuh"
-#include "actor_wide_kernel.cuh"
 #include "env_kernel.cuh"
 #include "fuse_kernel.cuh"
 #include "metrics_kernel.cuh"
@@ -247,6 +245,7 @@ struct pod_env {
     int32_t *tile_start, *tile_k;
     uint64_t* step;
     uint32_t* err;
+    uint32_t* h_err;     // pinned host mirror of *err, refreshed by a D2H copy at the end of every rollout
     int32_t* h_starts;   // pinned staging for reset
     cudaStream_t cap_stream;
     std::vector<GraphEntry> graphs;
@@ -389,6 +388,8 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         if (e->sm_count < 2) e->sm_count = 2;
     }
     cudaError_t ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_starts), sizeof(int32_t) * e->n_tiles);
+    if (ce == cudaSuccess) ce = cudaMallocHost(reinterpret_cast<void**>(&e->h_err), sizeof(uint32_t));
+    if (ce == cudaSuccess) *e->h_err = 0;
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
     for (int g = 0; g < POD_MAX_GROUPS && ce == cudaSuccess; ++g) {
         ce = cudaStreamCreateWithFlags(&e->gstream[g], cudaStreamNonBlocking);
@@ -398,10 +399,6 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (ce == cudaSuccess)
-        ce = cudaFuncSetAttribute(actor_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (ce == cudaSuccess)
-        ce = cudaFuncSetAttribute(actor_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(env_step_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (ce == cudaSuccess)
@@ -469,6 +466,7 @@ extern "C" pod_status pod_env_destroy(pod_env_t* e) {
     }
     if (e->fork_ev) cudaEventDestroy(e->fork_ev);
     if (e->h_starts) cudaFreeHost(e->h_starts);
+    if (e->h_err) cudaFreeHost(e->h_err);
     delete e;
     return POD_OK;
 }
@@ -547,19 +545,19 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
     }
     POD_CUDA(cudaMemcpyAsync(e->tile_start, e->h_starts, sizeof(int32_t) * e->n_tiles, cudaMemcpyHostToDevice, s));
     POD_CUDA(cudaMemsetAsync(e->step, 0, 8, s));
+    POD_CUDA(cudaMemsetAsync(e->err, 0, 4, s));   // a fresh state carries no earlier fault
     EnvArgs a = env_args(e, 2);
     a.obs_out = obs0;
     env_step_fn(e)<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
     POD_CUDA(cudaGetLastError());
     POD_CUDA(cudaStreamSynchronize(s));   // the pinned staging buffer is reused by the next reset
+    *static_cast<volatile uint32_t*>(e->h_err) = 0;
     return POD_OK;
 }
 
 // ------------------------------------------------------------ rollout
 struct RolloutPlan {
     bool injected;
-    bool pair;          // 4-CTA clusters with the 2-SM MMA (per-agent env count a multiple of 256)
-    bool wide;          // 2-CTA clusters with the 2-SM MMA, no column split (actor_wide_kernel.cuh)
     ActorMaps maps;
     ActorArgs aa;
     size_t actor_smem;
@@ -588,29 +586,24 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         const int mtiles = e->groups == 1 ? e->cfg.n_agents * aa.tiles_per_agent : (m1 - m0);
         // 4-CTA clusters (two M-tiles of one agent) share weight tiles by multicast when
         // every agent has an even number of full M-tiles and so does this launch
-        aa.mc = (!p.pair && e->mc_ok && mtiles % e->mc_ok == 0 && m0 % e->mc_ok == 0) ? e->mc_ok : 0;
+        aa.mc = (e->mc_ok && mtiles % e->mc_ok == 0 && m0 % e->mc_ok == 0) ? e->mc_ok : 0;
         aa.mtiles = mtiles;
         // persistent clusters (one per SM pair) loop over the M-tiles: the next tile's obs and first
         // weight stages load while the current tile's head runs (multi-wave batches)
-        const int ncl = (!aa.mc && !p.pair && e->persist) ? std::min(mtiles, e->sm_count / 2) : mtiles;
-        lc.gridDim = dim3(static_cast<unsigned>(p.wide ? mtiles : 2 * ncl));   // wide: one CTA per M-tile
+        const int ncl = (!aa.mc && e->persist) ? std::min(mtiles, e->sm_count / 2) : mtiles;
+        lc.gridDim = dim3(static_cast<unsigned>(2 * ncl));
         actor_ctas = static_cast<int>(lc.gridDim.x);
         lc.blockDim = dim3(ACT_THREADS);
         lc.dynamicSmemBytes = p.actor_smem;
         lc.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = aa.mc ? 2 * aa.mc : (p.pair ? 4 : 2);
+        at[0].val.clusterDim.x = aa.mc ? 2 * aa.mc : 2;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        if (p.wide)
-            cudaLaunchKernelEx(&lc, actor_wide_kernel, p.maps, aa);
-        else if (p.pair)
-            cudaLaunchKernelEx(&lc, actor_pair_kernel, p.maps, aa);
-        else
-            cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
+        cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
     };
     EnvArgs a0 = env_args(e, 1);
     a0.tile0 = t0;
@@ -632,7 +625,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             aa.mtile0 = m0;
             aa.act_out = tr->act + static_cast<int64_t>(t) * N * n;
             aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
-            aa.logp_parts = (p.pair || p.wide || !tr->logp) ? nullptr : e->logp_parts;
+            aa.logp_parts = tr->logp ? e->logp_parts : nullptr;
             aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
             aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
             aa.val_out = tr->val ? tr->val + static_cast<int64_t>(t) * N : nullptr;
@@ -648,8 +641,8 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         a.dbg_hold = tr->dbg_hold ? tr->dbg_hold + static_cast<int64_t>(t) * N * n : nullptr;
         a.dbg_cash = tr->dbg_cash ? tr->dbg_cash + static_cast<int64_t>(t) * N : nullptr;
         a.equity = tr->equity ? tr->equity + static_cast<int64_t>(t) * N : nullptr;
-        // the column-split actor leaves its log-prob partials to this step (the other variants write logp)
-        a.logp_parts = (!p.injected && !p.pair && !p.wide && tr->logp) ? e->logp_parts : nullptr;
+        // the column-split actor leaves its log-prob partials to this step
+        a.logp_parts = (!p.injected && tr->logp) ? e->logp_parts : nullptr;
         a.logp_out = a.logp_parts ? tr->logp + static_cast<int64_t>(t) * N : nullptr;
         a.gen_noise = (sampling && t + 1 < T) ? 1 : 0;   // noise for the actor launch of step t+1
         a.noise_t = t + 1;
@@ -715,6 +708,9 @@ static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const
     if (!p.injected) bump_step_kernel<<<1, 1, 0, s>>>(e->step, static_cast<uint64_t>(T));
     if (fitness_out) fitness_kernel<<<e->cfg.n_agents, 1024, 0, s>>>(e->ep_ret, e->per_agent, fitness_out);
     POD_CUDA(cudaGetLastError());
+    // publish the device error word to the pinned host mirror: the next pod_rollout refuses to run on a
+    // state that an earlier rollout has already flagged (non-finite mean action or account value)
+    POD_CUDA(cudaMemcpyAsync(e->h_err, e->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     return POD_OK;
 }
 
@@ -741,6 +737,15 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
     if (reinterpret_cast<uintptr_t>(tr->obs) % 16 != 0) return pod_fail(POD_ERR_ARG, "traj.obs must be 16-byte aligned");
     const int N = e->cfg.n_envs;
     if (static_cast<int64_t>(T + 1) * N >= (1ll << 31)) return pod_fail(POD_ERR_SHAPE, "(T+1) * N must be < 2^31");
+    {
+        // an earlier rollout of this handle that has completed on the device flagged a non-finite actor
+        // mean or account value (pod_env_check / pod_env_reset clear it)
+        const uint32_t he = *static_cast<volatile uint32_t*>(e->h_err);
+        if (he)
+            return pod_fail(POD_ERR_NONFINITE,
+                            "an earlier rollout set the device error word 0x%x (1 = non-finite actor mean, 2 = "
+                            "non-finite account value); pod_env_check or pod_env_reset clears it", he);
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     RolloutPlan p{};
     p.injected = injected_u != nullptr;
@@ -764,24 +769,14 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             st = encode_bf16(&p.maps.obs, tr->obs, 2, dims, str, box);
             if (st) return st;
         }
-        {
-            // the 2-SM (cta_group::2) variant: opt-in — its MMA phase is faster but its
-            // epilogue/synchronisation currently costs more than it saves (measured)
-            const char* pp = getenv("POD_PAIR");
-            p.pair = (e->per_agent % 256 == 0) && pp && pp[0] == '1' && !tr->val;   // pair kernel: no critic output
-            const char* pw = getenv("POD_WIDE");
-            p.wide = !p.pair && !e->mc_ok && e->groups == 1 && pw && pw[0] == '1' &&
-                     actor_wide_ok(e->per_agent, actor->n_hidden, actor->hidden, L.n_out_pad);
-        }
         const char* kpe = getenv("POD_KPB");   // experiments: POD_KPB=0 keeps one box per stage
         const bool kpb_off = kpe && kpe[0] == '0';
         for (int l = 0; l < L.n_layers; ++l) {
             const int rows = L.w_rows[l];
-            // pair: each CTA stages half of its column half; wide: half of each <= 256-row chunk
-            const int bn = p.pair ? rows / 4 : (p.wide ? actor_wide_cw(rows) / 2 : actor_bn(rows / 2));
+            const int bn = actor_bn(rows / 2);   // this CTA's column half of the layer
             const int KB = L.w_cols[l] / ACT_BK;
-            // narrow layers: several K blocks per ring stage (not with the multicast / pair variants)
-            const int kph = (bn < ACT_BN && !p.pair && !p.wide && !e->mc_ok && !kpb_off) ? actor_kpb(KB, bn, l > 0) : 1;
+            // narrow layers: several K blocks per ring stage (not with the multicast variant)
+            const int kph = (bn < ACT_BN && !e->mc_ok && !kpb_off) ? actor_kpb(KB, bn, l > 0) : 1;
             p.aa.kpb_pack |= static_cast<uint32_t>(kph) << (5 * l);
             if (kph == 1) {
                 const uint64_t dims[3] = {static_cast<uint64_t>(L.w_cols[l]), static_cast<uint64_t>(rows),
@@ -824,9 +819,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         aa.znoise = e->znoise;
         aa.err = e->err;
         aa.trace = e->trace;
-        p.actor_smem = p.wide   ? actor_wide_smem_bytes(L.k_pad, actor->hidden)
-                       : p.pair ? actor_pair_smem_bytes(L.k_pad, actor->hidden)
-                                : actor_smem_bytes(L.k_pad, actor->hidden);
+        p.actor_smem = actor_smem_bytes(L.k_pad, actor->hidden);
         if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
     }
     if (!e->use_graphs) {
@@ -958,6 +951,7 @@ extern "C" pod_status pod_env_check(pod_env_t* e, void* stream) {
     uint32_t h = 0;
     POD_CUDA(cudaStreamSynchronize(s));
     POD_CUDA(cudaMemcpy(&h, e->err, 4, cudaMemcpyDeviceToHost));
+    *static_cast<volatile uint32_t*>(e->h_err) = 0;
     if (h) {
         POD_CUDA(cudaMemset(e->err, 0, 4));
         return pod_fail(POD_ERR_NONFINITE, "device error word 0x%x (1 = non-finite actor mean, 2 = non-finite account value)", h);
@@ -1062,11 +1056,15 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
         const int cpw = nchunks <= GAE_SEG_MAX ? 1 : GAE_CPW_MAX;
         const int seg = (nchunks + cpw - 1) / cpw;
         const int want = static_cast<int>(gae_seg_smem_bytes(seg, cpw));
+        // the opt-in is a per-device function attribute: track what each device has been granted
         static std::mutex seg_mu;
-        static int seg_attr = 0;   // dynamic shared memory granted so far
+        static int seg_attr[64] = {};   // dynamic shared memory granted so far, per device ordinal
+        int cur_dev = 0;
+        POD_CUDA(cudaGetDevice(&cur_dev));
+        if (cur_dev < 0 || cur_dev >= 64) return pod_fail(POD_ERR_UNSUPPORTED, "device ordinal %d >= 64", cur_dev);
         {
             std::lock_guard<std::mutex> lk(seg_mu);
-            if (seg_attr < want) {
+            if (seg_attr[cur_dev] < want) {
                 cudaError_t ce = cudaFuncSetAttribute(gae_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
                 if (ce != cudaSuccess) {
                     cudaFuncAttributes fa;
@@ -1081,7 +1079,7 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
                                     want, cudaGetErrorString(ce), cudaGetErrorString(ce2), fa.sharedSizeBytes,
                                     fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock, fa.numRegs, optin);
                 }
-                seg_attr = want;
+                seg_attr[cur_dev] = want;
             }
         }
         gae_seg_kernel<<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw), stream>>>(
@@ -1090,13 +1088,20 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
         return POD_OK;
     }
     const unsigned blocks = static_cast<unsigned>((groups + GAE_WARPS - 1) / GAE_WARPS);
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(gae_smem_bytes()));
-    });
-    POD_CUDA(attr_err);
+    {
+        // per-device opt-in (pod_gae may run on any device without an env handle there)
+        static std::mutex gae_mu;
+        static bool gae_attr[64] = {};
+        int cur_dev = 0;
+        POD_CUDA(cudaGetDevice(&cur_dev));
+        if (cur_dev < 0 || cur_dev >= 64) return pod_fail(POD_ERR_UNSUPPORTED, "device ordinal %d >= 64", cur_dev);
+        std::lock_guard<std::mutex> lk(gae_mu);
+        if (!gae_attr[cur_dev]) {
+            POD_CUDA(cudaFuncSetAttribute(gae_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(gae_smem_bytes())));
+            gae_attr[cur_dev] = true;
+        }
+    }
     gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), stream>>>(maps, rew, val, done, boot, T, N, gamma, lambda,
                                                                        adv, ret, use_bulk, stats);
     POD_CUDA(cudaGetLastError());

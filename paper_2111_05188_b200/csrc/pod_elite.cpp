@@ -45,23 +45,44 @@ extern "C" pod_status pod_elite_transfers(const int32_t* plan, int32_t P, int32_
         const int s = plan[g];
         if (s < 0 || s >= P || plan[s] != s) return pod_fail(POD_ERR_ARG, "plan[%d]=%d is not an elite slot", g, s);
     }
+    // An elite slab crosses to a remote rank at most once per (elite, destination rank): the first
+    // eliminated slot of that rank which takes the elite (ascending slot order, the same walk on every
+    // rank, so sends and receives pair up in order) receives it; the rank's later slots taking the same
+    // elite are filled by a local copy from that slot once the exchange has landed (kind 3).
     int cnt = 0;
+    auto emit = [&](pod_transfer op) -> bool {
+        if (cnt >= max_ops) return false;
+        ops[cnt++] = op;
+        return true;
+    };
+    std::vector<int32_t> landed(static_cast<size_t>(P) * (P / P_local), -1);   // [src][dest rank] -> local slot
+    // pass 0: local copies of local elites (kind 0)
+    for (int g = rank * P_local; g < (rank + 1) * P_local; ++g) {
+        const int src = plan[g];
+        if (src != g && src / P_local == rank && !emit(pod_transfer{0, rank, src % P_local, g % P_local}))
+            return pod_fail(POD_ERR_ARG, "max_ops %d too small", max_ops);
+    }
+    // pass 1: sends (1) and receives (2), ascending slot order over the whole population
     for (int g = 0; g < P; ++g) {
         const int src = plan[g];
         if (src == g) continue;
         const int dr = g / P_local, sr = src / P_local;
-        pod_transfer op{};
-        if (dr == rank && sr == rank) {
-            op = pod_transfer{0, rank, src % P_local, g % P_local};
-        } else if (sr == rank) {
-            op = pod_transfer{1, dr, src % P_local, -1};
-        } else if (dr == rank) {
-            op = pod_transfer{2, sr, -1, g % P_local};
-        } else {
-            continue;
-        }
-        if (cnt >= max_ops) return pod_fail(POD_ERR_ARG, "max_ops %d too small", max_ops);
-        ops[cnt++] = op;
+        if (dr == sr) continue;
+        int32_t& first = landed[static_cast<size_t>(src) * (P / P_local) + dr];
+        if (first >= 0) continue;   // this rank already receives the elite: fanned out in pass 2
+        first = g % P_local;
+        if (sr == rank && !emit(pod_transfer{1, dr, src % P_local, -1}))
+            return pod_fail(POD_ERR_ARG, "max_ops %d too small", max_ops);
+        if (dr == rank && !emit(pod_transfer{2, sr, -1, g % P_local}))
+            return pod_fail(POD_ERR_ARG, "max_ops %d too small", max_ops);
+    }
+    // pass 2: local fan-out of received slabs (kind 3), after the exchange
+    for (int g = rank * P_local; g < (rank + 1) * P_local; ++g) {
+        const int src = plan[g];
+        if (src == g || src / P_local == rank) continue;
+        const int32_t first = landed[static_cast<size_t>(src) * (P / P_local) + rank];
+        if (first != g % P_local && !emit(pod_transfer{3, src / P_local, first, g % P_local}))
+            return pod_fail(POD_ERR_ARG, "max_ops %d too small", max_ops);
     }
     *n_ops = cnt;
     return POD_OK;
@@ -212,7 +233,7 @@ extern "C" pod_status pod_select_elite(pod_comm_t* c, const double* fitness_loca
             return pod_fail(POD_ERR_CUDA, "local elite copy failed");
     }
     bool any_p2p = false;
-    for (int i = 0; i < nops; ++i) any_p2p |= c->ops[static_cast<size_t>(i)].kind != 0;
+    for (int i = 0; i < nops; ++i) any_p2p |= c->ops[static_cast<size_t>(i)].kind == 1 || c->ops[static_cast<size_t>(i)].kind == 2;
     if (any_p2p) {
         NCCL_TRY(api->GroupStart());
         for (int i = 0; i < nops; ++i) {
@@ -223,6 +244,13 @@ extern "C" pod_status pod_select_elite(pod_comm_t* c, const double* fitness_loca
                 NCCL_TRY(api->Recv(base + op.dst_local * param_bytes, param_bytes, ncclUint8, op.peer, c->comm, s));
         }
         NCCL_TRY(api->GroupEnd());
+    }
+    for (int i = 0; i < nops; ++i) {   // fan-out of received slabs, stream-ordered after the receives
+        const pod_transfer& op = c->ops[static_cast<size_t>(i)];
+        if (op.kind == 3 &&
+            cudaMemcpyAsync(base + op.dst_local * param_bytes, base + op.src_local * param_bytes, param_bytes,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return pod_fail(POD_ERR_CUDA, "elite fan-out copy failed");
     }
     return POD_OK;
 }

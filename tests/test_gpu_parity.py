@@ -344,6 +344,92 @@ def test_full_size_c3_sampled_rows():
     assert (tr.dbg_cash >= 0).all() and (tr.dbg_hold >= 0).all()
 
 
+@pytest.mark.parametrize("agents", [1, 8])
+def test_full_size_c5_sampled_rows(agents):
+    """C5 launch configuration (65,536 envs, n = 100, 3x512, default switches): the dense programmatic-
+    dependent env-step launch (2,048 tiles >= 7 per SM) and the persistent actor (512 M-tiles on 74 clusters,
+    ~7 tiles per cluster: barrier phases and TMEM buffers wrap around) against the oracle on sampled rows from
+    the first wave, the second wave and the last persistent tiles of each cluster; agents = 8 switches agent
+    inside the persistent loop (C4's population shape)."""
+    N = 65536
+    c = Case(n=100, f=3, T_data=60_000, N=N, H=3000, n_agents=agents, seed=5193, dt=1 / (252 * 390))
+    aws, params, actor = _actor(c, 3, 512, n_agents=agents)
+    T = 4
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, debug=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    c.env.check()
+    # M-tiles (128 envs): 0 and 73 (first wave), 74 and 147 (second wave), 438..511 (the last tile of every
+    # persistent cluster), plus env tiles (32 envs) at both ends of the PDL grid
+    mt = [0, 73, 74, 147, 148, 300, 438, 480, 510, 511]
+    rows = np.unique(np.concatenate([[m * 128 + o for m in mt for o in (0, 45, 127)], [31, 32, 65503, 65535]]))
+    obs_g = bf16_to_f64(tr.obs)[:, rows, : c.obs_dim]
+    mu_g = tr.mu.cpu().numpy()[:, rows].astype(np.float64)
+    raw_g = tr.act.cpu().numpy()[:, rows].astype(np.float64)
+    logp_g = tr.logp.cpu().numpy()[:, rows].astype(np.float64)
+    per_agent = N // agents
+    for t in range(T):
+        for k, e in enumerate(rows):
+            aw = aws[int(e) // per_agent]
+            w = oracle.actor_flat(aw.W, aw.b, aw.log_std)
+            ls = aw.log_std.astype(np.float64)
+            mu_check(mu_g[t, k][None, :], oracle.actor_mu(w, obs_g[t, k][None, :], 3, 512, 100))
+            z_o = oracle.normals(c.cfg.seed, c.cfg.env_offset + int(e), t, 100)
+            z_g = (raw_g[t, k] - mu_g[t, k]) / np.exp(ls)
+            assert np.all(np.abs(z_g - z_o) <= 2e-5 * np.abs(z_o) + 5e-4), (t, e)
+            lp_o = float(np.sum(-0.5 * z_o * z_o - ls - 0.5 * math.log(2 * math.pi)))
+            terms = float(np.sum(0.5 * z_o * z_o + np.abs(ls) + 0.5 * math.log(2 * math.pi)))
+            assert abs(logp_g[t, k] - lp_o) <= 1e-5 * terms + 1e-4, (t, e)
+    a_g = tr.dbg_aint.cpu().numpy()
+    o = oracle.Env(c.market.close, c.market.feat, len(rows), **dict(c.kw, n_agents=1))
+    o.reset(c.env_starts()[rows])
+    out = o.rollout(T, "replay", a_rep=np.ascontiguousarray(a_g[:, rows]), want=("obs", "rew", "done", "hold", "cash"))
+    np.testing.assert_array_equal(tr.dbg_hold.cpu().numpy()[:, rows], out["hold"])
+    np.testing.assert_array_equal(tr.dbg_cash.cpu().numpy()[:, rows], out["cash"])
+    np.testing.assert_array_equal(tr.rew.cpu().numpy()[:, rows], out["rew"].astype(np.float32))
+    np.testing.assert_array_equal(tr.done.cpu().numpy()[:, rows], out["done"])
+    assert_obs_close(tr.obs[:, rows], out["obs"], c.obs_dim)
+    assert (tr.dbg_cash >= 0).all() and (tr.dbg_hold >= 0).all()
+    assert torch.isfinite(tr.mu).all() and torch.isfinite(tr.logp).all()
+
+
+@pytest.mark.parametrize("where", ["head_bias", "hidden_weight"])
+def test_nonfinite_weights_set_error_word(where):
+    """S:L288 / §8(b): a non-finite actor mean sets the device error word; pod_env_check reports
+    POD_ERR_NONFINITE (and clears it), and a later pod_rollout on the flagged state refuses to run with
+    POD_ERR_NONFINITE until the word is cleared; pod_env_reset also clears it."""
+    c = Case(n=30, f=3, T_data=400, N=256, H=50, seed=71)
+    aws, params, actor = _actor(c, 2, 128)
+    L = api.actor_layout(c.cfg, 2, 128)
+    raw = params.view(torch.uint8)
+    if where == "head_bias":
+        off = L.b_offset[L.n_layers - 1] + 4 * 3   # b_L[3] = NaN: mu_3 of every env
+        raw[0, off : off + 4] = torch.tensor([0, 0, 192, 127], dtype=torch.uint8)
+    else:
+        off = L.w_offset[1]   # W_1[0][0] = +inf (bf16 0x7F80): propagates to the mean through the head
+        raw[0, off : off + 2] = torch.tensor([128, 127], dtype=torch.uint8)
+    tr = api.Trajectory.allocate(3, c.N, c.n, c.k_pad)
+    c.env.reset(c.starts)
+    c.env.rollout(3, tr, actor=actor)
+    with pytest.raises(PodError) as ei:
+        c.env.check()
+    assert ei.value.status == 7
+    c.env.check()   # cleared
+    # the next rollout after a flagged one (completed on the device) refuses to run
+    c.env.rollout(1, tr, actor=actor)
+    torch.cuda.synchronize()
+    with pytest.raises(PodError) as ei:
+        c.env.rollout(1, tr, actor=actor)
+    assert ei.value.status == 7
+    # reset clears the word; with finite weights the rollout is accepted again
+    _, params2, actor2 = _actor(c, 2, 128)
+    c.env.reset(c.starts)
+    c.env.rollout(2, tr, actor=actor2)
+    torch.cuda.synchronize()
+    c.env.rollout(2, tr, actor=actor2)
+    c.env.check()
+
+
 def test_profile_events_in_graph():
     c = Case(n=30, f=3, T_data=300, N=256, H=40)
     aws, params, actor = _actor(c, 2, 128)
@@ -435,23 +521,6 @@ def test_weight_multicast_bit_identical(mcg, monkeypatch):
         outs.append(tr)
     for name in ("obs", "act", "logp", "rew", "done", "dbg_hold", "dbg_cash", "mu"):
         assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
-
-
-def test_pair_kernel_matches_single_cta_kernel(monkeypatch):
-    """The 2-SM (cta_group::2) actor and the 2-CTA column-split actor agree (same K order)."""
-    outs = []
-    for pp in ("0", "1"):
-        monkeypatch.setenv("POD_PAIR", pp)
-        c = Case(n=100, f=3, T_data=2000, N=512, H=300, seed=14, dt=1 / (252 * 390))
-        aws, params, actor = _actor(c, 3, 512)
-        tr = api.Trajectory.allocate(3, 512, 100, c.k_pad, debug=True)
-        c.env.reset(c.starts)
-        c.env.rollout(3, tr, actor=actor)
-        c.env.check()
-        outs.append(tr)
-    mu0 = outs[0].mu.cpu().numpy().astype(np.float64)
-    mu1 = outs[1].mu.cpu().numpy().astype(np.float64)
-    np.testing.assert_allclose(mu1, mu0, rtol=1e-5, atol=1e-5)
 
 
 @pytest.mark.parametrize("n,nh,hid", [(100, 3, 512), (30, 2, 128), (32, 2, 256)])
@@ -784,31 +853,6 @@ def test_ppo_concurrent_learners_on_streams():
         a, b = conc[k].master.cpu().numpy(), solo[k].master.cpu().numpy()
         assert np.isfinite(a).all()
         assert (np.abs(a - b) > 1e-2 * 1e-3).mean() < 0.01
-
-
-@pytest.mark.parametrize("hidden", [512, 128])
-def test_wide_actor_matches_column_split(tmp_path, hidden):
-    """The opt-in 2-SM wide actor (POD_WIDE=1, actor_wide_kernel) against the default column-split actor
-    on the same seeded step (each process reads the switch at plan time): mu and V agree to bf16-level
-    accumulation differences (different K order inside the float32 accumulators), logp likewise.  The
-    narrow head (n_out_pad = 32 < one 64-column atom) once raced its first atom: caught here."""
-    import os
-    import subprocess
-
-    outs = {}
-    for flag in ("0", "1"):
-        path = tmp_path / f"wide{flag}.npz"
-        env = dict(os.environ, POD_WIDE=flag)
-        subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "wide_actor_run.py"), str(path),
-                        str(hidden)],
-                       check=True, env=env, cwd=os.path.dirname(os.path.dirname(__file__)), timeout=300)
-        outs[flag] = np.load(path)
-    for k in ("mu", "val"):
-        a, b = outs["0"][k].astype(np.float64), outs["1"][k].astype(np.float64)
-        scale = np.abs(a).max() + 1e-12
-        assert np.abs(a - b).max() <= 1e-2 * scale, (k, np.abs(a - b).max() / scale)
-    la, lb = outs["0"]["logp"].astype(np.float64), outs["1"]["logp"].astype(np.float64)
-    assert np.abs(la - lb).max() <= 1e-4 * np.abs(la).max()
 
 
 # ----------------------------------------------------------------- shape sweep (edge configurations)

@@ -119,26 +119,50 @@ def test_elite_plan_matches_oracle():
 
 
 def _apply_transfers(slabs_per_rank, plan, P_local):
-    """Reference semantics of the routing: every rank's slabs after the moves."""
+    """Reference semantics of the routing: every rank's slabs after the moves (kind 0 local copies, then the
+    sends/receives matched in order per rank pair, then kind 3 fan-out copies of received slabs)."""
     out = [s.copy() for s in slabs_per_rank]
     R = len(slabs_per_rank)
+    ops = [api.pod_elite_transfers(plan, P_local, r) for r in range(R)]
     for r in range(R):
-        for kind, peer, src, dst in api.pod_elite_transfers(plan, P_local, r):
+        kinds = [k for k, _, _, _ in ops[r]]
+        assert kinds == sorted(kinds, key=lambda k: {0: 0, 1: 1, 2: 1, 3: 2}[k])   # execution order
+        for kind, peer, src, dst in ops[r]:
             if kind == 0:
                 out[r][dst] = slabs_per_rank[r][src]
-            elif kind == 2:
-                # the matching send on `peer` carries the slab of the plan's source
-                pass
-    # receives: match each rank's recv list against the peer's send list in order
     for r in range(R):
-        recvs = [(p, d) for k, p, s, d in api.pod_elite_transfers(plan, P_local, r) if k == 2]
+        recvs = [(p, d) for k, p, s, d in ops[r] if k == 2]
         for peer in range(R):
-            sends = [s for k, p, s, d in api.pod_elite_transfers(plan, P_local, peer) if k == 1 and p == r]
+            sends = [s for k, p, s, d in ops[peer] if k == 1 and p == r]
             mine = [d for p, d in recvs if p == peer]
             assert len(sends) == len(mine)
             for s, d in zip(sends, mine):
                 out[r][d] = slabs_per_rank[peer][s]
+    for r in range(R):
+        for kind, peer, src, dst in ops[r]:
+            if kind == 3:
+                out[r][dst] = out[r][src]
     return out
+
+
+def test_elite_slab_crosses_once_per_rank():
+    """k = 1 (the paper's experiment): the elite's slab leaves its rank once per other rank (a
+    broadcast), not once per eliminated slot; the other slots of each rank are filled by local copies."""
+    R, P_local = 8, 8
+    J = np.arange(R * P_local, dtype=float)   # agent 63 (rank 7) is the elite
+    plan = api.pod_elite_plan(J, 1)
+    sends = [op for op in api.pod_elite_transfers(plan, P_local, 7) if op[0] == 1]
+    assert sorted(p for _, p, _, _ in sends) == list(range(7))
+    for r in range(7):
+        ops = api.pod_elite_transfers(plan, P_local, r)
+        assert [k for k, _, _, _ in ops].count(2) == 1 and [k for k, _, _, _ in ops].count(3) == P_local - 1
+    # k = P/2 with every rank needing elites from every other rank: at most one receive per (elite, rank)
+    J = np.random.default_rng(5).normal(size=R * P_local)
+    plan = api.pod_elite_plan(J, R * P_local // 2)
+    for r in range(R):
+        rec = [(p, d) for k, p, s, d in api.pod_elite_transfers(plan, P_local, r) if k == 2]
+        srcs = [plan[r * P_local + d] for _, d in rec]
+        assert len(srcs) == len(set(srcs))
 
 
 def test_transfers_realise_the_plan():
@@ -177,10 +201,12 @@ def _gloo_worker(rank, world, port, q):
                 new[dst] = slabs[src]
             elif kind == 1:
                 dist.send(slabs[src].contiguous(), peer)
-            else:
+            elif kind == 2:
                 buf = torch.empty(W)
                 dist.recv(buf, peer)
                 new[dst] = buf
+            else:
+                new[dst] = new[src]
         allp = [torch.zeros(1, dtype=torch.int32) for _ in range(world)]
         q.put((rank, plan.tolist(), new[:, 0].tolist(), J.tolist()))
     finally:
