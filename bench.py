@@ -495,11 +495,19 @@ def main():
                            "frac_survey_bytes": gae_bytes_survey(T, N) / (g_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
                            "avg_launch_us_full_n": g_ms * 1e3, "launch_units_timed": acc["gae_n"],
                            "share_of_step": acc["gae_ms"] / pstep}
-        # the event-bracketed steps of the profiled pass run slower than the plain graph (the record nodes
-        # break the kernel-to-kernel launch path), so `achieved` keeps the bracketed (conservative) duration
-        # and `bracket_inflation` = profiled-pass step time / headline step time
-        for k in kern.values():
-            k["bracket_inflation"] = pstep / ms if ms > 0 else None
+        # the event-bracketed launches of the profiled pass run slower than in the plain graph (the record
+        # nodes break the kernel-to-kernel launch path), so `achieved` keeps the bracketed (conservative)
+        # duration; the rollout kernels' `share_of_step` is their bracketed proportion of the rollout's part
+        # of the headline step (step minus GAE), `bracket_inflation` = bracketed (actor + env) time per step
+        # over that part
+        if "actor_mlp" in kern and "env_step" in kern:
+            ra, re_ = kern["actor_mlp"], kern["env_step"]
+            roll = max(0.0, 1.0 - kern["gae"]["share_of_step"]) if "gae" in kern else 1.0
+            tot = ra["avg_launch_us_full_n"] + re_["avg_launch_us_full_n"]
+            infl = (ra["share_of_step"] + re_["share_of_step"]) / roll if roll > 0 else None
+            for k in (ra, re_):
+                k["share_of_step"] = roll * k["avg_launch_us_full_n"] / tot
+                k["bracket_inflation"] = infl
         dom = max(kern, key=lambda k: kern[k]["share_of_step"]) if kern else None
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -528,17 +536,19 @@ def main():
             wf = oracle.actor_flat(agents[0].W, agents[0].b, agents[0].log_std)
             wcr = np.append(agents[0].w_v.astype(np.float64), agents[0].b_v)
             env_starts = np.repeat(starts, 32)[:N]
-            Ts = 4
             t1s = oracle_step_sample(w, market, wf, cores, 1, cores, env_starts, wcr)
-            n_s = int(min(N, max(cores, (15.0 / max(t1s, 1e-9)) * cores / Ts)))
+            # ~10 s of all-core work: all N envs if they fit, for as many steps (4..T) as fit
+            per_env_step = t1s / cores   # wall seconds per env-step with `cores` threads
+            n_s = int(min(N, max(cores, 10.0 / max(per_env_step, 1e-9) / 4)))
             n_s = max(cores, n_s // cores * cores)
+            Ts = int(min(T, max(4, 10.0 / max(per_env_step * n_s, 1e-9))))
             tt = oracle_step_sample(w, market, wf, n_s, Ts, cores, env_starts, wcr)
             cpu = {"value": n_s * Ts / tt, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": f"{n_s} envs x {Ts} steps of {w.name} (float64 actor {w.n_hidden}x{w.hidden} + critic + "
                              f"env step + GAE on the critic values + normalisation + fitness + select), OpenMP over "
                              f"envs, {tt:.1f} s"}
             # the same oracle on one thread (a bounded sample of ~5 s)
-            n_1 = int(min(N, max(1, (5.0 / max(t1s * cores, 1e-9)) / Ts)))
+            n_1 = int(min(N, max(1, 5.0 / max(t1s, 1e-9) / Ts)))   # one thread: t1s per env-step
             t_1 = oracle_step_sample(w, market, wf, n_1, Ts, 1, env_starts, wcr)
             cpu["single_thread"] = {"value": n_1 * Ts / t_1, "unit": UNIT, "cores": 1,
                                     "sample": f"{n_1} envs x {Ts} steps of {w.name}, 1 thread, {t_1:.1f} s"}

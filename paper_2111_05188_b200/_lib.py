@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpod.so")
+LIB_PATH = os.environ.get("POD_LIB_PATH") or os.path.join(HERE, "libpod.so")   # override: A/B experiments only
 MAX_HIDDEN = 4
 
 STATUS = {0: "POD_OK", 1: "POD_ERR_ARG", 2: "POD_ERR_SHAPE", 3: "POD_ERR_RANGE", 4: "POD_ERR_WORKSPACE",

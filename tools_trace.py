@@ -20,7 +20,9 @@ buf = torch.zeros(grid * 64, dtype=torch.int64, device="cuda")
 ebuf = torch.zeros(env.n_tiles * 8, dtype=torch.int64, device="cuda")
 _lib.load().pod_debug_trace(env.h, C.c_void_p(buf.data_ptr()), C.c_void_p(ebuf.data_ptr()))
 env.reset(synth.tile_starts(env.n_tiles, w.T_data, min(w.horizon, w.T_data - 2), 1))
-for _ in range(3):
+# argv[2]: rollouts of T = 4 steps before the traced one (the trace keeps the last launch): a few dozen put the
+# envs in an episode's steady state (cash spent within the first buys of each step)
+for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     env.rollout(T, tr, actor=actor)
 torch.cuda.synchronize()
 b = buf.view(grid, 64).cpu().numpy().astype(np.int64)
@@ -47,7 +49,7 @@ erel = eb - eb[:, :1]
 for k, nm in enumerate(["start", "staged", "sells_done", "buys_done", "ledger_done", "rows_staged", "end"]):
     col = erel[:, k]
     print(f"env {nm:14s} median {int(np.median(col)):8d}  min {int(col.min()):8d}  max {int(col.max()):8d}")
-print("env slow-buy tickers per warp: median", int(np.median(eb[:, 7])), "max", int(eb[:, 7].max()))
+print("env trace slot 7: median", int(np.median(eb[:, 7])), "max", int(eb[:, 7].max()))
 
 lead = rel[0::2] if rel[1::2, 1].max() == 0 and rel[0::2, 1].max() > 0 else rel
 print("L0 stage ready (MMA side):", [int(np.median(lead[:, 32 + q])) for q in range(16)])
