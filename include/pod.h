@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define POD_ABI_VERSION 2
+#define POD_ABI_VERSION 3
 #define POD_ENV_TILE 32      /* envs per tile: one warp; a tile shares its episode start row */
 #define POD_MAX_HIDDEN_LAYERS 4
 
@@ -297,7 +297,10 @@ typedef struct {
     float adam_beta1;      /* 0.9                                            */
     float adam_beta2;      /* 0.999                                          */
     float adam_eps;        /* 1e-8                                           */
-    float reserved;
+    int32_t fp32_operands; /* 0: bf16 operands on the tcgen05 tensor cores (the
+                            * rollout slab's weights, bf16 activations / deltas,
+                            * f32 accumulate); 1: float32 operands on the float32
+                            * reference core (master weights; for parity checks) */
 } pod_ppo_hparams;
 
 /* Workspace bytes of pod_ppo_update for minibatches of `batch` rows (host). */
@@ -311,11 +314,17 @@ pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, i
  *   rho = exp(logp_theta(raw | s) - logp_old),
  *   L = -mean[min(rho A, clip(rho, 1-eps, 1+eps) A)] - c_ent H(pi)
  *       + c_v mean[(V(s) - R)^2],   H(pi) = sum_i (log sigma_i + (1 + ln 2 pi)/2),
- * the gradient of L (forward + backward with bf16 x bf16 -> float32 tensor-core
- * GEMMs on cuBLAS: the weights are the bf16 rollout slab, kept equal to the
- * rounded float32 master after every step) and one Adam step (bias-corrected,
- * step t = adam_t + j + 1):  m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
+ * the gradient of L (forward + backward as this library's GEMM kernels: with
+ * hp->fp32_operands == 0, bf16 x bf16 -> float32 on the tcgen05 tensor cores,
+ * the weights being the bf16 rollout slab, kept equal to the rounded float32
+ * master after every step; with 1, float32 operands on the CUDA cores) and one
+ * Adam step (bias-corrected, step t = adam_t + j + 1):
+ *   m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
  *   theta <- theta - lr (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps).
+ * A minibatch whose loss is not finite (divergence) sets the
+ * workspace's error word and is not applied (nor are the call's later
+ * minibatches); pod_ppo_check reports it, and the next pod_ppo_update on the
+ * same workspace returns POD_ERR_NONFINITE until pod_ppo_check has cleared it.
  * Afterwards the agent's rollout slab `params` (pod_actor_layout; agent 0 of
  * the slab array) is rewritten from theta (bf16 weights, RNE).
  *   master, adam_m, adam_v [dev] f32 [layout.n_elems] (pod_fuse_pods order), in/out;
@@ -331,16 +340,22 @@ pod_status pod_ppo_workspace_size(const pod_env_config* cfg, int32_t n_hidden, i
  * given set of pointers and sizes (adam_t, the hyper-parameters and the stream
  * excepted: they are passed through device memory, so schedules replay the same
  * graph) and replayed by later calls (library-owned, 16 per thread,
- * least recently used evicted); the calling thread's first call also creates
- * its cuBLAS handle (the only allocation).  cuBLAS scratch lives in `ws`, so
- * learners with distinct buffers may run concurrently on different streams.
- * POD_PPO_GRAPH=0 launches eagerly instead.  Stream-ordered.  Errors: ARG, SHAPE, UNSUPPORTED, CUDA. */
+ * least recently used evicted); the first call on a workspace allocates its
+ * 4-byte pinned error mirror.  All scratch lives in `ws`, so learners with
+ * distinct buffers may run concurrently on different streams.
+ * POD_PPO_GRAPH=0 launches eagerly instead.  Stream-ordered.
+ * Errors: ARG, SHAPE, UNSUPPORTED, CUDA, NONFINITE (an earlier loss, above). */
 pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, int32_t act,
                           const pod_ppo_hparams* hp, float* master, float* adam_m, float* adam_v, int64_t adam_t,
                           void* params, size_t param_bytes, const uint16_t* obs, const float* act_raw,
                           const float* logp_old, const float* adv, const float* ret, int64_t M,
                           const int32_t* perm, int32_t batch, int32_t n_minibatches, double* losses,
                           float* grad_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Synchronise `stream`, then report (and clear) the learner error word of
+ * workspace `ws`: POD_ERR_NONFINITE if a minibatch loss of an earlier
+ * pod_ppo_update on it was not finite (the caller aborts the pod). */
+pod_status pod_ppo_check(void* ws, void* stream);
 
 /* ----------------------------------------------------------- evaluator */
 /* Backtest metrics of one account-value curve per env (§5.2

@@ -341,17 +341,34 @@ def ppo_unflatten(theta, k_pad, hidden, n_hidden, n_out_pad):
     return Ws, bs, ls
 
 
-def ppo_loss_grad(theta, dims, obs, act_raw, logp_old, adv, ret, eps, c_ent, c_v, act=0):
+def bf16_round(x):
+    """Round to bfloat16 (round to nearest, ties to even, on the float32 value: the precision model of a
+    float32 result stored as a bf16 operand), returned as float64."""
+    u = np.ascontiguousarray(np.asarray(x, dtype=np.float32)).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def ppo_loss_grad(theta, dims, obs, act_raw, logp_old, adv, ret, eps, c_ent, c_v, act=0, bf16_operands=False,
+                  magnitudes=False):
     """Minibatch loss L = -mean(min(rho A, clip(rho, 1-eps, 1+eps) A)) - c_ent H + c_v mean((V - R)^2),
     H = sum_i (log sigma_i + (1 + ln 2 pi)/2), and its analytic gradient (backpropagation written out; the
     min's derivative is that of rho A when rho A <= clip(rho) A, else 0).  dims = (k_pad, hidden, n_hidden,
-    n, n_out_pad).  Returns (L, grad [same layout as theta], (sum objective, sum (V-R)^2, H))."""
+    n, n_out_pad).  Returns (L, grad [same layout as theta], (sum objective, sum (V-R)^2, H)).
+    bf16_operands (DESIGN R#27): the same computation with the operands of every product rounded to bf16 as
+    the tensor-core learner stores them — each hidden activation X_{l+1} after its nonlinearity, and each
+    delta before it enters the weight- and input-gradient products (the bias gradients sum the unrounded
+    delta; the head output Z stays unrounded).
+    magnitudes: also return, in the layout of grad, the sums of the absolute values of the terms each
+    gradient entry is summed from (|delta_l|^T |X_l|, sum |delta_l|, sum |coef (z^2 - 1)| + c_ent): the
+    scale of an elementwise tolerance for a float implementation of the same sums."""
     k_pad, hidden, n_hidden, n, n_out_pad = dims
     Ws, bs, ls = ppo_unflatten(theta, k_pad, hidden, n_hidden, n_out_pad)
+    rnd = bf16_round if bf16_operands else (lambda a: a)
     X = [np.asarray(obs, dtype=np.float64)]
     f = (lambda z: np.maximum(z, 0.0)) if act == 0 else np.tanh
     for l in range(n_hidden):
-        X.append(f(X[-1] @ Ws[l].T + bs[l]))
+        X.append(rnd(f(X[-1] @ Ws[l].T + bs[l])))
     Z = X[-1] @ Ws[-1].T + bs[-1]
     B = Z.shape[0]
     mu, V = Z[:, :n], Z[:, n]
@@ -374,16 +391,27 @@ def ppo_loss_grad(theta, dims, obs, act_raw, logp_old, adv, ret, eps, c_ent, c_v
     dZ[:, n] = 2.0 * c_v * (V - R) / B
     g_ls = np.zeros(n_out_pad)
     g_ls[:n] = (coef[:, None] * (z * z - 1.0)).sum(axis=0) - c_ent
+    m_ls = np.zeros(n_out_pad)
+    m_ls[:n] = (np.abs(coef)[:, None] * np.abs(z * z - 1.0)).sum(axis=0) + c_ent
     gW, gb = [None] * (n_hidden + 1), [None] * (n_hidden + 1)
+    mW, mb = [None] * (n_hidden + 1), [None] * (n_hidden + 1)
     d = dZ
     for l in range(n_hidden, -1, -1):
-        gW[l] = d.T @ X[l]
+        dr = rnd(d)
+        gW[l] = dr.T @ X[l]
         gb[l] = d.sum(axis=0)
+        if magnitudes:
+            mW[l] = np.abs(dr).T @ np.abs(X[l])
+            mb[l] = np.abs(d).sum(axis=0)
         if l > 0:
-            dx = d @ Ws[l]
+            dx = dr @ Ws[l]
             d = dx * ((X[l] > 0.0) if act == 0 else (1.0 - X[l] ** 2))
     grad = np.concatenate([g.ravel() for g in gW] + [g.ravel() for g in gb] + [g_ls])
-    return Lval, grad, (float(obj.sum()), float(((V - R) ** 2).sum()), H)
+    sums = (float(obj.sum()), float(((V - R) ** 2).sum()), H)
+    if magnitudes:
+        mag = np.concatenate([m.ravel() for m in mW] + [m.ravel() for m in mb] + [m_ls])
+        return Lval, grad, sums, mag
+    return Lval, grad, sums
 
 
 def adam_step(theta, m, v, g, t, lr, b1=0.9, b2=0.999, eps=1e-8):

@@ -30,7 +30,7 @@ def nvcc_cmd(out: str = LIB):
     return [nvcc, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
             "-Xcompiler", "-fPIC,-Wall", "-Xptxas", "-v", "-shared",
             "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
-            "-o", out] + SOURCES + ["-ldl", "-L/usr/local/cuda/lib64", "-lcublas"]
+            "-o", out] + SOURCES + ["-ldl"]
 
 
 def needs_build() -> bool:

@@ -45,7 +45,7 @@ class ActorLayout(C.Structure):
 class PpoHparams(C.Structure):
     _fields_ = [("ratio_clip", C.c_float), ("entropy_coef", C.c_float), ("value_coef", C.c_float),
                 ("learning_rate", C.c_float), ("adam_beta1", C.c_float), ("adam_beta2", C.c_float),
-                ("adam_eps", C.c_float), ("reserved", C.c_float)]
+                ("adam_eps", C.c_float), ("fp32_operands", C.c_int32)]
 
 
 class Traj(C.Structure):
@@ -60,7 +60,7 @@ class Transfer(C.Structure):
 
 EXPORTS = ["pod_status_string", "pod_last_error", "pod_abi_version", "pod_actor_layout_get",
            "pod_env_workspace_size", "pod_env_create", "pod_env_destroy", "pod_env_reset", "pod_rollout",
-           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan", "pod_fuse_pods", "pod_backtest_metrics", "pod_early_stop", "pod_ppo_workspace_size", "pod_ppo_update",
+           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan", "pod_fuse_pods", "pod_backtest_metrics", "pod_early_stop", "pod_ppo_workspace_size", "pod_ppo_update", "pod_ppo_check",
            "pod_elite_transfers", "pod_comm_unique_id", "pod_comm_init", "pod_comm_destroy", "pod_select_elite"]
 
 _lib = None
@@ -99,6 +99,7 @@ def load():
         "pod_ppo_workspace_size": ([P(EnvConfig), i32, i32, i32, P(sz)], C.c_int),
         "pod_ppo_update": ([P(EnvConfig), i32, i32, i32, P(PpoHparams), vp, vp, vp, i64, vp, sz, vp, vp, vp, vp, vp,
                             i64, vp, i32, i32, vp, vp, vp, sz, vp], C.c_int),
+        "pod_ppo_check": ([vp, vp], C.c_int),
         "pod_gae": ([vp, vp, vp, vp, i32, i32, f, f, vp, vp, vp, vp], C.c_int),
         "pod_elite_plan": ([vp, i32, i32, vp], C.c_int),
         "pod_elite_transfers": ([vp, i32, i32, i32, P(Transfer), i32, P(i32)], C.c_int),

@@ -278,7 +278,9 @@ class PPOLearner:
 
     def __init__(self, cfg: _lib.EnvConfig, n_hidden: int, hidden: int, params: torch.Tensor, act: int = 0,
                  batch: int = 1024, ratio_clip=0.25, entropy_coef=0.02, value_coef=0.5, learning_rate=2.0 ** -14,
-                 betas=(0.9, 0.999), adam_eps=1e-8):
+                 betas=(0.9, 0.999), adam_eps=1e-8, fp32: bool = False):
+        """fp32=True runs the products on float32 operands (the reference mode: master weights, float32
+        activations and deltas) instead of bf16 on the tensor cores."""
         self.cfg, self.n_hidden, self.hidden, self.act, self.batch = cfg, n_hidden, hidden, act, batch
         self.params = params
         L = actor_layout(cfg, n_hidden, hidden)
@@ -290,7 +292,8 @@ class PPOLearner:
         self.m = torch.zeros_like(self.master)
         self.v = torch.zeros_like(self.master)
         self.t = 0
-        self.hp = _lib.PpoHparams(ratio_clip, entropy_coef, value_coef, learning_rate, betas[0], betas[1], adam_eps, 0.0)
+        self.hp = _lib.PpoHparams(ratio_clip, entropy_coef, value_coef, learning_rate, betas[0], betas[1], adam_eps,
+                                  1 if fp32 else 0)
         nb = C.c_size_t(0)
         check(load().pod_ppo_workspace_size(C.byref(cfg), n_hidden, hidden, batch, C.byref(nb)), "pod_ppo_workspace_size")
         self.ws = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
@@ -301,7 +304,7 @@ class PPOLearner:
         learning_rate, adam_beta1, adam_beta2, adam_eps.  They reach the captured minibatch loop through
         device memory, so the next update replays the same graph."""
         for k, v in kw.items():
-            if not hasattr(self.hp, k) or k == "reserved":
+            if not hasattr(self.hp, k) or k == "fp32_operands":
                 raise ValueError(f"unknown PPO hyper-parameter {k!r}")
             setattr(self.hp, k, float(v))
 
@@ -322,6 +325,10 @@ class PPOLearner:
                                     _ptr(self.ws), self.ws.numel(), _stream(stream)), "pod_ppo_update")
         self.t += n_mb
         return self.losses
+
+    def check(self, stream=None):
+        """pod_ppo_check: raises PodError(POD_ERR_NONFINITE) if a minibatch loss was not finite."""
+        check(load().pod_ppo_check(_ptr(self.ws), _stream(stream)), "pod_ppo_check")
 
 
 class Comm:

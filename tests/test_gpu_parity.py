@@ -648,39 +648,20 @@ def test_equity_curve_exact_and_backtest_metrics():
     assert np.all(mf[[0, 1, 2, 4]] == 0.0) and np.all(np.isnan(mf[3]))
 
 
-@pytest.mark.parametrize("act,B,n,nh,hid", [(0, 512, 30, 2, 128), (1, 512, 30, 2, 128), (0, 1001, 30, 2, 128),
-                                            (0, 512, 64, 1, 256), (1, 384, 30, 4, 128)])
-def test_ppo_update_parity(act, B, n, nh, hid):
-    """R#26: one PPO minibatch on the device buffers of a rollout (critic values, normalised GAE):
-    the float32 gradient (cuBLAS GEMMs + this library's kernels) vs the float64 oracle's analytic
-    gradient at the same parameters on the same rows; the loss sums; the Adam step; the refreshed slab."""
-    c = Case(n=n, f=3, T_data=400, N=256, H=100, seed=51)   # n = 64: the critic row in a fresh pad block
+def _ppo_case(n, nh, hid, act, seed=51, N=256, T=8):
+    c = Case(n=n, f=3, T_data=400, N=N, H=100, seed=seed)   # n = 64: the critic row in a fresh pad block
     aws, params, actor = _actor(c, nh, hid, act=act)
-    T = 8   # B = 1001: ragged in every kernel's row blocking (8-sample head blocks, 16-row bias blocks)
     tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, critic=True)
     c.env.reset(c.starts)
     c.env.rollout(T, tr, actor=actor)
     adv, ret = api.pod_gae(tr.rew, tr.val[:T].contiguous(), tr.done, tr.val[T].contiguous(), 0.99, 0.95,
                            normalize=True)
     M = T * c.N
-    obs = tr.obs[:T].reshape(M, c.k_pad)
-    act_raw = tr.act.reshape(M, c.n)
-    lpo = tr.logp.reshape(M)
-    A = adv.reshape(M)
-    R = ret.reshape(M)
-    lr = 1e-3
-    learner = api.PPOLearner(c.cfg, nh, hid, params, act=act, batch=B, learning_rate=lr)
-    theta0 = learner.master.cpu().numpy().astype(np.float64)
-    rows = np.random.default_rng(3).permutation(M)[:B].astype(np.int32)
-    g_gpu = torch.empty(learner.n_elems, dtype=torch.float32, device="cuda")
-    losses = learner.update(obs, act_raw, lpo, A, R, torch.from_numpy(rows).cuda(), grad_out=g_gpu)
-    L = api.actor_layout(c.cfg, nh, hid)
-    dims = (L.k_pad, hid, nh, c.n, L.n_out_pad)
-    _, g_o, (sobj, svl, H) = oracle.ppo_loss_grad(
-        theta0, dims, bf16_to_f64(obs[rows]), act_raw[rows].cpu().numpy(), lpo[rows].cpu().numpy(),
-        A[rows].cpu().numpy(), R[rows].cpu().numpy(), 0.25, 0.02, 0.5, act)
-    g_g = g_gpu.cpu().numpy().astype(np.float64)
-    # segment by segment: W_l, b_l, log_std
+    args = (tr.obs[:T].reshape(M, c.k_pad), tr.act.reshape(M, c.n), tr.logp.reshape(M), adv.reshape(M), ret.reshape(M))
+    return c, params, args, M
+
+
+def _ppo_segments(L):
     segs, o = [], 0
     for l in range(L.n_layers):
         segs.append((o, o + L.w_rows[l] * L.w_cols[l]))
@@ -689,18 +670,70 @@ def test_ppo_update_parity(act, B, n, nh, hid):
         segs.append((o, o + L.w_rows[l]))
         o += L.w_rows[l]
     segs.append((o, o + L.n_out_pad))
-    # the learner's GEMMs take bf16 operands (weights = the bf16 slab, activations and deltas rounded to
-    # bf16) with float32 accumulation, against the float64 oracle: a bf16-level bar per segment
-    for a0, a1 in segs:
-        ref = g_o[a0:a1]
-        scale = np.abs(ref).max() + 1e-12
-        rel = np.linalg.norm(g_g[a0:a1] - ref) / (np.linalg.norm(ref) + 1e-30)
-        assert rel <= 2e-2, (a0, a1, rel)
-        assert np.all(np.abs(g_g[a0:a1] - ref) <= 5e-2 * scale + 1e-7), (a0, a1, np.abs(g_g[a0:a1] - ref).max() / scale)
+    return segs
+
+
+# PPO gradient bars (R#26/R#27), per parameter segment (W_l, b_l, log_std); m = the oracle's
+# magnitude of each entry (the sum of the absolute values of the terms it is summed from):
+#   float32 mode vs the float64 oracle:                 ||g-o|| <= 2e-4 ||o||, |g-o| <= 2e-3 (|o| + rms(o))
+#   bf16 mode vs the oracle with bf16 operand rounding: ||g-o|| <= 2e-3 ||o||; |g-o| <= 1e-2 m for every entry
+#                                                       with tanh; with ReLU for >= 97 % of a segment's entries
+#                                                       and |g-o| <= 0.5 m for all
+#   bf16 mode vs the plain float64 oracle:              ||g-o|| <= 3e-2 ||o||   (operand rounding moves rho)
+# (ReLU: where a pre-activation lies within rounding of 0 the two sides can take opposite derivatives: the
+# gradient entries of that unit pick up or lose a whole term — a large share of m for a rarely active unit —
+# and the changed delta spreads, at a small scale, into every unit of the layers below; tanh has no such
+# discontinuity, so its bar holds for every entry.  Measured at the C3 actor: <= 2.5 % of W_0's entries
+# beyond 1e-2 m, the largest 0.24 m, in W_1.)
+@pytest.mark.parametrize("fp32", [True, False])
+@pytest.mark.parametrize("act,B,n,nh,hid", [(0, 512, 30, 2, 128), (1, 512, 30, 2, 128), (0, 1001, 30, 2, 128),
+                                            (0, 512, 64, 1, 256), (1, 384, 30, 4, 128), (0, 1024, 100, 3, 512)])
+def test_ppo_update_parity(act, B, n, nh, hid, fp32):
+    """R#26: one PPO minibatch on the device buffers of a rollout (critic values, normalised GAE): the
+    gradient of this library's learner (tcgen05 GEMMs in bf16 mode, the float32 core in fp32 mode, the same
+    epilogues and reductions) vs the float64 oracle's analytic gradient at the same parameters on the same
+    rows; the loss sums; the Adam step; the refreshed slab.  B = 1001 is ragged in every tile (128-row GEMM
+    tiles, 8-sample head blocks); (100, 3, 512) is the C3 actor."""
+    c, params, args, M = _ppo_case(n, nh, hid, act, N=256 if n < 100 else 512)
+    obs, act_raw, lpo, A, R = args
+    lr = 1e-3
+    learner = api.PPOLearner(c.cfg, nh, hid, params, act=act, batch=B, learning_rate=lr, fp32=fp32)
+    theta0 = learner.master.cpu().numpy().astype(np.float64)
+    rows = np.random.default_rng(3).permutation(M)[:B].astype(np.int32)
+    g_gpu = torch.empty(learner.n_elems, dtype=torch.float32, device="cuda")
+    losses = learner.update(obs, act_raw, lpo, A, R, torch.from_numpy(rows).cuda(), grad_out=g_gpu)
+    learner.check()
+    L = api.actor_layout(c.cfg, nh, hid)
+    dims = (L.k_pad, hid, nh, c.n, L.n_out_pad)
+    oargs = (dims, bf16_to_f64(obs[rows]), act_raw[rows].cpu().numpy(), lpo[rows].cpu().numpy(),
+             A[rows].cpu().numpy(), R[rows].cpu().numpy(), 0.25, 0.02, 0.5, act)
+    _, g_o, (sobj, svl, H), m_o = oracle.ppo_loss_grad(theta0, *oargs, magnitudes=True)
+    _, g_e, (sobj_e, svl_e, _), m_e = oracle.ppo_loss_grad(theta0, *oargs, bf16_operands=True, magnitudes=True)
+    g_g = g_gpu.cpu().numpy().astype(np.float64)
+    ref, mag, nb = (g_o, m_o, 2e-4) if fp32 else (g_e, m_e, 2e-3)
+    for si, (a0, a1) in enumerate(_ppo_segments(L)):
+        o = ref[a0:a1]
+        d = g_g[a0:a1] - o
+        rel = np.linalg.norm(d) / (np.linalg.norm(o) + 1e-30)
+        assert rel <= nb, (a0, a1, rel)
+        if not fp32:
+            r = np.abs(d) / (mag[a0:a1] + 1e-30)
+            r[np.abs(d) <= 1e-9] = 0.0
+            frac = float((r > 1e-2).mean())
+            assert frac <= (0.0 if act == 1 else 0.03), (si, frac, float(r.max()))
+            assert r.max() <= 0.5, (si, float(r.max()))
+        else:
+            rms = np.sqrt(np.mean(o ** 2))
+            bad = np.abs(d) > 2e-3 * (np.abs(o) + rms) + 1e-9
+            assert not bad.any(), (a0, a1, float(np.max(np.abs(d) / (np.abs(o) + rms + 1e-30))))
+        if not fp32:   # and against the plain float64 oracle: operand rounding moves rho by ~1e-2
+            op = g_o[a0:a1]
+            assert np.linalg.norm(g_g[a0:a1] - op) <= 3e-2 * np.linalg.norm(op) + 1e-9, (a0, a1)
     ls = losses.cpu().numpy()
-    # bf16 forward: each rho carries ~1e-2 of relative error (as the rollout's own log-probs do)
     A_abs = float(np.abs(A[rows].cpu().numpy()).sum())
-    assert abs(ls[0] - sobj) <= 2e-2 * A_abs and ls[1] == pytest.approx(svl, rel=5e-2)
+    so, sv = (sobj, svl) if fp32 else (sobj_e, svl_e)
+    assert abs(ls[0] - so) <= (1e-4 if fp32 else 2e-3) * A_abs
+    assert ls[1] == pytest.approx(sv, rel=1e-4 if fp32 else 2e-3)
     assert ls[2] == pytest.approx(H, rel=1e-6) and ls[3] == B
     # Adam, first step, on the device gradient
     th1, _, _ = oracle.adam_step(theta0, np.zeros_like(theta0), np.zeros_like(theta0), g_g, 1, lr)
@@ -711,6 +744,50 @@ def test_ppo_update_parity(act, B, n, nh, hid):
     nw = sum(L.w_rows[l] * L.w_cols[l] for l in range(L.n_layers))
     np.testing.assert_array_equal(flat[:nw], bf16_to_f64(torch.from_numpy(m32[:nw]).to(torch.bfloat16)))
     np.testing.assert_array_equal(flat[nw:], m32[nw:].astype(np.float64))
+
+
+def test_ppo_bf16_mode_tracks_fp32_mode():
+    """The two learner modes on the same minibatch (C3 actor shape): they share every launch, layout and
+    epilogue and differ only in the operand precision of the products, so their gradients agree to the bf16
+    operand bar (a wrong operand layout in one core would show as an O(1) difference)."""
+    c, params, args, M = _ppo_case(100, 3, 512, 0, seed=57, N=512)
+    rows = torch.from_numpy(np.random.default_rng(8).permutation(M)[:1024].astype(np.int32)).cuda()
+    g = {}
+    for fp32 in (True, False):
+        lr_ = api.PPOLearner(c.cfg, 3, 512, params.clone(), batch=1024, learning_rate=1e-3, fp32=fp32)
+        g[fp32] = torch.empty(lr_.n_elems, dtype=torch.float32, device="cuda")
+        lr_.update(*args, rows, grad_out=g[fp32])
+    a, b = g[True].cpu().numpy().astype(np.float64), g[False].cpu().numpy().astype(np.float64)
+    L = api.actor_layout(c.cfg, 3, 512)
+    for a0, a1 in _ppo_segments(L):
+        assert np.linalg.norm(a[a0:a1] - b[a0:a1]) <= 3e-2 * np.linalg.norm(a[a0:a1]) + 1e-9, (a0, a1)
+
+
+def test_ppo_nonfinite_loss_is_flagged_and_not_applied():
+    """a non-finite loss signals divergence.  A NaN advantage in the minibatch sets the learner's
+    error word; the master, the moments and the slab are left as they were; pod_ppo_check reports
+    POD_ERR_NONFINITE and clears it; until then the next update on the workspace refuses to run."""
+    c, params, args, M = _ppo_case(30, 2, 128, 0, seed=58)
+    obs, act_raw, lpo, A, R = args
+    A = A.clone()
+    A[5] = float("nan")
+    learner = api.PPOLearner(c.cfg, 2, 128, params, batch=512, learning_rate=1e-3)
+    m0, slab0 = learner.master.clone(), params.clone()
+    rows = torch.arange(0, 512, dtype=torch.int32, device="cuda")
+    learner.update(obs, act_raw, lpo, A, R, rows)
+    torch.cuda.synchronize()
+    assert torch.equal(learner.master, m0) and torch.equal(params, slab0)
+    assert torch.count_nonzero(learner.m) == 0
+    with pytest.raises(PodError) as ei:
+        learner.update(obs, act_raw, lpo, A, R, rows)
+    assert ei.value.status == 7
+    with pytest.raises(PodError) as ei:
+        learner.check()
+    assert ei.value.status == 7
+    learner.check()   # cleared
+    learner.update(obs, act_raw, lpo, args[3], R, rows)   # finite data: applied
+    learner.check()
+    assert not torch.equal(learner.master, m0)
 
 
 def test_ppo_learner_improves_surrogate():
@@ -767,12 +844,8 @@ def test_ppo_graph_replay_step_counter():
     torch.cuda.synchronize()
     ma, mb = la.master.cpu().numpy(), lb.master.cpu().numpy()
     assert np.isfinite(ma).all() and np.abs(mb - m0).max() > 1e-4
-    # float atomics (bias and log-std reductions) make the gradient sums order-dependent, and Adam turns a
-    # near-zero gradient into a +-lr step: compare per element at 1 % of lr and allow a 1 % tail (a stale
-    # bias correction moves essentially every updated element by ~1/3 of lr)
-    moved = np.abs(mb - m0) > 0
-    off = np.abs(ma - mb) > 1e-2 * 1e-3
-    assert off[moved].mean() < 0.01, off[moved].mean()
+    # the learner is deterministic (fixed-order reductions, no float atomics in the gradient): bit-identical
+    np.testing.assert_array_equal(ma, mb)
 
 
 def test_ppo_hyperparameter_schedule_replays_graph():
@@ -808,14 +881,13 @@ def test_ppo_hyperparameter_schedule_replays_graph():
     a, b = sched.master.cpu().numpy(), fresh.master.cpu().numpy()
     moved = np.abs(b - theta.cpu().numpy()) > 0
     assert moved.mean() > 0.5
-    # float atomics in the reductions: compare at 1 % of the step, allowing a 1 % tail
-    assert (np.abs(a - b) > 1e-2 * 5e-3)[moved].mean() < 0.01
+    np.testing.assert_array_equal(a, b)   # deterministic learner: the replayed step is the fresh one exactly
 
 
 def test_ppo_concurrent_learners_on_streams():
-    """Two learners (distinct buffers, own cuBLAS scratch inside their workspaces) replayed concurrently on
-    two streams reach the same parameters as each run alone (float atomics in the reductions: float32-level
-    agreement; any sharing of scratch between the concurrent graphs would show as gross differences)."""
+    """Two learners (distinct buffers, all scratch inside their own workspaces) replayed concurrently on two
+    streams reach exactly the parameters of each run alone (any sharing of scratch between the concurrent
+    graphs would show)."""
     c = Case(n=30, f=3, T_data=400, N=256, H=100, seed=54)
     aws, params, actor = _actor(c, 2, 128)
     T, B = 8, 512
@@ -852,7 +924,7 @@ def test_ppo_concurrent_learners_on_streams():
     for k in range(2):
         a, b = conc[k].master.cpu().numpy(), solo[k].master.cpu().numpy()
         assert np.isfinite(a).all()
-        assert (np.abs(a - b) > 1e-2 * 1e-3).mean() < 0.01
+        np.testing.assert_array_equal(a, b)
 
 
 # ----------------------------------------------------------------- shape sweep (edge configurations)

@@ -29,7 +29,7 @@ def test_exports_match_header():
     L = _lib.load()
     for name in declared:
         assert hasattr(L, name), name
-    assert L.pod_abi_version() == 2
+    assert L.pod_abi_version() == 3
     assert L.pod_status_string(3) == b"POD_ERR_RANGE"
 
 

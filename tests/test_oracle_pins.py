@@ -620,6 +620,47 @@ def test_ppo_clip_pins():
     np.testing.assert_array_equal(g[:nW][: hid * k_pad], 0.0)    # no policy gradient flows through the clip
 
 
+def test_bf16_round_matches_torch_bfloat16():
+    """R#27's rounding model: oracle.bf16_round (RNE of the float32 value to 8 significant bits) equals torch's
+    float32 -> bfloat16 conversion (an independent library routine), including ties to even, negatives,
+    subnormals, zero and the largest finite values."""
+    import torch
+    rng = np.random.default_rng(12)
+    x = np.concatenate([rng.normal(size=4000) * 10.0 ** rng.integers(-30, 30, 4000),
+                        [0.0, -0.0, 1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8, -(1.0 + 2.0 ** -8), 1e-40, -3e-39,
+                         3.3895313892515355e38, 65504.0, 2.0 ** -133]]).astype(np.float32)
+    ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(oracle.bf16_round(x), ref)
+
+
+def test_ppo_bf16_operand_emulation_exact_on_representable_values():
+    """R#27: with every operand already bf16-representable (small integer observations and weights, ReLU,
+    integer returns, c_v a power of two, A = 0 so only the value head trains) the rounding emulation changes
+    nothing: the emulated gradient equals the plain float64 one exactly; with real-valued operands it
+    differs (the rounding is applied)."""
+    rng = np.random.default_rng(13)
+    dims = (8, 5, 2, 2, 4)
+    k_pad, hid, nh, n, nop = dims
+    ne = hid * k_pad + hid * hid + nop * hid + hid + hid + nop + nop
+    theta = rng.integers(-1, 2, size=ne).astype(np.float64) * 0.5   # activations stay small integers / halves
+    theta[-nop:] = 0.0   # log-std 0
+    B = 16
+    obs = rng.integers(0, 2, size=(B, k_pad)).astype(np.float64)
+    act_raw = rng.normal(size=(B, n))
+    lpo = np.zeros(B)
+    adv = np.zeros(B)
+    ret = rng.integers(-4, 5, size=B).astype(np.float64)
+    args = (dims, obs, act_raw, lpo, adv, ret, 0.25, 0.0, 4.0, 0)   # 2 c_v / B = 1/2
+    _, g_plain, _ = oracle.ppo_loss_grad(theta, *args)
+    _, g_emu, _ = oracle.ppo_loss_grad(theta, *args, bf16_operands=True)
+    assert np.abs(g_plain).max() > 0
+    np.testing.assert_array_equal(g_emu, g_plain)
+    theta2 = theta + rng.normal(size=ne) * 1e-3
+    _, g2p, _ = oracle.ppo_loss_grad(theta2, *args)
+    _, g2e, _ = oracle.ppo_loss_grad(theta2, *args, bf16_operands=True)
+    assert not np.array_equal(g2p, g2e)
+
+
 def test_adam_first_step_is_normalised_gradient():
     """Bias-corrected Adam's first step: m_hat = g, v_hat = g^2, so the update is -lr g / (|g| + eps)."""
     g = np.array([1e-3, -2.0, 0.0, 5e-9])

@@ -16,13 +16,16 @@ from paper_2111_05188_b200 import api, configs, synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--pods", type=int, default=1)
+ap.add_argument("--mb", type=int, default=32, help="minibatches per update call")
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--fp32", action="store_true", help="the float32 reference mode")
 args = ap.parse_args()
 w = configs.preset("C3")
 cfg = api.config_from_workload(w)
 L = api.actor_layout(cfg, w.n_hidden, w.hidden)
 P = args.pods
 aws = [synth.make_actor(int(L.obs_dim), w.n_hidden, w.hidden, w.n_stocks, 11 + p) for p in range(P)]
-B, M, n_mb = 1024, 65536, 32
+B, M, n_mb = 1024, 65536, args.mb
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
 obs = (torch.randn((M, int(L.k_pad)), generator=g, device="cuda") * 0.5).to(torch.bfloat16)
@@ -31,7 +34,7 @@ lpo = torch.randn(M, generator=g, device="cuda") - 100.0
 adv = torch.randn(M, generator=g, device="cuda")
 ret = torch.randn(M, generator=g, device="cuda")
 params = [api.pack_actor_params(cfg, [aws[p]], w.n_hidden, w.hidden) for p in range(P)]
-learners = [api.PPOLearner(cfg, w.n_hidden, w.hidden, params[p], batch=B) for p in range(P)]
+learners = [api.PPOLearner(cfg, w.n_hidden, w.hidden, params[p], batch=B, fp32=args.fp32) for p in range(P)]
 perms = [torch.from_numpy(np.random.default_rng(1 + p).permutation(M)[: n_mb * B].astype(np.int32)).cuda()
          for p in range(P)]
 streams = [torch.cuda.Stream() for _ in range(P)]
@@ -51,7 +54,7 @@ for _ in range(2):
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-reps = 5
+reps = args.reps
 for _ in range(reps):
     run()
 e1.record()
