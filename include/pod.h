@@ -279,13 +279,35 @@ pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, cons
  * pod_actor_layout of (cfg, n_hidden, hidden), in/out; bf16 weights are
  * rounded to nearest even from the float32 result.  prev [dev] f32
  * [P_local/K_local][layout.n_elems] the previous fused parameters (in/out);
- * may be NULL only when tau == 1 (hard adoption, S:L368 default).  work [dev]
- * f32 [P_local/K_local][layout.n_elems] scratch.  tau in [0, 1].
- * Stream-ordered; the cross-rank sum is one ncclAllReduce on `stream`.
- * Errors: ARG, SHAPE, UNSUPPORTED, NCCL, CUDA. */
+ * may be NULL only when tau == 1 (hard adoption, S:L368 default).  work: not
+ * used (kept for ABI compatibility; may be NULL).  tau in [0, 1].
+ * One kernel per rank: the local pod sum (float32, pod order) is published in
+ * a buffer every rank maps (CUDA IPC over NVLink, set up collectively on the
+ * first call and whenever a larger one is needed), every rank waits for the
+ * others' partials chunk by chunk, sums them in rank order (so every rank holds
+ * bit-identical fused parameters), blends and narrows into its pods; no
+ * collective library call.  Collective over `comm` (same arguments on every
+ * rank), stream-ordered.  Errors: ARG, SHAPE, UNSUPPORTED, NCCL (setup), CUDA. */
 pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
                          void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
                          float* prev, float* work, void* stream);
+
+/* Workspace bytes of pod_fuse_pods_local_ranks for R ranks (host only). */
+pod_status pod_fuse_workspace_size(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, int32_t P_local,
+                                   int32_t K_local, int32_t R, size_t* bytes);
+
+/* The same fusion over R (1..16) ranks' slab arrays that all live on this
+ * device, in one launch whose block rows play the ranks and exchange their
+ * partial sums through `ws` exactly as pod_fuse_pods' ranks do through peer
+ * memory (the single-process multi-learner form, and the one-device check of
+ * the cross-rank protocol).  params [host] R device pointers, each
+ * [P_local][param_bytes]; prev [host] R device pointers (f32
+ * [P_local/K_local][n_elems]) or NULL when tau == 1; K = K_local * R.
+ * ws [dev] >= pod_fuse_workspace_size bytes, 256-byte aligned.
+ * Stream-ordered.  Errors: ARG, SHAPE, WORKSPACE, UNSUPPORTED, CUDA. */
+pod_status pod_fuse_pods_local_ranks(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, void* const* params,
+                                     size_t param_bytes, int32_t R, int32_t P_local, int32_t K_local, float tau,
+                                     float* const* prev, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------ PPO update */
 /* Learner hyper-parameters (P:L472 PPO; Table 3 via S:L239–241; R#26). */

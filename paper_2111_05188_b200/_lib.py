@@ -60,7 +60,7 @@ class Transfer(C.Structure):
 
 EXPORTS = ["pod_status_string", "pod_last_error", "pod_abi_version", "pod_actor_layout_get",
            "pod_env_workspace_size", "pod_env_create", "pod_env_destroy", "pod_env_reset", "pod_rollout",
-           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan", "pod_fuse_pods", "pod_backtest_metrics", "pod_early_stop", "pod_ppo_workspace_size", "pod_ppo_update", "pod_ppo_check",
+           "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan", "pod_fuse_pods", "pod_fuse_workspace_size", "pod_fuse_pods_local_ranks", "pod_backtest_metrics", "pod_early_stop", "pod_ppo_workspace_size", "pod_ppo_update", "pod_ppo_check",
            "pod_elite_transfers", "pod_comm_unique_id", "pod_comm_init", "pod_comm_destroy", "pod_select_elite"]
 
 _lib = None
@@ -94,6 +94,8 @@ def load():
         "pod_env_read_state": ([vp, vp, vp, vp, vp, vp], C.c_int),
         "pod_env_check": ([vp, vp], C.c_int),
         "pod_fuse_pods": ([vp, P(EnvConfig), i32, i32, vp, sz, i32, i32, f, vp, vp, vp], C.c_int),
+        "pod_fuse_workspace_size": ([P(EnvConfig), i32, i32, i32, i32, i32, P(sz)], C.c_int),
+        "pod_fuse_pods_local_ranks": ([P(EnvConfig), i32, i32, vp, sz, i32, i32, i32, f, vp, vp, sz, vp], C.c_int),
         "pod_backtest_metrics": ([vp, vp, i32, i32, d, d, vp, vp], C.c_int),
         "pod_early_stop": ([vp, i32, i32, P(i32), P(i32)], C.c_int),
         "pod_ppo_workspace_size": ([P(EnvConfig), i32, i32, i32, P(sz)], C.c_int),

@@ -241,14 +241,31 @@ def fuse_pods(cfg: _lib.EnvConfig, n_hidden: int, hidden: int, params: torch.Ten
               stream=None):
     """K-pod ensemble fusion (pod_fuse_pods, R#24): params uint8 [P_local, param_bytes] (slots a*K_local + k are
     agent a's pods), prev float32 [P_local/K_local, n_elems] (in/out; optional when tau == 1)."""
-    L = actor_layout(cfg, n_hidden, hidden)
     P_local = params.shape[0]
-    if work is None:
-        work = torch.empty((P_local // K_local, int(L.n_elems)), dtype=torch.float32, device=params.device)
     check(load().pod_fuse_pods(comm.h if comm is not None else None, C.byref(cfg), n_hidden, hidden, _ptr(params),
                                params.shape[1], P_local, int(K_local), float(tau), _ptr(prev), _ptr(work),
                                _stream(stream)), "pod_fuse_pods")
     return prev
+
+
+def fuse_pods_local_ranks(cfg: _lib.EnvConfig, n_hidden: int, hidden: int, params: Sequence[torch.Tensor],
+                          K_local: int, tau: float = 1.0, prevs: Optional[Sequence[torch.Tensor]] = None, stream=None):
+    """pod_fuse_pods_local_ranks: the fusion over R ranks' slab arrays on this device in one launch (block rows
+    play the ranks and exchange partial sums as pod_fuse_pods' ranks do over peer memory)."""
+    R = len(params)
+    P_local = params[0].shape[0]
+    nb = C.c_size_t(0)
+    check(load().pod_fuse_workspace_size(C.byref(cfg), n_hidden, hidden, P_local, int(K_local), R, C.byref(nb)),
+          "pod_fuse_workspace_size")
+    ws = torch.empty(int(nb.value), dtype=torch.uint8, device=params[0].device)
+    pp_arr = (C.c_void_p * R)(*[p.data_ptr() for p in params])
+    pv_arr = (C.c_void_p * R)(*[p.data_ptr() for p in prevs]) if prevs is not None else None
+    pp = C.cast(pp_arr, C.c_void_p)
+    pv = C.cast(pv_arr, C.c_void_p) if pv_arr is not None else None
+    check(load().pod_fuse_pods_local_ranks(C.byref(cfg), n_hidden, hidden, pp, params[0].shape[1], R, P_local,
+                                           int(K_local), float(tau), pv, _ptr(ws), ws.numel(), _stream(stream)),
+          "pod_fuse_pods_local_ranks")
+    return ws
 
 
 def backtest_metrics(v0: torch.Tensor, curve: torch.Tensor, periods_per_year: float, rf_per_period: float = 0.0,

@@ -1109,58 +1109,142 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
 }
 
 // ------------------------------------------------------------ K-pod ensemble fusion (R#24)
-extern "C" pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
-                                    void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
-                                    float* prev, float* work, void* stream) {
-    if (!params || !work) return pod_fail(POD_ERR_ARG, "params and work must be non-NULL");
+// the parts of fuse_x_kernel's arguments that depend only on the slab layout
+static pod_status fuse_x_common(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden, size_t param_bytes,
+                                int32_t P_local, int32_t K_local, float tau, int32_t R, FuseXArgs* a) {
     if (K_local < 1 || P_local < 1 || P_local % K_local != 0)
         return pod_fail(POD_ERR_ARG, "P_local (%d) must be a positive multiple of K_local (%d)", P_local, K_local);
     if (!(tau >= 0.0f && tau <= 1.0f)) return pod_fail(POD_ERR_ARG, "tau must be in [0, 1]");
-    if (!prev && tau != 1.0f) return pod_fail(POD_ERR_ARG, "prev is required when tau < 1");
+    if (R < 1 || R > FUSE_MAX_RANKS) return pod_fail(POD_ERR_ARG, "ranks must be in [1, %d]", FUSE_MAX_RANKS);
     pod_actor_layout L;
     pod_status st = pod_actor_layout_get(cfg, n_hidden, hidden, &L);
     if (st) return st;
     if (param_bytes < L.param_bytes || param_bytes % 16 != 0)
         return pod_fail(POD_ERR_SHAPE, "param_bytes %zu must be >= %zu and a multiple of 16", param_bytes, L.param_bytes);
-    st = pod_require_sm100();
-    if (st) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    FuseArgs a{};
+    memset(a, 0, sizeof(*a));
     uint64_t flat = 0;
     int ns = 0;
     for (int l = 0; l < L.n_layers; ++l) {
-        a.seg[ns++] = FuseSeg{L.w_offset[l], flat, static_cast<uint32_t>(L.w_rows[l]) * L.w_cols[l], 1u};
+        a->seg[ns++] = FuseSeg{L.w_offset[l], flat, static_cast<uint32_t>(L.w_rows[l]) * L.w_cols[l], 1u};
         flat += static_cast<uint64_t>(L.w_rows[l]) * L.w_cols[l];
     }
     for (int l = 0; l < L.n_layers; ++l) {
-        a.seg[ns++] = FuseSeg{L.b_offset[l], flat, static_cast<uint32_t>(L.w_rows[l]), 0u};
+        a->seg[ns++] = FuseSeg{L.b_offset[l], flat, static_cast<uint32_t>(L.w_rows[l]), 0u};
         flat += static_cast<uint64_t>(L.w_rows[l]);
     }
-    a.seg[ns++] = FuseSeg{L.log_std_offset, flat, static_cast<uint32_t>(L.n_out_pad), 0u};
+    a->seg[ns++] = FuseSeg{L.log_std_offset, flat, static_cast<uint32_t>(L.n_out_pad), 0u};
     flat += static_cast<uint64_t>(L.n_out_pad);
-    a.n_seg = ns;
-    a.K_local = K_local;
-    a.n_elems = static_cast<int64_t>(flat);
-    a.param_bytes = param_bytes;
-    a.params = static_cast<char*>(params);
-    a.work = work;
-    a.prev = prev;
+    a->n_seg = ns;
+    a->K_local = K_local;
+    a->n_elems = static_cast<int64_t>(flat);
+    a->param_bytes = param_bytes;
+    a->scale = 1.0f / static_cast<float>(K_local * R);
+    a->tau = tau;
+    a->R = R;
+    a->A_local = P_local / K_local;
+    a->nchunks = (a->n_elems + FUSE_CHUNK - 1) / FUSE_CHUNK;
+    if (a->n_elems % 8 != 0) return pod_fail(POD_ERR_SHAPE, "flat parameter count must be a multiple of 8");
+    return pod_require_sm100();
+}
+
+// resident blocks of fuse_x_kernel on this device (every block of an R-rank launch must be resident)
+static int fuse_x_capacity() {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fuse_x_kernel, 256, 0);
+    return sms * (per > 0 ? per : 1);
+}
+
+extern "C" pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                    void* params, size_t param_bytes, int32_t P_local, int32_t K_local, float tau,
+                                    float* prev, float* work, void* stream) {
+    (void)work;   // no float32 work vector: the exchange happens inside fuse_x_kernel
+    if (!params) return pod_fail(POD_ERR_ARG, "params must be non-NULL");
+    if (!prev && tau != 1.0f) return pod_fail(POD_ERR_ARG, "prev is required when tau < 1");
+    if (reinterpret_cast<uintptr_t>(params) % 16 != 0 || (prev && reinterpret_cast<uintptr_t>(prev) % 16 != 0))
+        return pod_fail(POD_ERR_ARG, "params and prev must be 16-byte aligned");
     const int nranks = comm ? pod_comm_size(comm) : 1;
-    a.scale = 1.0f / static_cast<float>(K_local * nranks);
-    a.tau = tau;
-    const int A_local = P_local / K_local;
-    if (a.n_elems % 8 != 0 || param_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(params) % 16 != 0 ||
-        reinterpret_cast<uintptr_t>(work) % 16 != 0 || (prev && reinterpret_cast<uintptr_t>(prev) % 16 != 0))
-        return pod_fail(POD_ERR_ARG, "params, prev and work must be 16-byte aligned");
-    const int64_t groups8 = a.n_elems / 8;
-    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((groups8 + 255) / 256, 8 * 148)), static_cast<unsigned>(A_local));
-    fuse_sum_kernel<<<grid, 256, 0, s>>>(a);
-    POD_CUDA(cudaGetLastError());
-    if (comm && nranks > 1) {
-        st = pod_comm_allreduce_sum_f32(comm, work, static_cast<size_t>(A_local) * a.n_elems, s);
+    FuseXArgs a;
+    pod_status st = fuse_x_common(cfg, n_hidden, hidden, param_bytes, P_local, K_local, tau, nranks, &a);
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int me = comm ? pod_comm_rank(comm) : 0;
+    a.my_rank = me;
+    a.params[me] = static_cast<char*>(params);
+    a.prev[me] = prev;
+    a.epoch = 1;
+    if (nranks > 1) {
+        float* stage[FUSE_MAX_RANKS];
+        uint32_t *flag[FUSE_MAX_RANKS], *ack[FUSE_MAX_RANKS];
+        const size_t nflags = static_cast<size_t>(a.A_local) * a.nchunks;
+        st = pod_comm_fuse_buffers(comm, static_cast<size_t>(a.A_local) * a.n_elems, nflags, stage, flag, ack, &a.epoch, s);
         if (st) return st;
+        for (int q = 0; q < nranks; ++q) {
+            a.stage[q] = stage[q];
+            a.flag[q] = flag[q];
+            a.ack[q] = ack[q];
+        }
     }
-    fuse_blend_kernel<<<grid, 256, 0, s>>>(a);
+    const int64_t chunks = static_cast<int64_t>(a.A_local) * a.nchunks;
+    const unsigned X = static_cast<unsigned>(std::min<int64_t>(chunks, fuse_x_capacity()));
+    fuse_x_kernel<<<dim3(X, 1), 256, 0, s>>>(a);
+    POD_CUDA(cudaGetLastError());
+    return POD_OK;
+}
+
+extern "C" pod_status pod_fuse_workspace_size(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                              int32_t P_local, int32_t K_local, int32_t R, size_t* bytes) {
+    if (!bytes) return pod_fail(POD_ERR_ARG, "bytes is NULL");
+    pod_actor_layout L;
+    pod_status st = pod_actor_layout_get(cfg, n_hidden, hidden, &L);
+    if (st) return st;
+    if (K_local < 1 || P_local < 1 || P_local % K_local != 0 || R < 1 || R > FUSE_MAX_RANKS)
+        return pod_fail(POD_ERR_ARG, "bad P_local / K_local / R");
+    const size_t A = static_cast<size_t>(P_local / K_local), ne = L.n_elems;
+    const size_t nch = (ne + FUSE_CHUNK - 1) / FUSE_CHUNK;
+    *bytes = static_cast<size_t>(R) * (round_up(A * ne * 4, 256) + round_up(2 * A * nch * 4, 256));
+    return POD_OK;
+}
+
+extern "C" pod_status pod_fuse_pods_local_ranks(const pod_env_config* cfg, int32_t n_hidden, int32_t hidden,
+                                                void* const* params, size_t param_bytes, int32_t R, int32_t P_local,
+                                                int32_t K_local, float tau, float* const* prev, void* ws,
+                                                size_t ws_bytes, void* stream) {
+    if (!params || !ws) return pod_fail(POD_ERR_ARG, "params and ws must be non-NULL");
+    if (!prev && tau != 1.0f) return pod_fail(POD_ERR_ARG, "prev is required when tau < 1");
+    FuseXArgs a;
+    pod_status st = fuse_x_common(cfg, n_hidden, hidden, param_bytes, P_local, K_local, tau, R, &a);
+    if (st) return st;
+    size_t need = 0;
+    st = pod_fuse_workspace_size(cfg, n_hidden, hidden, P_local, K_local, R, &need);
+    if (st) return st;
+    if (ws_bytes < need || reinterpret_cast<uintptr_t>(ws) % 256 != 0)
+        return pod_fail(POD_ERR_WORKSPACE, "workspace needs %zu bytes, 256-byte aligned", need);
+    const size_t A = static_cast<size_t>(a.A_local);
+    const size_t sb = round_up(A * a.n_elems * 4, 256), fb = round_up(2 * A * a.nchunks * 4, 256);
+    char* w = static_cast<char*>(ws);
+    for (int q = 0; q < R; ++q) {
+        if (!params[q] || reinterpret_cast<uintptr_t>(params[q]) % 16 != 0)
+            return pod_fail(POD_ERR_ARG, "params[%d] must be non-NULL and 16-byte aligned", q);
+        a.params[q] = static_cast<char*>(params[q]);
+        a.prev[q] = prev ? prev[q] : nullptr;
+        if (a.prev[q] && reinterpret_cast<uintptr_t>(a.prev[q]) % 16 != 0)
+            return pod_fail(POD_ERR_ARG, "prev[%d] must be 16-byte aligned", q);
+        char* b = w + static_cast<size_t>(q) * (sb + fb);
+        a.stage[q] = reinterpret_cast<float*>(b);
+        a.flag[q] = reinterpret_cast<uint32_t*>(b + sb);
+        a.ack[q] = reinterpret_cast<uint32_t*>(b + sb) + A * a.nchunks;
+    }
+    a.my_rank = -1;   // block row y plays rank y
+    a.epoch = 1;
+    const int cap = fuse_x_capacity();
+    if (cap < R) return pod_fail(POD_ERR_UNSUPPORTED, "%d ranks exceed the resident blocks of the device", R);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int q = 0; q < R; ++q) POD_CUDA(cudaMemsetAsync(a.flag[q], 0, fb, s));   // flags and acks: epoch 1 from zero
+    const int64_t chunks = static_cast<int64_t>(A) * a.nchunks;
+    const unsigned X = static_cast<unsigned>(std::min<int64_t>(chunks, cap / R));
+    fuse_x_kernel<<<dim3(X, static_cast<unsigned>(R)), 256, 0, s>>>(a);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }

@@ -96,8 +96,6 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
-        nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -123,14 +121,13 @@ NcclApi* nccl() {
     LOAD(CommInitRank);
     LOAD(CommDestroy);
     LOAD(AllGather);
-    LOAD(AllReduce);
     LOAD(Send);
     LOAD(Recv);
     LOAD(GroupStart);
     LOAD(GroupEnd);
     LOAD(GetErrorString);
 #undef LOAD
-    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.Send || !api.Recv ||
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.Send || !api.Recv ||
         !api.GroupStart || !api.GroupEnd) {
         api.h = nullptr;
         return nullptr;
@@ -145,6 +142,11 @@ struct pod_comm {
     double* d_all;
     double* h_all;
     std::vector<pod_transfer> ops;
+    // fused fusion (pod_comm_fuse_buffers): this rank's buffer and every rank's mapping of theirs
+    void* fx_base = nullptr;
+    size_t fx_bytes = 0, fx_stage = 0;
+    std::vector<void*> fx_peer;   // [nranks], own entry = fx_base
+    uint32_t fx_epoch = 0;
 };
 
 #define NCCL_TRY(call)                                                                                        \
@@ -196,8 +198,18 @@ extern "C" pod_status pod_comm_init(const uint8_t id[128], int32_t nranks, int32
     return POD_OK;
 }
 
+static void fx_release(pod_comm_t* c) {
+    for (int q = 0; q < static_cast<int>(c->fx_peer.size()); ++q)
+        if (q != c->rank && c->fx_peer[static_cast<size_t>(q)]) cudaIpcCloseMemHandle(c->fx_peer[static_cast<size_t>(q)]);
+    c->fx_peer.clear();
+    if (c->fx_base) cudaFree(c->fx_base);
+    c->fx_base = nullptr;
+    c->fx_bytes = c->fx_stage = 0;
+}
+
 extern "C" pod_status pod_comm_destroy(pod_comm_t* c) {
     if (!c) return POD_OK;
+    fx_release(c);
     NcclApi* api = nccl();
     if (api && api->CommDestroy) api->CommDestroy(c->comm);
     cudaFree(c->d_all);
@@ -256,11 +268,55 @@ extern "C" pod_status pod_select_elite(pod_comm_t* c, const double* fitness_loca
 }
 
 int pod_comm_size(const pod_comm_t* c) { return c ? c->nranks : 1; }
+int pod_comm_rank(const pod_comm_t* c) { return c ? c->rank : 0; }
 
-// in-place sum over the communicator's ranks (K-pod fusion): one ncclAllReduce on `stream`
-pod_status pod_comm_allreduce_sum_f32(pod_comm_t* c, float* buf, size_t count, cudaStream_t stream) {
+pod_status pod_comm_fuse_buffers(pod_comm_t* c, size_t stage_elems, size_t nflags, float** stage, uint32_t** flag,
+                                 uint32_t** ack, uint32_t* epoch, cudaStream_t s) {
     NcclApi* api = nccl();
     if (!api) return pod_fail(POD_ERR_NCCL, "NCCL not loaded");
-    NCCL_TRY(api->AllReduce(buf, buf, count, ncclFloat32, ncclSum, c->comm, stream));
+    const size_t stage_bytes = (stage_elems * sizeof(float) + 255) / 256 * 256;
+    const size_t need = stage_bytes + 2 * nflags * sizeof(uint32_t);
+    if (!c->fx_base || c->fx_bytes < need || c->fx_stage != stage_bytes) {
+        // (re)build collectively: every rank reaches this with the same sizes (pod_fuse_pods is collective)
+        fx_release(c);
+        if (cudaMalloc(&c->fx_base, need) != cudaSuccess) return pod_fail(POD_ERR_CUDA, "fusion buffer allocation failed");
+        if (cudaMemset(c->fx_base, 0, need) != cudaSuccess) return pod_fail(POD_ERR_CUDA, "fusion buffer clear failed");
+        c->fx_bytes = need;
+        c->fx_stage = stage_bytes;
+        c->fx_epoch = 0;
+        cudaIpcMemHandle_t h;
+        if (cudaIpcGetMemHandle(&h, c->fx_base) != cudaSuccess) return pod_fail(POD_ERR_CUDA, "cudaIpcGetMemHandle failed");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handles are 64 bytes");
+        uint8_t* dh = nullptr;
+        if (cudaMalloc(&dh, 64 * static_cast<size_t>(c->nranks + 1)) != cudaSuccess)
+            return pod_fail(POD_ERR_CUDA, "handle exchange buffer allocation failed");
+        std::vector<uint8_t> all(64 * static_cast<size_t>(c->nranks));
+        cudaMemcpy(dh, &h, 64, cudaMemcpyHostToDevice);
+        ncclResult_t r = api->AllGather(dh, dh + 64, 64, ncclUint8, c->comm, s);
+        cudaError_t ce = r == ncclSuccess ? cudaStreamSynchronize(s) : cudaErrorUnknown;
+        if (ce == cudaSuccess) ce = cudaMemcpy(all.data(), dh + 64, all.size(), cudaMemcpyDeviceToHost);
+        cudaFree(dh);
+        if (r != ncclSuccess) return pod_fail(POD_ERR_NCCL, "IPC handle all-gather failed");
+        if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "IPC handle exchange: %s", cudaGetErrorString(ce));
+        c->fx_peer.assign(static_cast<size_t>(c->nranks), nullptr);
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank) {
+                c->fx_peer[static_cast<size_t>(q)] = c->fx_base;
+                continue;
+            }
+            cudaIpcMemHandle_t hq;
+            memcpy(&hq, all.data() + 64 * static_cast<size_t>(q), 64);
+            if (cudaIpcOpenMemHandle(&c->fx_peer[static_cast<size_t>(q)], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                return pod_fail(POD_ERR_CUDA, "cudaIpcOpenMemHandle of rank %d failed (peer access over NVLink?)", q);
+        }
+    }
+    for (int q = 0; q < c->nranks; ++q) {
+        char* b = static_cast<char*>(c->fx_peer[static_cast<size_t>(q)]);
+        stage[q] = reinterpret_cast<float*>(b);
+        flag[q] = reinterpret_cast<uint32_t*>(b + stage_bytes);
+        ack[q] = reinterpret_cast<uint32_t*>(b + stage_bytes + nflags * sizeof(uint32_t));
+    }
+    *epoch = ++c->fx_epoch;
     return POD_OK;
 }
+

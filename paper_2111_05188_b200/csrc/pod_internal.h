@@ -9,4 +9,10 @@ pod_status pod_require_sm100();
 #include <cuda_runtime.h>
 // communicator helpers for the fusion entry point (pod_elite.cpp)
 int pod_comm_size(const pod_comm_t* c);
-pod_status pod_comm_allreduce_sum_f32(pod_comm_t* c, float* buf, size_t count, cudaStream_t stream);
+int pod_comm_rank(const pod_comm_t* c);
+// the peer-mapped buffers of the fused cross-rank fusion (fuse_x_kernel): on first use, or when they must
+// grow, every rank (collectively) allocates one zeroed buffer of stage_elems floats + 2 nflags words,
+// exchanges its CUDA IPC handle over NCCL and maps the others'; returns every rank's stage / flag / ack
+// pointers ([nranks] each, in this process's address space) and this call's epoch (1, 2, ... per buffer set)
+pod_status pod_comm_fuse_buffers(pod_comm_t* c, size_t stage_elems, size_t nflags, float** stage, uint32_t** flag,
+                                 uint32_t** ack, uint32_t* epoch, cudaStream_t stream);

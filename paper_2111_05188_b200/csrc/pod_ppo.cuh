@@ -379,9 +379,7 @@ pod_status ppo_enqueue(const PpoPlan& p, cudaStream_t s, cudaStream_t s2) {
             POD_CUDA(cudaEventRecord(ev[9], s2));
         }
     }
-    // rejoin the side branch (stream capture needs every forked stream joined back)
-    POD_CUDA(cudaEventRecord(ev[7], s2));
-    POD_CUDA(cudaStreamWaitEvent(s, ev[7], 0));
+    // (the last minibatch's join above leaves nothing on the side branch: the capture is closed on s)
     if (p.n_mb == 0) {
         fuse_blend_kernel<<<ngrid, 256, 0, s>>>(*p.fa);
         POD_CUDA(cudaGetLastError());

@@ -622,6 +622,51 @@ def test_fuse_pods_parity(tau):
     c.env.check()
 
 
+@pytest.mark.parametrize("R,tau", [(2, 1.0), (4, 0.3), (3, 0.0)])
+def test_fuse_pods_local_ranks_exchange(R, tau):
+    """R#24, the cross-rank fusion kernel: R ranks' slab arrays (K_local = 2 pods of 2 agents each) fused in one
+    launch whose block rows play the ranks and exchange partial sums through flags and staging buffers as
+    pod_fuse_pods' ranks do over peer memory.  Every pod of an agent on every rank ends bit-identical, and equal
+    to the float64 oracle over all R x K_local pods within the fusion bars; prev likewise."""
+    c = Case(n=30, f=3, T_data=300, N=64, H=20)
+    nh, hid, K, A = 2, 128, 2, 2
+    L = api.actor_layout(c.cfg, nh, hid)
+    E = int(L.n_elems)
+    params = [api.pack_actor_params(c.cfg, [synth.make_actor(c.obs_dim, nh, hid, c.n, 300 + 10 * r + s)
+                                            for s in range(K * A)], nh, hid) for r in range(R)]
+    before = [p.cpu().numpy() for p in params]
+    prev0 = torch.from_numpy(np.random.default_rng(19).normal(size=(A, E)).astype(np.float32)).cuda()
+    prevs = [prev0.clone() for _ in range(R)] if tau != 1.0 else None
+    api.fuse_pods_local_ranks(c.cfg, nh, hid, params, K, tau=tau, prevs=prevs)
+    torch.cuda.synchronize()
+    after = [p.cpu().numpy() for p in params]
+    nw = sum(L.w_rows[l] * L.w_cols[l] for l in range(L.n_layers))
+    for a in range(A):
+        ref = after[0][a * K]
+        for r in range(R):
+            for k in range(K):
+                assert np.array_equal(after[r][a * K + k], ref), (a, r, k)
+        flats = np.stack([_slab_flat(before[r][a * K + k], L) for r in range(R) for k in range(K)])
+        exp = oracle.fuse(flats, prev0[a].cpu().numpy().astype(np.float64), tau)
+        got = _slab_flat(ref, L)
+        mag = tau * np.abs(flats).mean(axis=0) + (1.0 - tau) * np.abs(prev0[a].cpu().numpy())
+        tol32 = 8.0 * 2.0 ** -24 * mag
+        assert np.all(np.abs(got[:nw] - exp[:nw]) <= np.abs(exp[:nw]) * 2.0 ** -8 + 2.0 * tol32[:nw]), a
+        assert np.all(np.abs(got[nw:] - exp[nw:]) <= tol32[nw:]), a
+        if prevs is not None:
+            for r in range(R):
+                np.testing.assert_array_equal(prevs[r][a].cpu().numpy(), prevs[0][a].cpu().numpy())
+            assert np.all(np.abs(prevs[0][a].cpu().numpy() - exp) <= tol32), a
+    if (R * K) & (R * K - 1):
+        return
+    # a second call (fresh flags) over identical pods: with a power-of-two pod count the float32 mean is exact
+    snap = [p.clone() for p in params]
+    api.fuse_pods_local_ranks(c.cfg, nh, hid, params, K, tau=1.0)
+    torch.cuda.synchronize()
+    for r in range(R):
+        assert torch.equal(params[r], snap[r])
+
+
 def test_equity_curve_exact_and_backtest_metrics():
     """R#25: traj.equity (v_{t+1} after each step) equals the oracle's float64 account value bit for bit;
     the device backtest metrics of those curves match the oracle's metric definitions."""
