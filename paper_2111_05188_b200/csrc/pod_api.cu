@@ -381,7 +381,7 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         const char* ps = getenv("POD_PERSIST");
         e->persist = !(ps && ps[0] == '0');
         const char* pd = getenv("POD_PDL");
-        e->pdl = !(pd && pd[0] == '0');
+        e->pdl = (pd && pd[0] == '0') ? 0 : ((pd && pd[0] == '2') ? 2 : 1);   // 2: every env step (experiments)
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -655,7 +655,8 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         const int idle_sms = std::max(0, e->sm_count - actor_ctas);
         const bool dense = tiles >= 7 * e->sm_count;
         const bool roomy = 2 * idle_sms >= tiles;
-        const bool pdl = e->pdl && e->groups == 1 && !p.injected && (dense || roomy) && !(prof && t % prof->stride == 0);
+        const bool pdl = e->pdl && e->groups == 1 && !p.injected && (dense || roomy || e->pdl == 2) &&
+                         !(prof && t % prof->stride == 0);
         if (pdl) {
             a.pdl = 1;
             cudaLaunchConfig_t lc{};

@@ -27,6 +27,27 @@ def test_reference_arm_json_line():
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
 
 
+def test_gpus_flag_relaunches_one_rank_per_gpu():
+    """`--gpus N` without a torchrun environment re-executes bench.py under torch.distributed.run with N ranks
+    (rendezvous on 127.0.0.1); rank 0 alone prints the line, with n_gpus = N.  Checked through the reference
+    arm, the one bench path that runs without a GPU."""
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "C1", "--steps", "1",
+                          "--warmup", "1", "--gpus", "2"], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                         check=True)
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout + out.stderr
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_gpus_flag_must_match_world_size():
+    """Under torchrun, --gpus must equal WORLD_SIZE (a silent mismatch would mislabel the measurement)."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "C1", "--steps", "1",
+                        "--warmup", "1", "--gpus", "2"], cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)
+
+
 import pytest  # noqa: E402
 
 

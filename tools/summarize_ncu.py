@@ -25,7 +25,9 @@ for r in data:
     if m == "gpu__time_duration.sum":
         cnt[k] += 1
 tot = sum(a["gpu__time_duration.sum"] for a in agg.values())
-lines = ["# ncu launch list (C3 shapes: 8192 envs, n=100, 3x512; T=8 rollout + GAE + selection)",
+lines = ["# ncu launch list (C3 shapes: 8192 envs, n=100, 3x512; T=16 rollout + GAE + selection; "
+         "--cache-control none: L2 warm across launches, so DRAM write-backs of one launch land in the next ones "
+         "and the per-launch average over the window counts reads and writes)",
          "", "| kernel | launches | total us | avg us | share | DRAM read+write per launch (MB) |", "|---|---|---|---|---|---|"]
 traffic = {}
 for k, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]):
@@ -62,16 +64,20 @@ for k in ("actor_forward", "env_step", "gae"):
     out.append("")
 open(os.path.join(dst, "ncu_full_summary.md"), "w").write("\n".join(out) + "\n")
 
-# ---- per-launch DRAM traffic of the hot kernels, for bench.py's roofline.traffic
-def mb(x):
-    v, u = x.split()[0].replace(",", ""), x.split()[1] if len(x.split()) > 1 else "byte"
-    return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+# ---- per-launch DRAM traffic of the hot kernels, for bench.py's roofline.traffic: the multi-launch window of
+# the launch list (read + write, averaged over the launches of each kernel)
+names = {"pod::actor_forward_kernel": "actor_mlp", "gae": "gae"}
 tj = {}
-for k, name in (("actor_forward", "actor_mlp"), ("env_step", "env_step"), ("gae", "gae")):
-    if k in summ and "dram__bytes_read.sum" in summ[k]:
-        tj[name] = mb(summ[k]["dram__bytes_read.sum"]) + mb(summ[k]["dram__bytes_write.sum"])
-json.dump({"C3": tj, "_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from one ncu --set full capture "
-           "(profiles/" + os.path.basename(dst) + "/ncu_full_summary.md)"},
+for k, rw in traffic.items():
+    if "actor_forward" in k:
+        tj["actor_mlp"] = rw
+    elif "env_step_kernel" in k:
+        tj["env_step"] = max(tj.get("env_step", 0.0), rw)
+    elif "gae" in k and "normalize" not in k:
+        tj["gae"] = max(tj.get("gae", 0.0), rw)
+json.dump({"C3": tj, "_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over the launches of a "
+           "T = 16 C3 rollout with the L2 warm between launches (ncu --cache-control none; profiles/"
+           + os.path.basename(dst) + "/ncu_launches_c3.md)"},
           open(os.path.join(os.path.dirname(dst), "ncu_traffic.json"), "w"), indent=1)
 print("\n".join(lines))
 print("\n".join(out))
