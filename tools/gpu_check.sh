@@ -4,9 +4,9 @@ tag=$1; shift; kexpr=$1; shift
 out=gpurun_out/$tag; mkdir -p $out
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { echo build failed; tail -30 $out/build.log; exit 1; }
 if [ "$kexpr" = "all" ]; then
-  timeout 1800 python -m pytest tests -m gpu -x -q > $out/pytest.log 2>&1; echo "pytest rc=$?" >> $out/pytest.log
+  timeout ${PYTEST_TIMEOUT:-900} python -m pytest tests -m gpu -x -q > $out/pytest.log 2>&1; echo "pytest rc=$?" >> $out/pytest.log
 elif [ "$kexpr" != "none" ]; then
-  timeout 1800 python -m pytest tests -m gpu -x -q -k "$kexpr" > $out/pytest.log 2>&1; echo "pytest rc=$?" >> $out/pytest.log
+  timeout ${PYTEST_TIMEOUT:-900} python -m pytest tests -m gpu -x -q -k "$kexpr" > $out/pytest.log 2>&1; echo "pytest rc=$?" >> $out/pytest.log
 fi
 tail -3 $out/pytest.log 2>/dev/null
 for c in "$@"; do
