@@ -19,7 +19,7 @@
 //   FWD_HIDDEN  x = act(acc + b)  -> out [row][c], out_t [c][row]          (rows >= M written as 0)
 //   FWD_HEAD    z = acc + b       -> outf [row][c] (f32)
 //   DW          g = acc           -> outf [row][c] (f32, the gradient segment of W_l)
-//   DX          d = acc act'(x_l) -> out, out_t, and the column sums of the warp's 32 rows (the bias
+//   DX          d = acc act'(x_l) -> out, out_t, and the column sums of the tile's 128 rows (the bias
 //               gradient of the layer below, reduced later in a fixed order: deterministic)
 // act' from the stored post-activation x: ReLU' = [x > 0], tanh' = 1 - x^2.
 #pragma once
@@ -48,7 +48,7 @@ struct GemmEpi {
     T* out_t;            // [N][ld_out_t]             (FWD_HIDDEN, DX)
     float* outf;         // [rows][ld_outf]           (FWD_HEAD, DW)
     const T* xl;         // [rows][ld_xl]             (DX: the layer input, post-activation)
-    float* bpart;        // [rows / 32][N]            (DX: per-warp column sums)
+    float* bpart;        // [rows / 128][N]           (DX: per-tile column sums)
     int32_t ld_out, ld_out_t, ld_outf, ld_xl;
 };
 
@@ -122,7 +122,7 @@ __device__ __forceinline__ float warp_transpose_sum32(float (&v)[32], int lane) 
 // lane's row, rows of a warp consecutive); columns >= N are never stored
 template <class T>
 __device__ __forceinline__ void gemm_epilogue_chunk(const GemmEpi<T>& e, int row, int c0, float (&v)[32], int lane,
-                                                    const float* bias_s) {
+                                                    const float* bias_s, float* red_s) {
     const bool rv = row < e.M;
     const bool full = c0 + 32 <= e.N;
     if (e.mode == EPI_FWD_HIDDEN || e.mode == EPI_FWD_HEAD) {
@@ -176,13 +176,19 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const GemmEpi<T>& e, int row
     for (int j = 0; j < 32; ++j)
         if (c0 + j < e.N) e.out_t[static_cast<int64_t>(c0 + j) * e.ld_out_t + row] = from_f32<T>(v[j]);
     if (e.mode == EPI_DX) {
-        const float s = warp_transpose_sum32(v, lane);   // column c0 + lane, over the warp's 32 rows
-        if (c0 + lane < e.N) e.bpart[static_cast<int64_t>(row >> 5) * e.N + c0 + lane] = s;
+        // the tile's column sums: each warp's 32 rows (transpose-reduce), then the 4 warps in order
+        const int wq = (threadIdx.x >> 5) & 3;
+        red_s[wq * 32 + lane] = warp_transpose_sum32(v, lane);   // column c0 + lane
+        named_bar_sync(1, 128);
+        if (wq == 0 && c0 + lane < e.N)
+            e.bpart[static_cast<int64_t>(row >> 7) * e.N + c0 + lane] =
+                ((red_s[lane] + red_s[32 + lane]) + red_s[64 + lane]) + red_s[96 + lane];
+        named_bar_sync(1, 128);
     }
 }
 
 __host__ __device__ constexpr int gemm_smem_bytes(int BN) {
-    return 1024 + GEMM_STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + 256 + 4 * BN;
+    return 1024 + GEMM_STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + 256 + 4 * BN + 512;
 }
 
 // bf16 x bf16 -> f32 on tcgen05; grid (M_rows / 128, ceil(N / BN)); K a multiple of 64
@@ -201,6 +207,7 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(const __grid_constant__
     const uint32_t full_b = bars, empty_b = bars + 8u * GEMM_STAGES, done_b = bars + 16u * GEMM_STAGES;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(gsm + GEMM_STAGES * STAGE + 16 * GEMM_STAGES + 8);
     float* bias_s = reinterpret_cast<float*>(gsm + GEMM_STAGES * STAGE + 256);   // [BN] (forward epilogues)
+    float* red_s = bias_s + BN;                                                   // [4][32] (input-gradient)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == 0) tmem_alloc(smem_u32(tslot), TCOLS);
     if (tid == 32) {
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(const __grid_constant__
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        gemm_epilogue_chunk(ep, row, n0 + cc * 32, v, lane, bias_s + cc * 32);
+        gemm_epilogue_chunk(ep, row, n0 + cc * 32, v, lane, bias_s + cc * 32, red_s);
     }
     tc_fence_before();
     __syncthreads();
@@ -272,6 +279,7 @@ __global__ void __launch_bounds__(128) simt_gemm_f32_kernel(const float* __restr
     __shared__ float As[32][GEMM_BM + 1];
     __shared__ float Bs[32][BN];
     __shared__ float bias_s[BN];
+    __shared__ float red_s[128];
     const int tid = threadIdx.x, lane = tid & 31;
     const int m0 = static_cast<int>(blockIdx.x) * GEMM_BM, n0 = static_cast<int>(blockIdx.y) * BN;
     if (ep.bias)
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(128) simt_gemm_f32_kernel(const float* __restr
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = acc[cc * 32 + j];
-        gemm_epilogue_chunk(ep, row, n0 + cc * 32, v, lane, bias_s + cc * 32);
+        gemm_epilogue_chunk(ep, row, n0 + cc * 32, v, lane, bias_s + cc * 32, red_s);
     }
 }
 

@@ -52,7 +52,7 @@ inline PpoWs ppo_ws_layout(const pod_actor_layout& L, int n_hidden, int hidden, 
     }
     for (int l = 1; l <= n_hidden; ++l)   // W_l^T [in_l][out_l (head: padded to 64)]
         w.wt[l] = take(E * static_cast<size_t>(hidden) * (l == n_hidden ? w.kp64 : hidden));
-    for (int l = 0; l < n_hidden; ++l) w.bpart[l] = take(sizeof(float) * (Bp / 32) * hidden);
+    for (int l = 0; l < n_hidden; ++l) w.bpart[l] = take(sizeof(float) * (Bp / 128) * hidden);
     w.bpart[n_hidden] = take(sizeof(float) * (Bp / PPO_HEAD_ROWS) * L.n_out_pad);
     w.lspart = take(sizeof(float) * (Bp / PPO_HEAD_ROWS) * L.n_out_pad);
     w.act = take(sizeof(float) * Bp * n);
@@ -259,8 +259,8 @@ pod_status ppo_enqueue(const PpoPlan& p, cudaStream_t s, cudaStream_t s2) {
     br.n_layers = NL;
     br.n = p.n;
     br.n_out_pad = L.n_out_pad;
-    br.nparts = Bp / 32;
     for (int l = 0; l < NL; ++l) {
+        br.nparts[l] = l == NL - 1 ? Bp / PPO_HEAD_ROWS : Bp / GEMM_BM;
         br.rows[l] = L.w_rows[l];
         br.part[l] = reinterpret_cast<const float*>(w + W.bpart[l]);
     }

@@ -35,8 +35,8 @@ struct PpoDev {
     uint32_t err;
 };
 
-constexpr int PPO_HEAD_WARPS = 8;
-constexpr int PPO_HEAD_SPW = 4;                                   // samples per warp
+constexpr int PPO_HEAD_WARPS = 32;                                // one sample per warp: the head's latency is
+constexpr int PPO_HEAD_SPW = 1;                                   // one sample's (samples per warp)
 constexpr int PPO_HEAD_ROWS = PPO_HEAD_WARPS * PPO_HEAD_SPW;      // samples per block (32: one partial per 32 rows)
 
 template <class T>
@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(32 * PPO_HEAD_WARPS) ppo_head_kernel(const Ppo
 // the bias and log-std gradients are reduced from their partials (one per 32 rows) inside the Adam kernel,
 // in a fixed order (deterministic)
 struct PpoBiasReduce {
-    int32_t n_layers, n, n_out_pad, nparts;        // nparts = B_pad / 32 for every layer
+    int32_t n_layers, n, n_out_pad;
+    int32_t nparts[POD_MAX_HIDDEN_LAYERS + 1];     // partials of layer l (B_pad / 128; the head: B_pad / 32)
     int32_t rows[POD_MAX_HIDDEN_LAYERS + 1];       // bias length of layer l
     const float* part[POD_MAX_HIDDEN_LAYERS + 1];  // [nparts][rows]
     const float* lspart;                           // [nparts][n_out_pad]
@@ -274,9 +275,14 @@ __global__ void ppo_adam_narrow_kernel(const __grid_constant__ FuseArgs fa, cons
                                        const PpoDev* __restrict__ d, int j) {
     if (d->err) return;
     const float lr = d->lr, b1 = d->b1, b2 = d->b2, eps = d->eps;
-    const double step = static_cast<double>(d->step_base + j + 1);
-    const float c1 = static_cast<float>(1.0 - pow(static_cast<double>(b1), step));
-    const float c2 = static_cast<float>(1.0 - pow(static_cast<double>(b2), step));
+    __shared__ float c12[2];   // the bias corrections 1 - beta^t, once per block (float64 pow)
+    if (threadIdx.x == 0) {
+        const double step = static_cast<double>(d->step_base + j + 1);
+        c12[0] = static_cast<float>(1.0 - pow(static_cast<double>(b1), step));
+        c12[1] = static_cast<float>(1.0 - pow(static_cast<double>(b2), step));
+    }
+    __syncthreads();
+    const float c1 = c12[0], c2 = c12[1];
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t n8 = fa.n_elems / 8;
     for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n8; q += stride) {
@@ -295,7 +301,8 @@ __global__ void ppo_adam_narrow_kernel(const __grid_constant__ FuseArgs fa, cons
             const float* src = ls ? br.lspart : br.part[l];
             const int rows = ls ? br.n_out_pad : br.rows[l];
             float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int p = 0; p < br.nparts; ++p) {
+            const int np = br.nparts[ls ? br.n_layers - 1 : l];
+            for (int p = 0; p < np; ++p) {
                 const float4* r4 = reinterpret_cast<const float4*>(src + static_cast<int64_t>(p) * rows + o);
                 const float4 a0 = r4[0], a1 = r4[1];
                 acc[0] += a0.x; acc[1] += a0.y; acc[2] += a0.z; acc[3] += a0.w;
