@@ -304,26 +304,31 @@ def test_degenerate_calls():
 
 
 # ----------------------------------------------------------------- full size (bench launch config)
-def test_full_size_c3_sampled_rows():
-    """C3 launch configuration (8192 envs, n=100, 3x512, one agent) on sampled rows."""
-    c = Case(n=100, f=3, T_data=60_000, N=8192, H=2000, seed=5191, dt=1 / (252 * 390))
-    aws, params, actor = _actor(c, 3, 512)
+@pytest.mark.parametrize("agents", [1, 8])
+def test_full_size_c3_sampled_rows(agents):
+    """C3 launch configuration (8192 envs, n=100, 3x512, one agent) on sampled rows; with 8 agents, C4's
+    (8 x 1,024 envs: agent switches between the clusters' tiles)."""
+    c = Case(n=100, f=3, T_data=60_000, N=8192, H=2000, n_agents=agents, seed=5191, dt=1 / (252 * 390))
+    aws, params, actor = _actor(c, 3, 512, n_agents=agents)
     T = 4
     tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, debug=True)
     c.env.reset(c.starts)
     c.env.rollout(T, tr, actor=actor)
     c.env.check()
-    rows = np.unique(np.concatenate([np.arange(0, 8192, 257), [8191, 127, 128]]))
+    rows = np.unique(np.concatenate([np.arange(0, 8192, 257), [8191, 127, 128, 1023, 1024, 4095, 4096]]))
     obs_g = bf16_to_f64(tr.obs)[..., : c.obs_dim]
     mu_g = tr.mu.cpu().numpy().astype(np.float64)
-    w = oracle.actor_flat(aws[0].W, aws[0].b, aws[0].log_std)
     raw_g = tr.act.cpu().numpy().astype(np.float64)
     logp_g = tr.logp.cpu().numpy().astype(np.float64)
-    ls = aws[0].log_std.astype(np.float64)
+    per = 8192 // agents
     for t in range(T):
-        mu_check(mu_g[t, rows], oracle.actor_mu(w, obs_g[t, rows], 3, 512, 100))
+        for a in range(agents):
+            ra = rows[(rows >= a * per) & (rows < (a + 1) * per)]
+            w = oracle.actor_flat(aws[a].W, aws[a].b, aws[a].log_std)
+            mu_check(mu_g[t, ra], oracle.actor_mu(w, obs_g[t, ra], 3, 512, 100))
         # noise (Philox, drawn by the previous env step) and the log-prob (partials summed by the env step)
         for e in rows:
+            ls = aws[int(e) // per].log_std.astype(np.float64)
             z_o = oracle.normals(c.cfg.seed, c.cfg.env_offset + int(e), t, 100)
             z_g = (raw_g[t, e] - mu_g[t, e]) / np.exp(ls)
             assert np.all(np.abs(z_g - z_o) <= 2e-5 * np.abs(z_o) + 5e-4), (t, e)
@@ -333,7 +338,7 @@ def test_full_size_c3_sampled_rows():
     # env replay on the sampled envs (envs are independent: batch equivalence)
     a_g = tr.dbg_aint.cpu().numpy()
     starts = c.env_starts()[rows]
-    o = oracle.Env(c.market.close, c.market.feat, len(rows), **c.kw)
+    o = oracle.Env(c.market.close, c.market.feat, len(rows), **dict(c.kw, n_agents=1))
     o.reset(starts)
     out = o.rollout(T, "replay", a_rep=np.ascontiguousarray(a_g[:, rows]), want=("obs", "rew", "done", "hold", "cash"))
     np.testing.assert_array_equal(tr.dbg_hold.cpu().numpy()[:, rows], out["hold"])
@@ -342,6 +347,38 @@ def test_full_size_c3_sampled_rows():
     assert_obs_close(tr.obs[:, rows], out["obs"], c.obs_dim)
     # properties over all rows
     assert (tr.dbg_cash >= 0).all() and (tr.dbg_hold >= 0).all()
+
+
+def test_full_size_c2_sampled_rows():
+    """C2 launch configuration (Dow-30 daily, 4,096 envs, 2x128, H = 1,024: the env step launched as a
+    programmatic dependent of the actor, whose 32 M-tiles leave most SMs idle) on sampled rows, T = 6."""
+    c = Case(n=30, f=3, T_data=2611, N=4096, H=1024, seed=5190)
+    aws, params, actor = _actor(c, 2, 128)
+    T = 6
+    tr = api.Trajectory.allocate(T, c.N, c.n, c.k_pad, debug=True, critic=True)
+    c.env.reset(c.starts)
+    c.env.rollout(T, tr, actor=actor)
+    c.env.check()
+    rows = np.unique(np.concatenate([np.arange(0, 4096, 131), [4095, 31, 32, 127, 128, 2047, 2048]]))
+    obs_g = bf16_to_f64(tr.obs)[:, rows, : c.obs_dim]
+    mu_g = tr.mu.cpu().numpy()[:, rows].astype(np.float64)
+    val_g = tr.val.cpu().numpy()[:, rows].astype(np.float64)
+    w = oracle.actor_flat(aws[0].W, aws[0].b, aws[0].log_std)
+    for t in range(T):
+        mu_check(mu_g[t], oracle.actor_mu(w, obs_g[t], 2, 128, 30))
+        v_o = oracle.actor_value(aws[0].W, aws[0].b, aws[0].w_v, aws[0].b_v, obs_g[t], 2, 128)
+        v_abs = np.abs(oracle.actor_value(aws[0].W, aws[0].b, np.abs(aws[0].w_v), abs(aws[0].b_v), obs_g[t], 2, 128))
+        rms = math.sqrt(float(np.mean(v_o ** 2)))
+        assert np.all(np.abs(val_g[t] - v_o) <= 2e-2 * (np.abs(v_o) + rms) + 1e-2 * v_abs + 1e-6), t
+    a_g = tr.dbg_aint.cpu().numpy()
+    o = oracle.Env(c.market.close, c.market.feat, len(rows), **c.kw)
+    o.reset(c.env_starts()[rows])
+    out = o.rollout(T, "replay", a_rep=np.ascontiguousarray(a_g[:, rows]), want=("obs", "rew", "done", "hold", "cash"))
+    np.testing.assert_array_equal(tr.dbg_hold.cpu().numpy()[:, rows], out["hold"])
+    np.testing.assert_array_equal(tr.dbg_cash.cpu().numpy()[:, rows], out["cash"])
+    np.testing.assert_array_equal(tr.rew.cpu().numpy()[:, rows], out["rew"].astype(np.float32))
+    np.testing.assert_array_equal(tr.done.cpu().numpy()[:, rows], out["done"])
+    assert_obs_close(tr.obs[:, rows], out["obs"], c.obs_dim)
 
 
 @pytest.mark.parametrize("agents", [1, 8])
