@@ -18,6 +18,7 @@
 // coalesced 128-B row stores.  Misaligned inputs (N % 16 != 0) use the
 // plain-load path (same arithmetic, same order).
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include <cuda.h>
@@ -192,6 +193,12 @@ inline size_t gae_seg_smem_bytes(int seg, int cpw) {
     return static_cast<size_t>(seg) * cpw * sizeof(GaeStage) + sizeof(GaeSegSum) + 8 * GAE_SEG_MAX * GAE_CPW_MAX + 128;
 }
 
+// NORM: the per-buffer normalisation (R#23) fused in — a cooperative launch (every block resident): block 0
+// zeroes the statistics before a first grid barrier, pass 2 keeps A in shared memory (over r, no longer
+// needed) instead of writing it, the float64 sums are flushed, a second grid barrier, and every block
+// rewrites its own A as (A - m) / s — one launch and one pass over adv instead of three launches (memset,
+// scan, normalisation) and a re-read.
+template <bool NORM>
 __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
     gae_seg_kernel(const __grid_constant__ GaeMaps maps, const float* __restrict__ boot, int T, int N, float gamma,
                    float lambda, float* __restrict__ adv, float* __restrict__ ret, int cpw,
@@ -223,6 +230,13 @@ __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
         }
     }
     __syncthreads();   // every warp's barrier initialisation is visible before anyone waits on it
+    if (NORM) {   // zero the statistics before anyone adds to them (the loads above are in flight meanwhile)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            stats[0] = 0.0;
+            stats[1] = 0.0;
+        }
+        cooperative_groups::this_grid().sync();
+    }
     for (int j = j0; j < j1; ++j) mbar_wait(bars + 8u * j, 0u);
     // V at the row just after this segment (first row of the newer warp's oldest chunk) or the bootstrap
     float v_in = boot[active ? e : e0];
@@ -268,7 +282,8 @@ __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
             const float A = delta + gl * nd * a_next;
             if (active) {
                 const int64_t i = static_cast<int64_t>(t_base + q) * N + e;
-                adv[i] = A;
+                if (NORM) st[j].r[q][lane] = A;   // r of this row is not read again
+                else adv[i] = A;
                 ret[i] = A + v;
                 s1 += A;
                 s2 += static_cast<double>(A) * A;
@@ -278,6 +293,21 @@ __global__ void __launch_bounds__(32 * GAE_SEG_MAX)
         }
     }
     if (stats) gae_stats_flush(s1, s2, stats);
+    if (NORM) {
+        cooperative_groups::this_grid().sync();
+        const double count = static_cast<double>(T) * N;
+        const double m = __ldcg(stats) / count;
+        const double var = __ldcg(stats + 1) / count - m * m;
+        const float mf = static_cast<float>(m);
+        const float inv = var > 0.0 ? static_cast<float>(1.0 / sqrt(var)) : 0.0f;
+        if (active)
+            for (int j = j0; j < j1; ++j) {
+                const int t_base = T - (j + 1) * GAE_L;
+                const int q_lo = t_base < 0 ? -t_base : 0;
+                for (int q = GAE_L - 1; q >= q_lo; --q)
+                    adv[static_cast<int64_t>(t_base + q) * N + e] = (st[j].r[q][lane] - mf) * inv;
+            }
+    }
 }
 
 // advantage normalisation in place (R#23): A <- (A - m) / s, m = S1 / count, s^2 = S2 / count - m^2

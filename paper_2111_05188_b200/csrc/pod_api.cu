@@ -980,18 +980,17 @@ extern "C" pod_status pod_env_read_state(pod_env_t* e, int32_t* hold, double* ca
 // ------------------------------------------------------------ GAE
 static pod_status gae_launch(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
                              int32_t N, float gamma, float lambda, float* adv, float* ret, double* stats,
-                             cudaStream_t stream);
+                             cudaStream_t stream, bool* normalized);
 
 extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
                               int32_t N, float gamma, float lambda, float* adv, float* ret, double* adv_stats,
                               void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (adv_stats) {
-        if (reinterpret_cast<uintptr_t>(adv_stats) % 8 != 0) return pod_fail(POD_ERR_ARG, "adv_stats must be 8-byte aligned");
-        POD_CUDA(cudaMemsetAsync(adv_stats, 0, 2 * sizeof(double), s));
-    }
-    pod_status st = gae_launch(rew, val, done, boot, T, N, gamma, lambda, adv, ret, adv_stats, s);
-    if (st || !adv_stats) return st;
+    if (adv_stats && reinterpret_cast<uintptr_t>(adv_stats) % 8 != 0)
+        return pod_fail(POD_ERR_ARG, "adv_stats must be 8-byte aligned");
+    bool normalized = false;
+    pod_status st = gae_launch(rew, val, done, boot, T, N, gamma, lambda, adv, ret, adv_stats, s, &normalized);
+    if (st || !adv_stats || normalized) return st;
     const int64_t count = static_cast<int64_t>(T) * N;
     const int64_t want = (count / 4 + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
@@ -1002,7 +1001,8 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
 
 static pod_status gae_launch(const float* rew, const float* val, const uint8_t* done, const float* boot, int32_t T,
                              int32_t N, float gamma, float lambda, float* adv, float* ret, double* stats,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, bool* normalized) {
+    *normalized = false;
     if (!rew || !val || !done || !boot || !adv || !ret) return pod_fail(POD_ERR_ARG, "GAE pointers must be non-NULL");
     if (T < 1 || N < 1) return pod_fail(POD_ERR_ARG, "T and N must be >= 1");
     if (static_cast<int64_t>(T) * N >= (1ll << 40)) return pod_fail(POD_ERR_SHAPE, "T * N too large");
@@ -1067,11 +1067,13 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
         {
             std::lock_guard<std::mutex> lk(seg_mu);
             if (seg_attr[cur_dev] < want) {
-                cudaError_t ce = cudaFuncSetAttribute(gae_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
+                cudaError_t ce = cudaFuncSetAttribute(gae_seg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
+                if (ce == cudaSuccess)
+                    ce = cudaFuncSetAttribute(gae_seg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
                 if (ce != cudaSuccess) {
                     cudaFuncAttributes fa;
                     memset(&fa, 0, sizeof(fa));
-                    cudaError_t ce2 = cudaFuncGetAttributes(&fa, gae_seg_kernel);
+                    cudaError_t ce2 = cudaFuncGetAttributes(&fa, gae_seg_kernel<false>);
                     int dev = 0, optin = 0;
                     cudaGetDevice(&dev);
                     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1084,11 +1086,40 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
                 seg_attr[cur_dev] = want;
             }
         }
-        gae_seg_kernel<<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw), stream>>>(
+        if (stats) {
+            // normalisation fused in when every block fits on the device at once (cooperative launch)
+            int per_sm = 0, sms = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_seg_kernel<true>, 32 * seg,
+                                                          gae_seg_smem_bytes(seg, cpw));
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
+            static const bool fuse_off = [] {   // experiments: POD_GAE_FUSED_NORM=0 keeps the separate pass
+                const char* v = getenv("POD_GAE_FUSED_NORM");
+                return v && v[0] == '0';
+            }();
+            if (!fuse_off && per_sm * sms >= groups) {
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3(static_cast<unsigned>(groups));
+                lc.blockDim = dim3(static_cast<unsigned>(32 * seg));
+                lc.dynamicSmemBytes = gae_seg_smem_bytes(seg, cpw);
+                lc.stream = stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                POD_CUDA(cudaLaunchKernelEx(&lc, gae_seg_kernel<true>, maps, boot, T, N, gamma, lambda, adv, ret, cpw,
+                                            stats));
+                *normalized = true;
+                return POD_OK;
+            }
+            POD_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(double), stream));
+        }
+        gae_seg_kernel<false><<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw), stream>>>(
             maps, boot, T, N, gamma, lambda, adv, ret, cpw, stats);
         POD_CUDA(cudaGetLastError());
         return POD_OK;
     }
+    if (stats) POD_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(double), stream));
     const unsigned blocks = static_cast<unsigned>((groups + GAE_WARPS - 1) / GAE_WARPS);
     {
         // per-device opt-in (pod_gae may run on any device without an env handle there)
