@@ -38,6 +38,7 @@
 
 #include <cstdint>
 
+#include "env_kernel.cuh"
 #include "philox.cuh"
 #include "ptx.cuh"
 
@@ -121,7 +122,29 @@ constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
     return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_STAGE_BYTES +
-           ACT_BIAS_FLOATS * 4 + 2 * 4 * 128 * 4 + 256;   // + double-buffered log-prob partials + barriers
+           ACT_BIAS_FLOATS * 4 + 2 * 4 * 128 * 4 + 512;   // + double-buffered log-prob partials + barriers
+}
+
+// The fused rollout (rollout_fused_kernel): one cluster per 128-env M-tile runs the actor AND the env step
+// of its 128 envs for all T steps.  The env part of step t (4 env tiles of 32 envs: two per CTA, one per
+// 4-warp half of the epilogue warps) runs in the activation buffer, which is idle between the head's MMAs
+// and the next observation.
+struct FusedEnvArgs {
+    EnvArgs env;        // the env-step arguments with the step-0 slices (rew, done, obs_out = obs[1], ...)
+    int32_t T;          // steps; iteration T (when val_out is set) is the critic bootstrap pass over obs[T]
+    int32_t sampling;   // the env step of step t draws the actor noise of step t+1 (t + 1 < T)
+    int32_t env_stride; // bytes between the two env tiles' shared-memory areas inside the activation buffer
+    int32_t k_pad;
+};
+struct FusedMaps {
+    ActorMaps am;
+    EnvMaps em;
+};
+// shared memory of the two env tiles of a CTA fits in the activation buffer
+inline bool fused_env_fits(int n, int k_pad, int hidden) {
+    const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
+    const int es = (env_smem_bytes(n, k_pad) + 127) / 128 * 128;
+    return 2 * es <= ka * 16384;
 }
 
 // tanh(x) = 1 - 2 / (e^{2x} + 1) on the SFU (ex2.approx, approximate reciprocal): absolute error
@@ -156,8 +179,11 @@ __device__ __forceinline__ void epi_pack(const uint32_t (&v)[32], const float4* 
     }
 }
 
-__global__ void __launch_bounds__(ACT_THREADS, 1)
-    actor_forward_kernel(const __grid_constant__ ActorMaps maps, const ActorArgs a) {
+// FUSED: the rollout kernel (one M-tile per cluster, iteration it = step it, see FusedEnvArgs); else the
+// actor forward of one step over M-tiles mtile0 + c, + c + nclusters, ...
+template <bool FUSED, int SELL_UNROLL, int BUY_UNROLL>
+__device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArgs& a, const EnvMaps* emaps,
+                                           const FusedEnvArgs* fe) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -193,6 +219,11 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     const uint32_t logpfree_b = obs_b + 96u;   // [2] CTA 1: CTA 0 has read partial buffer p (1 remote arrival)
     const uint32_t tslot_s = obs_b + 112u;
     const uint32_t accl_b = obs_b + 120u;      // this CTA's MMAs of a layer are complete (local commit)
+    // FUSED: both CTAs' heads of step t are written (2 arrivals: this CTA's and the peer's), both CTAs' env
+    // steps of step t are done (s_{t+1}, holdings and noise written), and the env tiles' own mbarriers
+    const uint32_t headdone_b = obs_b + 128u;
+    const uint32_t envdone_b = obs_b + 136u;
+    const uint32_t envbar_b = obs_b + 144u;    // [2 tiles][1 + ENV_BUY_CHUNKS]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
     // persistent over M-tiles: cluster c (one CTA pair per M-tile) takes tiles mtile0 + c + it * nclusters
@@ -201,8 +232,11 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     struct Tile {
         int agent, env0, rows_valid;
     };
+    // FUSED: iterations 0..T-1 are the steps, T the critic bootstrap pass (when val_out is set)
+    const int n_iter = FUSED ? fe->T + (a.val_out ? 1 : 0) : 0;
     auto tile_of = [&](int it, Tile& tl) -> bool {
-        const int k = cid + it * ncl;
+        if (FUSED && it >= n_iter) return false;
+        const int k = FUSED ? cid : cid + it * ncl;
         if (k >= a.mtiles) return false;
         const int mtile = a.mtile0 + k;
         tl.agent = mtile / a.tiles_per_agent;
@@ -238,6 +272,14 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 mbar_init(ownrdy_b + 8u * j, 256);   // the 256 epilogue threads
                 mbar_init(peerrdy_b + 8u * j, 1);    // the MMA thread's expect_tx + the peer's bytes
             }
+            if (FUSED) {
+                mbar_init(headdone_b, 2);
+                mbar_init(envdone_b, 2);
+                for (int g = 0; g < 2; ++g) {
+                    mbar_init(envbar_b + 64u * g, 1);   // the env tile's TMA barrier
+                    for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(envbar_b + 64u * g + 8u * (c + 1), 32);
+                }
+            }
             fence_mbar_init();
             prefetch_tmap(&maps.obs);
             for (int l = 0; l < a.n_layers; ++l) prefetch_tmap(&maps.w[l]);
@@ -250,12 +292,12 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     tc_fence_after();
     // the env-step grid that follows may be scheduled now (its blocks stage their inputs on free SMs and
     // wait for this grid's completion before reading the actions); a no-op without a dependent
-    if (threadIdx.x == 0) pdl_launch_dependents();
+    if (!FUSED && threadIdx.x == 0) pdl_launch_dependents();
     const uint32_t tmem = *tslot;
-    unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 64 : nullptr;
+    unsigned long long* tr = (a.trace && !FUSED) ? a.trace + blockIdx.x * 64 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = clock64();
 #ifdef POD_EXP_GTIME
-    if (threadIdx.x == 0 && a.t < 1024) atomicMin(&g_gtime[a.t][0], gtimer());
+    if (!FUSED && threadIdx.x == 0 && a.t < 1024) atomicMin(&g_gtime[a.t][0], gtimer());
 #endif
 
     if (warp == 0) {
@@ -266,12 +308,31 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             Tile tl;
             for (int it = 0; tile_of(it, tl); ++it) {
                 // the obs tile goes into act_s once this CTA's MMAs of the previous tile are done with it
-                if (it > 0) mbar_wait(actfree_b, static_cast<uint32_t>(it - 1) & 1u);
-                const int kb0 = a.k_pad / 64;
-                mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
-                for (int kb = 0; kb < kb0; ++kb)
-                    tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, a.obs_row0 + tl.env0, obs_b);
+                // (FUSED: and both CTAs' env steps of the previous step, which write s_{t+1} and use act_s
+                // as their shared memory, are done; the first ring stages of layer 0 are issued before that
+                // wait, so the weight stream of step t+1 starts during the env step of step t)
+                bool obs_issued = false;
+                int pre = it > 0 ? ACT_STAGES : 0;
+                auto issue_obs = [&] {
+                    if (it > 0) mbar_wait(actfree_b, static_cast<uint32_t>(it - 1) & 1u);
+                    if (FUSED && it > 0) mbar_wait_cluster(envdone_b, static_cast<uint32_t>(it - 1) & 1u);
+                    const int kb0 = a.k_pad / 64;
+                    const int row0 = FUSED ? it * a.N : a.obs_row0;
+                    mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
+                    for (int kb = 0; kb < kb0; ++kb)
+                        tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, row0 + tl.env0, obs_b);
+                    obs_issued = true;
+                };
+                auto before_stage = [&](int l) {
+                    if constexpr (FUSED) {
+                        if (l == 0 && !obs_issued && pre-- == 0) issue_obs();
+                    }
+                };
+                if constexpr (!FUSED) issue_obs();
                 for (int l = 0; l < a.n_layers; ++l) {
+                    if constexpr (FUSED) {
+                        if (l == 1 && !obs_issued) issue_obs();
+                    }
                     const int K = l == 0 ? a.k_pad : a.hidden;
                     const int half = actor_layer_out(l, a.n_layers, a.hidden, a.n_out_pad) / 2;
                     const int bn = actor_bn(half);
@@ -284,6 +345,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         const int kso = l == 0 ? 0 : static_cast<int>(rank) * (ns / 2);
                         for (int j = 0; j < ns; ++j) {
                             const int ks = (j + kso) % ns;
+                            before_stage(l);
                             mbar_wait(empty_b + 8u * stage, phase ^ 1u);
                             mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn * kp) * (ACT_BK * 2));
                             tma_load_4d(ring_s + stage * stage_bytes, &maps.w[l], 0, static_cast<int>(rank) * half,
@@ -299,6 +361,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                     for (int c = 0; c < half / bn; ++c) {
                         for (int j = 0; j < KB; ++j) {
                             const int kb = (j + kbo) % KB;
+                            before_stage(l);
                             mbar_wait(empty_b + 8u * stage, phase ^ 1u);
                             mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * (ACT_BK * 2));
                             if (!a.mc) {
@@ -319,6 +382,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         }
                     }
                 }
+                if constexpr (FUSED) {
+                    if (!obs_issued) issue_obs();
+                }
             }
         }
         __syncwarp();
@@ -334,6 +400,10 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             for (int it = 0; tile_of(it, tl); ++it) {
                 mbar_wait(obs_b, static_cast<uint32_t>(it) & 1u);
                 tc_fence_after();
+#ifdef POD_EXP_GTIME
+                // fused rollout, CTA 0: [step][obs landed, head accumulator ready, both heads written, env done]
+                if (FUSED && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
+#endif
                 if (tr && it == 0) tr[1] = clock64();
                 for (int l = 0; l < a.n_layers; ++l) {
                     const int g = it * a.n_layers + l;                 // layer count over tiles: TMEM buffer g & 1
@@ -453,14 +523,27 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 }
                 staged_agent = tl.agent;
             }
-            // prefetch this thread's head noise z (written by the previous env-step launch):
+            // this iteration's outputs (FUSED: the slices of step it; iteration T is the value-only pass)
+            const bool vo = a.value_only || (FUSED && it == fe->T);
+            const bool det = a.deterministic || vo;
+            const int64_t so = FUSED ? it : 0;
+            const int64_t Nn = static_cast<int64_t>(a.N) * a.n;
+            float* const act_out = vo ? nullptr : a.act_out + so * Nn;
+            float* const mu_out = (vo || !a.mu_out) ? nullptr : a.mu_out + so * Nn;
+            int16_t* const dbg_aint = (vo || !a.dbg_aint) ? nullptr : a.dbg_aint + so * Nn;
+            float* const logp_out = (vo || !a.logp_out) ? nullptr : a.logp_out + so * a.N;
+            float* const val_out = a.val_out ? a.val_out + so * a.N : nullptr;
+            // FUSED: both CTAs' env steps of the previous step are done (the noise of this step is written)
+            if (FUSED && it > 0) mbar_wait_cluster(envdone_b, static_cast<uint32_t>(it - 1) & 1u);
+            // prefetch this thread's head noise z (written by the previous env step; L2 loads: the peer CTA
+            // writes half of it inside the fused kernel):
             // one round of independent loads, long before the head needs them
             float zr[ACT_MAX_HQ];
 #pragma unroll
             for (int q = 0; q < ACT_MAX_HQ; ++q) {
                 const int i = static_cast<int>(rank) * head_half + hh * hq + q;
-                zr[q] = (q < hq && valid && i < a.n && !a.deterministic) ? a.znoise[static_cast<int64_t>(i) * a.N + e]
-                                                                          : 0.0f;
+                const float* zp = a.znoise + static_cast<int64_t>(i) * a.N + e;
+                zr[q] = (q < hq && valid && i < a.n && !det) ? (FUSED ? __ldcg(zp) : *zp) : 0.0f;
             }
             named_bar_sync(1, 256);
             int boff = 0;
@@ -508,7 +591,12 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             const int gL = it * a.n_layers + L;
             mbar_wait(accl_b, static_cast<uint32_t>(gL) & 1u);
             tc_fence_after();
+#ifdef POD_EXP_GTIME
+            if (FUSED && blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][1] = gtimer();
+#endif
             if (tr && it == 0 && etid == 0) tr[24] = clock64();
+            // the head: sampling, the action map and the log-prob partials
+            auto head = [&] {
             const float* bias = bias_s + boff;
             const float* log_std = bias_s + boff + head_half;
             const float* sigma = bias_s + boff + 2 * head_half;
@@ -526,15 +614,15 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 __syncwarp();
                 tmem_ld8(trow + (static_cast<uint32_t>(gL) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
                 tmem_ld_wait();
-                if (valid && i0 <= a.n && a.val_out && a.n < i0 + 8) {
+                if (valid && i0 <= a.n && val_out && a.n < i0 + 8) {
                     // critic: head row n over the same trunk (R#22)
                     float vh = 0.0f;
     #pragma unroll
                     for (int jj = 0; jj < 8; ++jj)
                         if (i0 + jj == a.n) vh = __uint_as_float(hv[jj]);
-                    a.val_out[e] = vh + bias[tc + (a.n - i0)];
+                    val_out[e] = vh + bias[tc + (a.n - i0)];
                 }
-                if (valid && i0 < a.n && !a.value_only) {
+                if (valid && i0 < a.n && !vo) {
                     float raw[8], mu[8];
                     int16_t ai8[8];
     #pragma unroll
@@ -550,10 +638,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         bad |= !isfinite(mu[jj]);
                         raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
                         logp += (-0.5f * z * z - ls) - half_ln_2pi;
+#if defined(POD_EXP_HEAD) && POD_EXP_HEAD == 3
+                        ai8[jj] = static_cast<int16_t>(raw[jj]);
+#else
                         const float u = tanh_sfu(raw[jj]);
                         const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
                         ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
+#endif
+#if !defined(POD_EXP_HEAD) || POD_EXP_HEAD != 2
                         a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
+#endif
                     };
                     // chunk-uniform branch: straight-line code for the full 8-ticker chunks
                     if (i0 + 8 <= a.n) {
@@ -564,12 +658,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                         for (int jj = 0; jj < 8; ++jj)
                             if (i0 + jj < a.n) sample(jj);
                     }
-                    if (a.dbg_aint) {
+                    if (dbg_aint) {
                         for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
-                            a.dbg_aint[static_cast<int64_t>(e) * a.n + i0 + jj] = ai8[jj];
+                            dbg_aint[static_cast<int64_t>(e) * a.n + i0 + jj] = ai8[jj];
                     }
-                    float* arow = a.act_out + static_cast<int64_t>(e) * a.n + i0;
-                    float* mrow = a.mu_out ? a.mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;
+#if defined(POD_EXP_HEAD) && POD_EXP_HEAD == 1
+                    if (raw[0] == 12345.0f)
+#endif
+                    {
+                    float* arow = act_out + static_cast<int64_t>(e) * a.n + i0;
+                    float* mrow = mu_out ? mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;
                     if (vec && i0 + 8 <= a.n) {
                         reinterpret_cast<float4*>(arow)[0] = make_float4(raw[0], raw[1], raw[2], raw[3]);
                         reinterpret_cast<float4*>(arow)[1] = make_float4(raw[4], raw[5], raw[6], raw[7]);
@@ -586,6 +684,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                             }
                         }
                     }
+                    }
                 }
             }
             if (bad && valid) atomicOr(a.err, 1u);
@@ -595,7 +694,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
             if (a.logp_parts) {
                 // the env step that follows combines the four partials ((p0 + p1) + p2) + p3: no
                 // cross-CTA exchange in this kernel's tail
-                if (valid && a.logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
+                if (valid && logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
             } else {
                 const uint32_t pb = static_cast<uint32_t>(it) & 1u;
                 float* logp_s = logp_s0 + pb * 512;
@@ -605,11 +704,70 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
                 mbar_arrive_remote(mapa_shared(logp_b, cr & ~1u));   // release: the partial is visible with the arrival
                 if (rank == 0) {
                     mbar_wait_cluster(logp_b, static_cast<uint32_t>(it) & 1u);
-                    if (hh == 0 && valid && a.logp_out)
-                        a.logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
+                    if (hh == 0 && valid && logp_out)
+                        logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
                     named_bar_sync(2, 256);
                     if (etid == 0) mbar_arrive_remote(mapa_shared(logpfree_b + 8u * pb, peer));
                 }
+            }
+            };
+            if constexpr (FUSED) {
+                if (!vo) {
+                    // ----- the env step of step it on this CTA's two env tiles of the M-tile (epilogue warps
+                    // 2-5: tile 2 rank, warps 6-9: tile 2 rank + 1), once both CTAs' heads are written.
+                    // (Issuing the tiles' holdings TMA and state loads before the head instead slowed the
+                    // head more than it hid: C3 37.6 -> 38.4 us per step.)
+                    head();
+#ifdef POD_EXP_GTIME
+                    if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][2] = gtimer();
+#endif
+                    __threadfence();
+                    fence_proxy_async_global();   // the actions, read by the env tiles' TMA
+                    named_bar_sync(1, 256);
+                    if (etid == 0) {
+                        mbar_arrive(headdone_b);
+                        mbar_arrive_remote(mapa_shared(headdone_b, peer));
+                    }
+                    mbar_wait_cluster(headdone_b, static_cast<uint32_t>(it) & 1u);
+#ifdef POD_EXP_GTIME
+                    if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][3] = gtimer();
+#endif
+                    const int grp = ew >> 2;
+                    const EnvArgs& ea = fe->env;
+                    EnvStep st;
+                    st.rew = ea.rew + so * a.N;
+                    st.done = ea.done + so * a.N;
+                    st.obs_out = ea.obs_out + so * a.N * fe->k_pad;
+                    st.dbg_hold = ea.dbg_hold ? ea.dbg_hold + so * Nn : nullptr;
+                    st.dbg_cash = ea.dbg_cash ? ea.dbg_cash + so * a.N : nullptr;
+                    st.equity = ea.equity ? ea.equity + so * a.N : nullptr;
+                    st.logp_out = ea.logp_out ? ea.logp_out + so * a.N : nullptr;
+                    st.gen_noise = (fe->sampling && it + 1 < fe->T) ? 1 : 0;
+                    st.noise_t = it + 1;
+                    env_step_tile<SELL_UNROLL, BUY_UNROLL>(*emaps, ea, st, (tl.env0 >> 5) + 2 * static_cast<int>(rank) + grp,
+                                                           etid & 127, base + grp * fe->env_stride, envbar_b + 64u * grp,
+                                                           static_cast<uint32_t>(it) & 1u, 3 + grp);
+#ifdef POD_EXP_GTIME
+                    if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][4] = gtimer();
+#endif
+                    // s_{t+1} and the holdings (TMA reads of the next step), the noise (the peer's loads), and
+                    // this tile's shared memory (the next obs tile lands there)
+                    __threadfence();
+                    fence_proxy_async_global();
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, 256);
+                    if (etid == 0) {
+                        mbar_arrive(envdone_b);
+                        mbar_arrive_remote(mapa_shared(envdone_b, peer));
+#ifdef POD_EXP_GTIME
+                        if (blockIdx.x == 0 && it < 1024) g_ftime[it][5] = gtimer();
+#endif
+                    }
+                } else {
+                    head();
+                }
+            } else {
+                head();
             }
         }
     }
@@ -622,8 +780,21 @@ __global__ void __launch_bounds__(ACT_THREADS, 1)
     }
     if (tr && threadIdx.x == 0) tr[26] = clock64();
 #ifdef POD_EXP_GTIME
-    if (threadIdx.x == 0 && a.t < 1024) atomicMax(&g_gtime[a.t][1], gtimer());
+    if (!FUSED && threadIdx.x == 0 && a.t < 1024) atomicMax(&g_gtime[a.t][1], gtimer());
 #endif
+}
+
+__global__ void __launch_bounds__(ACT_THREADS, 1)
+    actor_forward_kernel(const __grid_constant__ ActorMaps maps, const __grid_constant__ ActorArgs a) {
+    actor_body<false, 1, 1>(maps, a, nullptr, nullptr);
+}
+
+// the fused rollout: grid = 2 x M-tiles (one wave), cluster 2; see FusedEnvArgs
+template <int SELL_UNROLL, int BUY_UNROLL>
+__global__ void __launch_bounds__(ACT_THREADS, 1)
+    rollout_fused_kernel(const __grid_constant__ FusedMaps maps, const __grid_constant__ ActorArgs a,
+                         const __grid_constant__ FusedEnvArgs fe) {
+    actor_body<true, SELL_UNROLL, BUY_UNROLL>(maps.am, a, &maps.em, &fe);
 }
 
 }  // namespace pod

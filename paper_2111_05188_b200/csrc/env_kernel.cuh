@@ -119,17 +119,38 @@ __device__ __forceinline__ uint16_t f2bf(float x) {
 
 // SELL_UNROLL / BUY_UNROLL: unroll depths of the ledger's two ticker loops (16 / 8 for many tickers,
 // 8 / 4 for few: the deeper unroll is +1.5 % at n = 100 and -3 % at n = 30)
-template <int SELL_UNROLL, int BUY_UNROLL>
-__global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_constant__ EnvMaps maps, const EnvArgs a) {
-    extern __shared__ __align__(128) uint8_t env_smem[];
-    const int tid = threadIdx.x;
+// the per-step outputs of one env step (slices of the trajectory at step t)
+struct EnvStep {
+    float* rew;
+    uint8_t* done;
+    uint16_t* obs_out;
+    int32_t* dbg_hold;
+    double* dbg_cash;
+    double* equity;
+    float* logp_out;
+    int32_t gen_noise;
+    int32_t noise_t;
+};
+
+// One env tile (32 envs) on 128 threads (tid 0..127).  sync_id 0: the tile is a whole block (__syncthreads,
+// the block initialises its own mbarriers at `bar`); sync_id > 0: the tile is a 128-thread group of a larger
+// block (the fused rollout kernel) synchronised with named barrier sync_id, whose mbarriers at `bar` were
+// initialised once and complete once per step (wait parity `par`).
+// StepT: EnvStep, or EnvArgs itself (the standalone kernel reads its step slices straight from the parameters)
+template <int SELL_UNROLL, int BUY_UNROLL, typename StepT>
+__device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs a, const StepT st, const int tile,
+                                              const int tid, uint8_t* env_smem, const uint32_t bar_in, const uint32_t par,
+                                              const int sync_id) {
+    auto sync = [sync_id] {
+        if (sync_id == 0) __syncthreads();
+        else named_bar_sync(static_cast<uint32_t>(sync_id), ENV_THREADS);
+    };
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    const int tile = a.tile0 + static_cast<int>(blockIdx.x);
-    unsigned long long* trc = (a.trace && a.mode == 0) ? a.trace + tile * 8 : nullptr;
-    if (trc && threadIdx.x == 0) trc[0] = clock64();
+    unsigned long long* trc = (a.trace && a.mode == 0 && sync_id == 0) ? a.trace + tile * 8 : nullptr;
+    if (trc && tid == 0) trc[0] = clock64();
 #ifdef POD_EXP_GTIME
-    if (threadIdx.x == 0 && a.mode == 0 && a.noise_t - 1 < 1024) atomicMin(&g_gtime[a.noise_t - 1][2], gtimer());
+    if (sync_id == 0 && tid == 0 && a.mode == 0 && st.noise_t - 1 < 1024) atomicMin(&g_gtime[st.noise_t - 1][2], gtimer());
 #endif
     const int n = a.n;
     const int e_pad = env_e_pad(n);
@@ -146,7 +167,8 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     uint16_t* tmpl = reinterpret_cast<uint16_t*>(env_smem + SL.tmpl);
     uint16_t* stg = reinterpret_cast<uint16_t*>(env_smem + SL.stg);                           // [32][e_pad]
     double* ph_s = reinterpret_cast<double*>(env_smem + SL.ph);                               // [32]
-    const uint32_t bar = smem_u32(env_smem + SL.bar);
+    // (computed here, not by the caller: an early smem address kept live costs the ledger 8 registers)
+    const uint32_t bar = sync_id == 0 ? smem_u32(env_smem + SL.bar) : bar_in;
 
     const int e = tile * 32 + lane;                 // this lane's env (all four warps)
     const bool active = e < a.N;
@@ -158,7 +180,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
 
     // ---- 1. fetch the tile's holdings h_t[n][32] and actions a_t[n][32]: two 2-D TMA boxes
     const uint32_t chunk_bar = bar + 8u;   // [ENV_BUY_CHUNKS] buy chunk c released by warp 0 (32 arrivals)
-    if (tid == 0 && stepping) {
+    if (sync_id == 0 && tid == 0 && stepping) {
         for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(chunk_bar + 8u * c, 32);
         if (!tma) fence_mbar_init();
     }
@@ -167,8 +189,10 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
     // running; griddepcontrol.wait precedes the first read of the actor's outputs (the actions) and the
     // first write the actor could observe (the next step's noise).
     if (tma && tid == 0) {
-        mbar_init(bar, 1);
-        fence_mbar_init();
+        if (sync_id == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(n) * (stepping ? 192u : 128u));
         tma_load_2d(smem_u32(hold_s), &maps.hold, tile * 32, 0, bar);
         if (stepping && !a.pdl) tma_load_2d(smem_u32(aint_s), &maps.aint, tile * 32, 0, bar);
@@ -232,7 +256,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             else if (idx < total) tmpl[1 + 2 * n + (idx - 3 * n)] = f2bf(vals[q]);
         }
     }
-    __syncthreads();
+    sync();
     // ---- 3. per-tile constants: unit price p_t (1 + c), p/p0 at t_obs, zero pad
     const double opc = __dadd_rn(1.0, a.cost);
     for (int i = tid; i < n; i += ENV_THREADS) {
@@ -258,13 +282,20 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                 for (int i = warp; i < n; i += 4) aint_s[i * 32 + lane] = active ? a.aint[i * N + e] : 0;
         }
     }
-    if (tma) mbar_wait(bar, 0);
-    __syncthreads();
-    if (trc && threadIdx.x == 0) trc[1] = clock64();
-    if (warp == 1 && stepping && a.logp_parts && a.logp_out && active) {
+    if (tma) mbar_wait(bar, par);
+    sync();
+    if (trc && tid == 0) trc[1] = clock64();
+#ifdef POD_EXP_GTIME
+    if (sync_id == 3 && tid == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][6] = gtimer();
+#endif
+    if (warp == 1 && stepping && a.logp_parts && st.logp_out && active) {
         // the actor's four log-prob partials of this env, summed in the actor's own order
         const float* pp = a.logp_parts + e;
-        a.logp_out[e] = ((pp[0] + pp[N]) + pp[2 * N]) + pp[3 * N];
+        if (sync_id == 0) {
+            st.logp_out[e] = ((pp[0] + pp[N]) + pp[2 * N]) + pp[3 * N];
+        } else {   // L2 loads: the peer CTA of the fused rollout wrote half of them
+            st.logp_out[e] = ((__ldcg(pp) + __ldcg(pp + N)) + __ldcg(pp + 2 * N)) + __ldcg(pp + 3 * N);
+        }
     }
 
     // ---- 4. the float64 ledger, warp 0, lane = env, in exactly the order of
@@ -380,10 +411,10 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             if (trc && lane == 0) trc[3] = clock64();
         }
     } else {
-        if (a.gen_noise) {
+        if (st.gen_noise) {
             // the actor's Gaussian noise for the next actor launch (R#14: Philox4x32-10 keyed on
             // (global env, global step, ticker quad)), drawn while warp 0 runs the ledger
-            const uint64_t step = *a.step_base + static_cast<uint64_t>(a.noise_t);
+            const uint64_t step = *a.step_base + static_cast<uint64_t>(st.noise_t);
             const int nq = (n + 3) / 4;
             for (int idx = tid - 32; idx < 32 * nq; idx += ENV_THREADS - 32) {
                 const int el = idx & 31;
@@ -413,7 +444,7 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             }
             double ph = 0.0;
             for (int c = 0; c < nch; ++c) {
-                mbar_wait_parked(chunk_bar + 8u * c, 0u);
+                mbar_wait_parked(chunk_bar + 8u * c, par);
                 const int i0 = c * CH;
                 const int i1 = i0 + CH < n ? i0 + CH : n;
                 if (warp == 1) {
@@ -431,8 +462,8 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
                         if (active) *hrow = h * hkeep;
                         my[1 + i] = f2bf(static_cast<float>(h * hkeep) * p_1[i] * inv_c0);
                     }
-                    if (a.dbg_hold && active)
-                        for (int i = ib; i < i1; i += 2) a.dbg_hold[static_cast<int64_t>(e) * n + i] = hold_s[i * 32 + lane];
+                    if (st.dbg_hold && active)
+                        for (int i = ib; i < i1; i += 2) st.dbg_hold[static_cast<int64_t>(e) * n + i] = hold_s[i * 32 + lane];
                 }
             }
             if (warp == 1) ph_s[lane] = ph;
@@ -446,8 +477,11 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
         a.tile_k[tile] = 0;
         a.tile_gpow[tile] = 1.0;
     }
-    __syncthreads();
-    if (trc && threadIdx.x == 0) trc[4] = clock64();
+    sync();
+    if (trc && tid == 0) trc[4] = clock64();
+#ifdef POD_EXP_GTIME
+    if (sync_id == 3 && tid == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][7] = gtimer();
+#endif
     if (stepping) {
         // revalue at p_{t+1} (Eq. 2 reward), episode bookkeeping, and the cash entry of s_{t+1}
         if (warp == 0) {
@@ -456,10 +490,10 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             double disc = __dadd_rn(disc0, __dmul_rn(gpow, r));
             double v = v1;
             if (active) {
-                a.rew[e] = static_cast<float>(r);
-                a.done[e] = done ? 1 : 0;
-                if (a.dbg_cash) a.dbg_cash[e] = cash;
-                if (a.equity) a.equity[e] = v1;
+                st.rew[e] = static_cast<float>(r);
+                st.done[e] = done ? 1 : 0;
+                if (st.dbg_cash) st.dbg_cash[e] = cash;
+                if (st.equity) st.equity[e] = v1;
                 if (!isfinite(v1)) atomicOr(a.err, 2u);
                 if (done) a.ep_ret[e] = disc;
             }
@@ -490,15 +524,15 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             my[1 + i] = a.mode == 2 ? 0 : f2bf(static_cast<float>(h) * p_obs[i] * inv_c0);
         }
     }
-    __syncthreads();
-    if (trc && threadIdx.x == 0) trc[5] = clock64();
+    sync();
+    if (trc && tid == 0) trc[5] = clock64();
     // ---- 6. write s_{t+1}: env rows spread over the 4 warps, 16-B chunks (512 B per instruction)
-    if (a.obs_out) {
+    if (st.obs_out) {
         const int chunks = a.k_pad / 8;
         const int rows = min(32, a.N - tile * 32);
 #pragma unroll 4
         for (int row = warp; row < rows; row += 4) {
-            uint4* dst = reinterpret_cast<uint4*>(a.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
+            uint4* dst = reinterpret_cast<uint4*>(st.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
             for (int c = lane; c < chunks; c += 32) {
                 const uint4 val = c * 8 < e_pad ? *reinterpret_cast<const uint4*>(stg + row * e_pad + c * 8)
                                                 : *reinterpret_cast<const uint4*>(tmpl + c * 8);
@@ -506,11 +540,19 @@ __global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_cons
             }
         }
     }
-    __syncthreads();
-    if (trc && threadIdx.x == 0) trc[6] = clock64();
+    sync();
+    if (trc && tid == 0) trc[6] = clock64();
 #ifdef POD_EXP_GTIME
-    if (threadIdx.x == 0 && a.mode == 0 && a.noise_t - 1 < 1024) atomicMax(&g_gtime[a.noise_t - 1][3], gtimer());
+    if (sync_id == 0 && tid == 0 && a.mode == 0 && st.noise_t - 1 < 1024) atomicMax(&g_gtime[st.noise_t - 1][3], gtimer());
 #endif
+}
+
+template <int SELL_UNROLL, int BUY_UNROLL>
+__global__ void __launch_bounds__(ENV_THREADS) env_step_kernel(const __grid_constant__ EnvMaps maps,
+                                                                  const EnvArgs a) {
+    extern __shared__ __align__(128) uint8_t env_smem[];
+    env_step_tile<SELL_UNROLL, BUY_UNROLL>(maps, a, a, a.tile0 + static_cast<int>(blockIdx.x),
+                                           static_cast<int>(threadIdx.x), env_smem, 0u, 0u, 0);
 }
 
 // injected actions: a[i][e] = sgn(u) floor(|u| h_max + 1/2)  (R#6)

@@ -254,6 +254,7 @@ struct pod_env {
     bool use_graphs;
     int persist;                // persistent actor clusters (POD_PERSIST=0 turns it off)
     int pdl;                    // env step as a programmatic dependent of the actor (POD_PDL=0 turns it off)
+    int fused;                  // the fused rollout kernel where eligible (POD_FUSED=0 turns it off)
     int sm_count;
     int profile;                // 0 = off, k = bracket every k-th step
     unsigned long long* trace;  // diagnostics: actor clock64 stamps of the last launch
@@ -383,6 +384,8 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         e->persist = !(ps && ps[0] == '0');
         const char* pd = getenv("POD_PDL");
         e->pdl = (pd && pd[0] == '0') ? 0 : ((pd && pd[0] == '2') ? 2 : 1);   // 2: every env step (experiments)
+        const char* fu = getenv("POD_FUSED");
+        e->fused = !(fu && fu[0] == '0');
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -400,6 +403,10 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
     if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(actor_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(rollout_fused_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(rollout_fused_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (ce == cudaSuccess)
         ce = cudaFuncSetAttribute(env_step_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (ce == cudaSuccess)
@@ -559,10 +566,24 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
 // ------------------------------------------------------------ rollout
 struct RolloutPlan {
     bool injected;
+    bool fused;          // one rollout_fused_kernel launch for the T steps (see fused_eligible)
     ActorMaps maps;
     ActorArgs aa;
     size_t actor_smem;
 };
+
+// The fused rollout needs every M-tile's cluster resident at once (one wave: the clusters are independent
+// over the T steps, but a second wave would serialise T steps per tile), M-tiles aligned with the 32-env
+// tiles and with agents, and both env tiles of a CTA inside its activation buffer.
+static bool fused_eligible(const pod_env* e, const RolloutPlan& p) {
+    // (env_tma_ok: the env tiles read the actions through the tensor map, i.e. from L2 — plain loads could hit
+    // lines of the peer CTA's actions cached in this SM's L1 by an earlier step)
+    if (!e->fused || p.injected || e->groups != 1 || e->mc_ok || !e->env_tma_ok) return false;
+    if (e->per_agent % 128 != 0) return false;
+    const int mtiles = e->cfg.n_agents * (e->per_agent / 128);
+    if (2 * mtiles > e->sm_count) return false;
+    return fused_env_fits(e->cfg.n_stocks, e->k_pad, p.aa.hidden);
+}
 
 // one group's chain: s_0, then T x {actor (or injected map), env step}
 static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj, cudaStream_t s,
@@ -612,6 +633,54 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
     a0.gen_noise = sampling;          // noise for the actor launch of step 0
     a0.noise_t = 0;
     env_step_fn(e)<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
+    if (p.fused && !prof) {
+        // the T steps (and the critic bootstrap pass) in one launch: cluster c owns M-tile c for all steps
+        FusedMaps fm;
+        fm.am = p.maps;
+        fm.em = e->env_maps;
+        ActorArgs aa = p.aa;
+        aa.t = 0;
+        aa.obs_row0 = 0;
+        aa.mtile0 = 0;
+        aa.mc = 0;
+        aa.mtiles = e->cfg.n_agents * (e->per_agent / 128);
+        aa.act_out = tr->act;
+        aa.logp_out = tr->logp;
+        aa.logp_parts = e->logp_parts;
+        aa.mu_out = tr->mu;
+        aa.dbg_aint = tr->dbg_aint;
+        aa.val_out = tr->val;
+        FusedEnvArgs fe{};
+        fe.env = env_args(e, 0);
+        fe.env.rew = tr->rew;
+        fe.env.done = tr->done;
+        fe.env.obs_out = tr->obs + static_cast<int64_t>(N) * e->k_pad;
+        fe.env.dbg_hold = tr->dbg_hold;
+        fe.env.dbg_cash = tr->dbg_cash;
+        fe.env.equity = tr->equity;
+        fe.env.logp_parts = e->logp_parts;
+        fe.env.logp_out = tr->logp;
+        fe.env.trace = nullptr;
+        fe.T = T;
+        fe.sampling = sampling;
+        fe.env_stride = (env_smem_bytes(n, e->k_pad) + 127) / 128 * 128;
+        fe.k_pad = e->k_pad;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(static_cast<unsigned>(2 * aa.mtiles));
+        lc.blockDim = dim3(ACT_THREADS);
+        lc.dynamicSmemBytes = p.actor_smem;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        if (n >= 64) cudaLaunchKernelEx(&lc, rollout_fused_kernel<16, 8>, fm, aa, fe);
+        else cudaLaunchKernelEx(&lc, rollout_fused_kernel<8, 4>, fm, aa, fe);
+        return;
+    }
     for (int t = 0; t < T; ++t) {
         mark(t, 0);
         if (p.injected) {
@@ -823,6 +892,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         aa.trace = e->trace;
         p.actor_smem = actor_smem_bytes(L.k_pad, actor->hidden);
         if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
+        p.fused = fused_eligible(e, p);
     }
     if (!e->use_graphs) {
         ProfEvents* prof = nullptr;
@@ -1319,5 +1389,8 @@ extern "C" int pod_debug_gtime(unsigned long long* host, int reset) {
         return cudaMemcpyToSymbol(pod::g_gtime, init, sizeof(init)) == cudaSuccess ? 0 : 1;
     }
     return cudaMemcpyFromSymbol(host, pod::g_gtime, sizeof(unsigned long long) * 1024 * 4) == cudaSuccess ? 0 : 1;
+}
+extern "C" int pod_debug_ftime(unsigned long long* host) {
+    return cudaMemcpyFromSymbol(host, pod::g_ftime, sizeof(unsigned long long) * 1024 * 8) == cudaSuccess ? 0 : 1;
 }
 #endif

@@ -520,6 +520,40 @@ def test_pdl_env_launch_bit_identical(n, N, nh, hid, monkeypatch):
         assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
 
 
+@pytest.mark.parametrize("n,N,agents,nh,hid,det", [(30, 512, 1, 2, 128, False), (30, 4096, 1, 2, 128, True),
+                                                   (100, 8192, 1, 3, 512, False), (100, 8192, 8, 3, 512, False),
+                                                   (100, 2048, 2, 3, 512, True)])
+def test_fused_rollout_bit_identical(n, N, agents, nh, hid, det, monkeypatch):
+    """The fused rollout kernel (one cluster per 128-env M-tile runs the actor and the env step of its envs for
+    all T steps, rollout_fused_kernel; the default where it fits one wave) against the separate actor and
+    env-step launches (POD_FUSED=0): every trajectory output — observations, actions, log-probs, mean
+    actions, rewards, done flags, holdings, cash, equity, critic values including the bootstrap V(s_T) —
+    and the env state left for the next rollout are bit-identical, over two chained rollouts with
+    episode resets inside them (H = 5)."""
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("POD_FUSED", flag)
+        c = Case(n=n, f=3, T_data=600, N=N, H=5, n_agents=agents, seed=15)
+        aws, params, actor = _actor(c, nh, hid, n_agents=agents)
+        res = []
+        tr = api.Trajectory.allocate(7, N, n, c.k_pad, debug=True, critic=True, equity=True)
+        c.env.reset(c.starts)
+        for _ in range(2):
+            c.env.rollout(7, tr, actor=actor, deterministic=det)
+            torch.cuda.synchronize()
+            res.append({k: v.clone() for k, v in vars(tr).items() if v is not None})
+        res.append(dict(zip(("hold", "cash", "asset", "ep_ret"), c.env.read_state())))
+        c.env.check()
+        outs.append(res)
+    for a, b in zip(*outs):
+        assert a.keys() == b.keys()
+        for k in a:
+            x, y = a[k], b[k]
+            if x.dtype == torch.bfloat16:
+                x, y = x.view(torch.int16), y.view(torch.int16)
+            assert torch.equal(x, y), k
+
+
 @pytest.mark.parametrize("cost", [0.0, 0.25, 0.002])
 @pytest.mark.parametrize("kind", ["all_buy", "uniform", "buy_then_sell"])
 def test_exact_quotient_ties(kind, cost):
