@@ -56,6 +56,10 @@ const char* pod_status_string(pod_status s);
 /* Detail of the last failing call on this thread ("" if none). */
 const char* pod_last_error(void);
 int pod_abi_version(void);
+/* Measurement support: the number of kernels this library has launched in this
+ * process (every entry point; a launch of a cached CUDA graph counts the graph's
+ * kernel nodes), e.g. sampled around a timed region. */
+unsigned long long pod_kernel_launches(void);
 
 typedef struct pod_env pod_env_t;    /* opaque */
 typedef struct pod_comm pod_comm_t;  /* opaque */
@@ -212,13 +216,21 @@ pod_status pod_env_reset(pod_env_t* env, const int64_t* tile_start_rows, uint16_
  * across calls; obs[T] is the bootstrap state.  fitness_out [dev] f64
  * [n_agents] or NULL: afterwards J_a = mean over agent a's envs of the
  * discounted return of each env's last completed episode (Eq. 1, R#15).
+ * Execution (results identical either way): when every 128-env M-tile's CTA
+ * pair fits on the device at once (2 x M-tiles <= SMs), agents hold whole
+ * M-tiles (N / n_agents % 128 == 0), one env group, no injected actions and
+ * no profiling, the T steps run as ONE launch in which each CTA pair runs the
+ * actor and the env step of its 128 envs for all steps (the rollout_fused
+ * kernel; POD_FUSED=0 in the environment at pod_env_create turns it off);
+ * otherwise as 2T launches (actor, env step).
  * Errors (host, synchronous): ARG, SHAPE, UNSUPPORTED, CUDA. */
 pod_status pod_rollout(pod_env_t* env, const pod_actor* actor, int32_t T, const pod_traj* traj,
                        const float* injected_u, int32_t deterministic, double* fitness_out,
                        void* stream);
 
 /* Per-kernel device timing (measurement support, not part of the method).
- * stride k > 0: subsequent pod_rollout calls record CUDA events around the
+ * stride k > 0: subsequent pod_rollout calls run the separate actor / env-step
+ * launches (not the fused rollout kernel) and record CUDA events around the
  * actor launches and the env-step launches of every k-th step, on the stream
  * (graph branch) each launch runs on; 0 turns it off.  pod_env_profile_read
  * synchronises `stream` and returns, for the most recent profiled rollout, the

@@ -58,7 +58,7 @@ class Transfer(C.Structure):
     _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("src_local", C.c_int32), ("dst_local", C.c_int32)]
 
 
-EXPORTS = ["pod_status_string", "pod_last_error", "pod_abi_version", "pod_actor_layout_get",
+EXPORTS = ["pod_status_string", "pod_last_error", "pod_abi_version", "pod_kernel_launches", "pod_actor_layout_get",
            "pod_env_workspace_size", "pod_env_create", "pod_env_destroy", "pod_env_reset", "pod_rollout",
            "pod_env_profile", "pod_env_profile_read", "pod_debug_trace", "pod_env_fitness", "pod_env_read_state", "pod_env_check", "pod_gae", "pod_elite_plan", "pod_fuse_pods", "pod_fuse_workspace_size", "pod_fuse_pods_local_ranks", "pod_backtest_metrics", "pod_early_stop", "pod_ppo_workspace_size", "pod_ppo_update", "pod_ppo_check",
            "pod_elite_transfers", "pod_comm_unique_id", "pod_comm_init", "pod_comm_destroy", "pod_select_elite"]
@@ -81,6 +81,7 @@ def load():
         "pod_status_string": ([C.c_int], C.c_char_p),
         "pod_last_error": ([], C.c_char_p),
         "pod_abi_version": ([], C.c_int),
+        "pod_kernel_launches": ([], C.c_ulonglong),
         "pod_actor_layout_get": ([P(EnvConfig), i32, i32, P(ActorLayout)], C.c_int),
         "pod_env_workspace_size": ([P(EnvConfig), P(sz)], C.c_int),
         "pod_env_create": ([P(EnvConfig), P(Market), vp, sz, P(vp)], C.c_int),

@@ -28,6 +28,11 @@ def _stream(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
+def kernel_launches() -> int:
+    """Kernels libpod has launched in this process (cached graphs count their kernel nodes)."""
+    return int(load().pod_kernel_launches())
+
+
 def make_config(n_envs, n_stocks, n_feat, horizon, n_agents=1, h_max=100, env_offset=0, initial_capital=1e6,
                 cost_rate=0.002, reward_scale=1.0, gamma=0.99, seed=0) -> _lib.EnvConfig:
     return _lib.EnvConfig(n_envs, n_stocks, n_feat, n_agents, horizon, h_max, env_offset, initial_capital, cost_rate,

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -219,11 +220,35 @@ struct ProfEvents {
     }
 };
 
+static std::atomic<unsigned long long> g_kernel_launches{0};
+void pod_note_launch(cudaStream_t s, unsigned long long n) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) cs = cudaStreamCaptureStatusNone;
+    if (cs == cudaStreamCaptureStatusNone) g_kernel_launches.fetch_add(n, std::memory_order_relaxed);
+}
+unsigned long long pod_graph_kernel_nodes(cudaGraph_t g) {
+    size_t n = 0;
+    if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess || n == 0) return 0;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+    unsigned long long k = 0;
+    for (size_t i = 0; i < n; ++i) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
+void pod_note_graph_launch(unsigned long long kernel_nodes) {
+    g_kernel_launches.fetch_add(kernel_nodes, std::memory_order_relaxed);
+}
+extern "C" unsigned long long pod_kernel_launches(void) { return g_kernel_launches.load(std::memory_order_relaxed); }
+
 struct GraphEntry {
     GraphKey key;
     cudaGraphExec_t exec;
     uint64_t last_use;
     ProfEvents* prof;
+    unsigned long long kernels;   // kernel nodes of the graph
 };
 
 struct pod_env {
@@ -424,6 +449,7 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         const int64_t nf = static_cast<int64_t>(market->T_data) * cfg->n_feat * cfg->n_stocks;
         uint32_t flags = 0;
         market_check_kernel<<<296, 256>>>(market->close, nc, market->feat, nf, e->err);
+        pod_note_launch(nullptr);
         ce = cudaGetLastError();
         if (ce == cudaSuccess) ce = cudaMemcpy(&flags, e->err, 4, cudaMemcpyDeviceToHost);
         if (ce == cudaSuccess) ce = cudaMemset(e->err, 0, 4);
@@ -557,6 +583,7 @@ extern "C" pod_status pod_env_reset(pod_env_t* e, const int64_t* starts, uint16_
     EnvArgs a = env_args(e, 2);
     a.obs_out = obs0;
     env_step_fn(e)<<<env_blocks(e), ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+    pod_note_launch(s);
     POD_CUDA(cudaGetLastError());
     POD_CUDA(cudaStreamSynchronize(s));   // the pinned staging buffer is reused by the next reset
     *static_cast<volatile uint32_t*>(e->h_err) = 0;
@@ -626,6 +653,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         lc.attrs = at;
         lc.numAttrs = 1;
         cudaLaunchKernelEx(&lc, actor_forward_kernel, p.maps, aa);
+        pod_note_launch(s);
     };
     EnvArgs a0 = env_args(e, 1);
     a0.tile0 = t0;
@@ -633,6 +661,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
     a0.gen_noise = sampling;          // noise for the actor launch of step 0
     a0.noise_t = 0;
     env_step_fn(e)<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a0);
+    pod_note_launch(s);
     if (p.fused && !prof) {
         // the T steps (and the critic bootstrap pass) in one launch: cluster c owns M-tile c for all steps
         FusedMaps fm;
@@ -679,6 +708,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         lc.numAttrs = 1;
         if (n >= 64) cudaLaunchKernelEx(&lc, rollout_fused_kernel<16, 8>, fm, aa, fe);
         else cudaLaunchKernelEx(&lc, rollout_fused_kernel<8, 4>, fm, aa, fe);
+        pod_note_launch(s);
         return;
     }
     for (int t = 0; t < T; ++t) {
@@ -688,6 +718,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             inject_map_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(
                 inj + static_cast<int64_t>(t) * N * n, N, n, e->cfg.h_max, e->aint,
                 tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr, e0, e1);
+            pod_note_launch(s);
         } else {
             ActorArgs aa = p.aa;
             aa.t = t;
@@ -740,8 +771,10 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             lc.attrs = at;
             lc.numAttrs = 1;
             cudaLaunchKernelEx(&lc, env_step_fn(e), e->env_maps, a);
+            pod_note_launch(s);
         } else {
             env_step_fn(e)<<<t1 - t0, ENV_THREADS, env_smem(e), s>>>(e->env_maps, a);
+            pod_note_launch(s);
         }
         mark(t, 3);
     }
@@ -777,7 +810,9 @@ static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const
         }
     }
     if (!p.injected) bump_step_kernel<<<1, 1, 0, s>>>(e->step, static_cast<uint64_t>(T));
+    if (!p.injected) pod_note_launch(s);
     if (fitness_out) fitness_kernel<<<e->cfg.n_agents, 1024, 0, s>>>(e->ep_ret, e->per_agent, fitness_out);
+    if (fitness_out) pod_note_launch(s);
     POD_CUDA(cudaGetLastError());
     // publish the device error word to the pinned host mirror: the next pod_rollout refuses to run on a
     // state that an earlier rollout has already flagged (non-finite mean action or account value)
@@ -943,6 +978,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
         cudaGraphExec_t exec;
         ce = cudaGraphInstantiate(&exec, graph, 0);
+        const unsigned long long kn = pod_graph_kernel_nodes(graph);
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
         if (e->graphs.size() >= 8) {
@@ -956,12 +992,13 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
             }
             e->graphs.erase(e->graphs.begin() + static_cast<long>(victim));
         }
-        e->graphs.push_back(GraphEntry{key, exec, 0, prof});
+        e->graphs.push_back(GraphEntry{key, exec, 0, prof, kn});
         hit = &e->graphs.back();
     }
     hit->last_use = ++e->use_clock;
     e->last_prof = hit->prof;
     POD_CUDA(cudaGraphLaunch(hit->exec, s));
+    pod_note_graph_launch(hit->kernels);
     return POD_OK;
 }
 
@@ -1013,6 +1050,7 @@ extern "C" pod_status pod_env_profile_read(pod_env_t* e, double* actor_ms, doubl
 extern "C" pod_status pod_env_fitness(pod_env_t* e, double* fitness_out, void* stream) {
     if (!e || !fitness_out) return pod_fail(POD_ERR_ARG, "env and fitness_out must be non-NULL");
     fitness_kernel<<<e->cfg.n_agents, 1024, 0, static_cast<cudaStream_t>(stream)>>>(e->ep_ret, e->per_agent, fitness_out);
+    pod_note_launch(static_cast<cudaStream_t>(stream));
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }
@@ -1039,6 +1077,7 @@ extern "C" pod_status pod_env_read_state(pod_env_t* e, int32_t* hold, double* ca
     if (hold) {
         const int64_t tot = static_cast<int64_t>(N) * n;
         hold_transpose_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(e->hold, N, n, hold);
+        pod_note_launch(s);
         POD_CUDA(cudaGetLastError());
     }
     if (cash) POD_CUDA(cudaMemcpyAsync(cash, e->cash, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
@@ -1065,6 +1104,7 @@ extern "C" pod_status pod_gae(const float* rew, const float* val, const uint8_t*
     const int64_t want = (count / 4 + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
     adv_normalize_kernel<<<blocks, 256, 0, s>>>(adv, count, adv_stats, reinterpret_cast<uintptr_t>(adv) % 16 == 0);
+    pod_note_launch(s);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }
@@ -1179,6 +1219,7 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
                 lc.numAttrs = 1;
                 POD_CUDA(cudaLaunchKernelEx(&lc, gae_seg_kernel<true>, maps, boot, T, N, gamma, lambda, adv, ret, cpw,
                                             stats));
+                pod_note_launch(stream);
                 *normalized = true;
                 return POD_OK;
             }
@@ -1186,6 +1227,7 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
         }
         gae_seg_kernel<false><<<static_cast<unsigned>(groups), 32 * seg, gae_seg_smem_bytes(seg, cpw), stream>>>(
             maps, boot, T, N, gamma, lambda, adv, ret, cpw, stats);
+        pod_note_launch(stream);
         POD_CUDA(cudaGetLastError());
         return POD_OK;
     }
@@ -1207,6 +1249,7 @@ static pod_status gae_launch(const float* rew, const float* val, const uint8_t* 
     }
     gae_kernel<<<blocks, 32 * GAE_WARPS, gae_smem_bytes(), stream>>>(maps, rew, val, done, boot, T, N, gamma, lambda,
                                                                        adv, ret, use_bulk, stats);
+    pod_note_launch(stream);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }
@@ -1292,6 +1335,7 @@ extern "C" pod_status pod_fuse_pods(pod_comm_t* comm, const pod_env_config* cfg,
     const int64_t chunks = static_cast<int64_t>(a.A_local) * a.nchunks;
     const unsigned X = static_cast<unsigned>(std::min<int64_t>(chunks, fuse_x_capacity()));
     fuse_x_kernel<<<dim3(X, 1), 256, 0, s>>>(a);
+    pod_note_launch(s);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }
@@ -1348,6 +1392,7 @@ extern "C" pod_status pod_fuse_pods_local_ranks(const pod_env_config* cfg, int32
     const int64_t chunks = static_cast<int64_t>(A) * a.nchunks;
     const unsigned X = static_cast<unsigned>(std::min<int64_t>(chunks, cap / R));
     fuse_x_kernel<<<dim3(X, static_cast<unsigned>(R)), 256, 0, s>>>(a);
+    pod_note_launch(s);
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }
@@ -1362,6 +1407,7 @@ extern "C" pod_status pod_backtest_metrics(const double* v0, const double* curve
     if (st) return st;
     backtest_metrics_kernel<<<static_cast<unsigned>((N + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
         v0, curve, T, N, periods_per_year, rf_per_period, out);
+    pod_note_launch(static_cast<cudaStream_t>(stream));
     POD_CUDA(cudaGetLastError());
     return POD_OK;
 }

@@ -77,6 +77,7 @@ struct PpoGraph {
     PpoGraphKey key;
     cudaGraphExec_t exec;
     uint64_t used;
+    unsigned long long kernels;   // kernel nodes of the graph
 };
 inline std::vector<PpoGraph>& ppo_graphs() {
     static thread_local std::vector<PpoGraph> g;
@@ -152,6 +153,7 @@ pod_status launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream
     lc.dynamicSmemBytes = smem;
     lc.stream = s;
     POD_CUDA(cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...));
+    pod_note_launch(s);
     return POD_OK;
 }
 
@@ -382,6 +384,7 @@ pod_status ppo_enqueue(const PpoPlan& p, cudaStream_t s, cudaStream_t s2) {
     // (the last minibatch's join above leaves nothing on the side branch: the capture is closed on s)
     if (p.n_mb == 0) {
         fuse_blend_kernel<<<ngrid, 256, 0, s>>>(*p.fa);
+        pod_note_launch(s);
         POD_CUDA(cudaGetLastError());
     }
     return POD_OK;
@@ -532,6 +535,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
     };
     ppo_set_step_kernel<<<1, 1, 0, user_s>>>(hpd, adam_t, hp->ratio_clip, hp->entropy_coef, hp->value_coef,
                                              hp->learning_rate, hp->adam_beta1, hp->adam_beta2, hp->adam_eps);
+    pod_note_launch(user_s);
     POD_CUDA(cudaGetLastError());
     static const bool use_graph = [] {
         const char* e = std::getenv("POD_PPO_GRAPH");
@@ -578,6 +582,7 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
             if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "PPO graph capture: %s", cudaGetErrorString(ce));
             cudaGraphExec_t exec;
             ce = cudaGraphInstantiate(&exec, graph, 0);
+            const unsigned long long kn = pod_graph_kernel_nodes(graph);
             cudaGraphDestroy(graph);
             if (ce != cudaSuccess) return pod_fail(POD_ERR_CUDA, "PPO graph instantiate: %s", cudaGetErrorString(ce));
             if (cache.size() >= kPpoGraphCache) {   // evict the least recently used
@@ -587,11 +592,12 @@ extern "C" pod_status pod_ppo_update(const pod_env_config* cfg, int32_t n_hidden
                 cudaGraphExecDestroy(cache[victim].exec);
                 cache.erase(cache.begin() + static_cast<long>(victim));
             }
-            cache.push_back(PpoGraph{key, exec, 0});
+            cache.push_back(PpoGraph{key, exec, 0, kn});
             hit = &cache.back();
         }
         hit->used = ++ppo_clock;
         POD_CUDA(cudaGraphLaunch(hit->exec, user_s));
+        pod_note_graph_launch(hit->kernels);
     }
     // publish the error word to the host mirror of this workspace (read by the next call / pod_ppo_check)
     POD_CUDA(cudaMemcpyAsync(herr, &hpd->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, user_s));

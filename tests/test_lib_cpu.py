@@ -24,12 +24,13 @@ def _built():
 
 def test_exports_match_header():
     hdr = open(os.path.join(ROOT, "include", "pod.h")).read()
-    declared = set(re.findall(r"^\s*(?:pod_status|const char\*|int)\s+(pod_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:pod_status|const char\*|int|unsigned long long)\s+(pod_\w+)\s*\(", hdr, re.M))
     assert declared == set(_lib.EXPORTS)
     L = _lib.load()
     for name in declared:
         assert hasattr(L, name), name
     assert L.pod_abi_version() == 3
+    assert isinstance(L.pod_kernel_launches(), int)
     assert L.pod_status_string(3) == b"POD_ERR_RANGE"
 
 
