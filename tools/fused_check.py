@@ -51,10 +51,15 @@ def run(w, fused: bool, T: int, horizon: int, deterministic: bool, reps: int = 0
 
 
 def main():
-    names = sys.argv[1:] or ["C2", "C3", "C4"]
+    time_only = "--time-only" in sys.argv
+    names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C2", "C3", "C4"]
     bad = 0
     for name in names:
         w = configs.preset(name, T_data=20000)
+        if time_only:
+            _, _, mf = run(w, True, w.T, w.horizon, False, reps=20)
+            print(f"{name} T={w.T}: fused {mf:.3f} ms/rollout ({mf * 1e3 / w.T:.2f} us/step)", flush=True)
+            continue
         for horizon, det in ((w.horizon, False), (40, False), (40, True)):
             T = 64
             t0 = time.time()
