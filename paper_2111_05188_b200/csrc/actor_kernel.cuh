@@ -630,42 +630,27 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                         mu[jj] = __uint_as_float(hv[jj]) + bias[tc + jj];
                         raw[jj] = mu[jj];
                     }
-                    // one ticker: noise z ~ N(0,1) for (env, step, ticker) generated by the previous env-step
-                    // launch, raw = mu + sigma z, log-prob term, tanh on the SFU, integer map in float64
-                    auto sample = [&](int jj) {
+                    // per ticker: noise z ~ N(0,1) for (env, step, ticker) generated by the previous env step,
+                    // raw = mu + sigma z, log-prob term, tanh on the SFU, integer map in float64.  One straight-line
+                    // body for all 8 columns of the chunk, the tickers past n masked (their stores and log-prob
+                    // terms predicated off): half the code of a separate guarded copy for the last chunk
+    #pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const bool ok = i0 + jj < a.n;
                         const float z = zr[cc * 8 + jj];
                         const float ls = log_std[tc + jj];
-                        bad |= !isfinite(mu[jj]);
+                        bad |= ok && !isfinite(mu[jj]);
                         raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
-                        logp += (-0.5f * z * z - ls) - half_ln_2pi;
-#if defined(POD_EXP_HEAD) && POD_EXP_HEAD == 3
-                        ai8[jj] = static_cast<int16_t>(raw[jj]);
-#else
+                        if (ok) logp += (-0.5f * z * z - ls) - half_ln_2pi;
                         const float u = tanh_sfu(raw[jj]);
                         const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
                         ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
-#endif
-#if !defined(POD_EXP_HEAD) || POD_EXP_HEAD != 2
-                        a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
-#endif
-                    };
-                    // chunk-uniform branch: straight-line code for the full 8-ticker chunks
-                    if (i0 + 8 <= a.n) {
-    #pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) sample(jj);
-                    } else {
-    #pragma unroll
-                        for (int jj = 0; jj < 8; ++jj)
-                            if (i0 + jj < a.n) sample(jj);
+                        if (ok) a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
                     }
                     if (dbg_aint) {
                         for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
                             dbg_aint[static_cast<int64_t>(e) * a.n + i0 + jj] = ai8[jj];
                     }
-#if defined(POD_EXP_HEAD) && POD_EXP_HEAD == 1
-                    if (raw[0] == 12345.0f)
-#endif
-                    {
                     float* arow = act_out + static_cast<int64_t>(e) * a.n + i0;
                     float* mrow = mu_out ? mu_out + static_cast<int64_t>(e) * a.n + i0 : nullptr;
                     if (vec && i0 + 8 <= a.n) {
@@ -683,7 +668,6 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                                 if (mrow) mrow[jj] = mu[jj];
                             }
                         }
-                    }
                     }
                 }
             }
