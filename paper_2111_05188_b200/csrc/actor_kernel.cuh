@@ -30,8 +30,7 @@
 //     half is still in flight (per-rank K order: own half first);
 //   * head: each CTA samples its half of the tickers with noise z that the
 //     previous env-step launch generated in its otherwise idle warps; the per-row
-//     log-prob partials go to a [4][N] scratch that the next env step sums in a fixed order (the
-//     DSMEM combine in CTA 0 remains for callers without the scratch).
+//     log-prob partials go to a [4][N] scratch that the next env step sums in a fixed order.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -87,7 +86,7 @@ struct ActorArgs {
     float* val_out;      // [N] critic V(s_t) = head row n (R#22), or null
     uint32_t* err;
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
-    float* logp_parts;           // [4][N] log-prob partials (rank, half) for the env step to combine, or null
+    float* logp_parts;           // [4][N] log-prob partials (rank, half) for the env step to combine (required)
     uint32_t kpb_pack;           // K blocks per ring stage of layer l in bits [5l, 5l+5) (0/1: one 3-D box)
 };
 
@@ -122,7 +121,7 @@ constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
     return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_STAGE_BYTES +
-           ACT_BIAS_FLOATS * 4 + 2 * 4 * 128 * 4 + 512;   // + double-buffered log-prob partials + barriers
+           ACT_BIAS_FLOATS * 4 + 512;   // + barriers
 }
 
 // The fused rollout (rollout_fused_kernel): one cluster per 128-env M-tile runs the actor AND the env step
@@ -206,8 +205,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t stage_bytes = ACT_STAGE_BYTES;
     const uint32_t bias_off = ka * 16384u + ACT_STAGES * stage_bytes;
     float* bias_s = reinterpret_cast<float*>(base + bias_off);                 // [ACT_BIAS_FLOATS]
-    float* logp_s0 = bias_s + ACT_BIAS_FLOATS;                                 // [2 tiles][4][128] (CTA 0)
-    const uint32_t bar_s = base_u32 + bias_off + ACT_BIAS_FLOATS * 4 + 2 * 4 * 128 * 4;
+    const uint32_t bar_s = base_u32 + bias_off + ACT_BIAS_FLOATS * 4;
     const uint32_t full_b = bar_s;                                   // [STAGES]
     const uint32_t empty_b = bar_s + 8u * ACT_STAGES;                // [STAGES]
     const uint32_t obs_b = bar_s + 16u * ACT_STAGES;
@@ -215,8 +213,6 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t ownrdy_b = obs_b + 16u;     // [4] atom j of this CTA's half of h_{l+1} written (256 arrivals)
     const uint32_t peerrdy_b = obs_b + 48u;    // [4] atom j of the peer's half landed (expect_tx)
     const uint32_t actfree_b = obs_b + 80u;    // this CTA's MMAs of a tile are done reading act_s (commit)
-    const uint32_t logp_b = obs_b + 88u;       // CTA 0: a tile's 4 x 128 log-prob partials written (512 arrivals)
-    const uint32_t logpfree_b = obs_b + 96u;   // [2] CTA 1: CTA 0 has read partial buffer p (1 remote arrival)
     const uint32_t tslot_s = obs_b + 112u;
     const uint32_t accl_b = obs_b + 120u;      // this CTA's MMAs of a layer are complete (local commit)
     // FUSED: both CTAs' heads of step t are written (2 arrivals: this CTA's and the peer's), both CTAs' env
@@ -265,9 +261,6 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             mbar_init(accum_b, 2);        // one multicast commit from each CTA of the pair
             mbar_init(accl_b, 1);
             mbar_init(actfree_b, 1);
-            mbar_init(logp_b, 512);
-            mbar_init(logpfree_b, 1);
-            mbar_init(logpfree_b + 8u, 1);
             for (int j = 0; j < 4; ++j) {
                 mbar_init(ownrdy_b + 8u * j, 256);   // the 256 epilogue threads
                 mbar_init(peerrdy_b + 8u * j, 1);    // the MMA thread's expect_tx + the peer's bytes
@@ -673,27 +666,9 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             }
             if (bad && valid) atomicOr(a.err, 1u);
             if (tr && it == 0 && etid == 0) tr[25] = clock64();
-            // log-prob partial of (rank, hh) for row r -> CTA 0's buffer (it & 1) [rank*2 + hh][r]; CTA 1 first
-            // makes sure CTA 0 has consumed the tile that last used this buffer (two tiles ago)
-            if (a.logp_parts) {
-                // the env step that follows combines the four partials ((p0 + p1) + p2) + p3: no
-                // cross-CTA exchange in this kernel's tail
-                if (valid && logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
-            } else {
-                const uint32_t pb = static_cast<uint32_t>(it) & 1u;
-                float* logp_s = logp_s0 + pb * 512;
-                if (rank == 1 && it >= 2)
-                    mbar_wait_cluster(logpfree_b + 8u * pb, static_cast<uint32_t>((it - 2) >> 1) & 1u);
-                st_cluster_f32(mapa_shared(smem_u32(logp_s + (rank * 2 + hh) * 128 + r), cr & ~1u), logp);
-                mbar_arrive_remote(mapa_shared(logp_b, cr & ~1u));   // release: the partial is visible with the arrival
-                if (rank == 0) {
-                    mbar_wait_cluster(logp_b, static_cast<uint32_t>(it) & 1u);
-                    if (hh == 0 && valid && logp_out)
-                        logp_out[e] = ((logp_s[r] + logp_s[128 + r]) + logp_s[256 + r]) + logp_s[384 + r];
-                    named_bar_sync(2, 256);
-                    if (etid == 0) mbar_arrive_remote(mapa_shared(logpfree_b + 8u * pb, peer));
-                }
-            }
+            // log-prob partial of (rank, hh) for row r -> the [4][N] scratch; the env step that follows combines
+            // the four partials ((p0 + p1) + p2) + p3, so the kernel's tail needs no cross-CTA exchange
+            if (valid && logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
             };
             if constexpr (FUSED) {
                 if (!vo) {

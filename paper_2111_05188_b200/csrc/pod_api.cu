@@ -726,7 +726,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
             aa.mtile0 = m0;
             aa.act_out = tr->act + static_cast<int64_t>(t) * N * n;
             aa.logp_out = tr->logp + static_cast<int64_t>(t) * N;
-            aa.logp_parts = tr->logp ? e->logp_parts : nullptr;
+            aa.logp_parts = e->logp_parts;
             aa.mu_out = tr->mu ? tr->mu + static_cast<int64_t>(t) * N * n : nullptr;
             aa.dbg_aint = tr->dbg_aint ? tr->dbg_aint + static_cast<int64_t>(t) * N * n : nullptr;
             aa.val_out = tr->val ? tr->val + static_cast<int64_t>(t) * N : nullptr;
@@ -791,6 +791,7 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         aa.mu_out = nullptr;
         aa.dbg_aint = nullptr;
         aa.val_out = tr->val + static_cast<int64_t>(T) * N;
+        aa.logp_parts = e->logp_parts;   // written only with logp_out: untouched here
         launch_actor(aa);
     }
 }
