@@ -134,6 +134,8 @@ struct FusedEnvArgs {
     int32_t sampling;   // the env step of step t draws the actor noise of step t+1 (t + 1 < T)
     int32_t env_stride; // bytes between the two env tiles' shared-memory areas inside the activation buffer
     int32_t k_pad;
+    int32_t persist;    // bytes of each env tile's persistent state (env_persist_bytes; 0: none, n % 4 != 0) after
+                        // the barrier region (the launch adds 2 x persist to the actor's shared memory)
 };
 struct FusedMaps {
     ActorMaps am;
@@ -220,6 +222,8 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t headdone_b = obs_b + 128u;
     const uint32_t envdone_b = obs_b + 136u;
     const uint32_t envbar_b = obs_b + 144u;    // [2 tiles][1 + ENV_BUY_CHUNKS]
+    const uint32_t envmkt_b = obs_b + 272u;    // [2 tiles] the next step's market rows landed (bulk copies)
+    uint8_t* const env_pst = base + bias_off + ACT_BIAS_FLOATS * 4 + 512;   // [2 tiles][persist] (FUSED)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
     // persistent over M-tiles: cluster c (one CTA pair per M-tile) takes tiles mtile0 + c + it * nclusters
@@ -268,6 +272,8 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             if (FUSED) {
                 mbar_init(headdone_b, 2);
                 mbar_init(envdone_b, 2);
+                mbar_init(envmkt_b, 1);
+                mbar_init(envmkt_b + 8u, 1);
                 for (int g = 0; g < 2; ++g) {
                     mbar_init(envbar_b + 64u * g, 1);   // the env tile's TMA barrier
                     for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(envbar_b + 64u * g + 8u * (c + 1), 32);
@@ -495,6 +501,31 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
         const int hq = head_half / 2;              // head tickers of this thread
         int staged_agent = -1;
         Tile tl;
+        if constexpr (FUSED) {
+            if (fe->persist && fe->T > 0 && tile_of(0, tl)) {
+                // this CTA's two env tiles: their state from HBM into the persistent shared-memory copies, and the
+                // first step's market rows
+                const int grp = ew >> 2, gtid = etid & 127;
+                const int etile = (tl.env0 >> 5) + 2 * static_cast<int>(rank) + grp;
+                uint8_t* pst = env_pst + grp * fe->persist;
+                const EnvArgs& ea = fe->env;
+                if (gtid < 32) {
+                    double* pl = reinterpret_cast<double*>(pst + ENVP_LEDGER);
+                    const int64_t ee = static_cast<int64_t>(etile) * 32 + gtid;
+                    pl[gtid] = ea.cash[ee];
+                    pl[32 + gtid] = ea.asset[ee];
+                    pl[64 + gtid] = ea.disc[ee];
+                }
+                if (gtid == 0) {
+                    const int64_t s0 = ea.tile_start[etile];
+                    const int k0 = ea.tile_k[etile];
+                    *reinterpret_cast<int64_t*>(pst + ENVP_HDR) = s0;
+                    *reinterpret_cast<int32_t*>(pst + ENVP_HDR + 8) = k0;
+                    *reinterpret_cast<double*>(pst + ENVP_HDR + 16) = ea.tile_gpow[etile];
+                    env_mkt_issue(ea, pst, s0, k0, envmkt_b + 8u * grp);
+                }
+            }
+        }
         for (int it = 0; tile_of(it, tl); ++it) {
             const int e = tl.env0 + r;
             const bool valid = r < tl.rows_valid && e < a.N;
@@ -705,7 +736,9 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     st.noise_t = it + 1;
                     env_step_tile<SELL_UNROLL, BUY_UNROLL>(*emaps, ea, st, (tl.env0 >> 5) + 2 * static_cast<int>(rank) + grp,
                                                            etid & 127, base + grp * fe->env_stride, envbar_b + 64u * grp,
-                                                           static_cast<uint32_t>(it) & 1u, 3 + grp);
+                                                           static_cast<uint32_t>(it) & 1u, 3 + grp,
+                                                           fe->persist ? env_pst + grp * fe->persist : nullptr,
+                                                           envmkt_b + 8u * grp, it + 1 < fe->T);
 #ifdef POD_EXP_GTIME
                     if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][4] = gtimer();
 #endif

@@ -132,15 +132,67 @@ struct EnvStep {
     int32_t noise_t;
 };
 
+// Fused rollout: an env tile's state kept in the CTA's shared memory across the T steps (outside the activation
+// buffer the per-step tile area lives in): the tile header, its 32 envs' ledger state, and the next step's market
+// rows, which TMA bulk copies bring in during the actor phase.  Byte offsets; `mkt` holds three 16-byte aligned
+// windows, [p_t | p_{t+1}], [p_0], [feat[t_obs]] ((3 + f) n floats), each starting up to 3 floats before its row
+// (bulk copies move whole 16-byte units); the header records where each row starts.
+constexpr int ENVP_HDR = 0;       // int64 s, int32 k, pad, double gpow, uint16 row offsets (floats) of p_t, p_0, feat
+constexpr int ENVP_LEDGER = 32;   // double cash[32], asset[32], disc[32]
+constexpr int ENVP_MKT = 800;
+__host__ __device__ inline int env_persist_bytes(int n, int f) {
+    return (ENVP_MKT + (3 + f) * n * 4 + 3 * 16 + 127) / 128 * 128;
+}
+// one row range [src, src + bytes) as a whole-16-byte window at smem dst; returns the window's bytes, and the
+// row's offset inside it in floats
+__device__ __forceinline__ uint32_t env_mkt_window(uint32_t dst, const float* src, uint32_t bytes, uint32_t bar,
+                                                   uint16_t* off) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t p0 = p & ~static_cast<uintptr_t>(15);
+    const uint32_t w = static_cast<uint32_t>((p + bytes - p0 + 15) & ~static_cast<uintptr_t>(15));
+    bulk_g2s(dst, reinterpret_cast<const void*>(p0), w, bar);
+    *off = static_cast<uint16_t>((p - p0) >> 2);
+    return w;
+}
+// the market rows of the step with episode start s and step k: bulk copies onto `bar`, which this arms (the copies
+// may read up to 12 bytes outside a row, inside the close / feat arrays' 16-byte-aligned allocation units)
+__device__ __forceinline__ void env_mkt_issue(const EnvArgs& a, uint8_t* pst, int64_t s, int k, uint32_t bar) {
+    const int n = a.n;
+    const int64_t t = s + k;
+    const bool done = (k + 1 == a.horizon) || (t + 1 == a.T_data - 1);
+    const int64_t t_obs = done ? s : t + 1;
+    const uint32_t m = smem_u32(pst + ENVP_MKT);
+    uint16_t* off = reinterpret_cast<uint16_t*>(pst + ENVP_HDR + 24);
+    auto span = [](const float* p, uint32_t bytes) {
+        const uintptr_t q = reinterpret_cast<uintptr_t>(p);
+        return static_cast<uint32_t>((q + bytes - (q & ~static_cast<uintptr_t>(15)) + 15) & ~static_cast<uintptr_t>(15));
+    };
+    const float* r0 = a.close + t * n;
+    const float* r1 = a.close + s * n;
+    const float* r2 = a.feat + t_obs * a.f * n;
+    const uint32_t b0 = static_cast<uint32_t>(2 * n * 4), b1 = static_cast<uint32_t>(n * 4);
+    const uint32_t b2 = static_cast<uint32_t>(a.f * n * 4);
+    const uint32_t w0 = span(r0, b0), w1 = span(r1, b1), w2 = span(r2, b2);
+    mbar_arrive_expect_tx(bar, w0 + w1 + w2);
+    env_mkt_window(m, r0, b0, bar, off);                  // p_t, p_{t+1}
+    env_mkt_window(m + w0, r1, b1, bar, off + 1);         // p_0
+    env_mkt_window(m + w0 + w1, r2, b2, bar, off + 2);    // indicators at t_obs
+    off[1] = static_cast<uint16_t>(off[1] + (w0 >> 2));
+    off[2] = static_cast<uint16_t>(off[2] + ((w0 + w1) >> 2));
+}
+
 // One env tile (32 envs) on 128 threads (tid 0..127).  sync_id 0: the tile is a whole block (__syncthreads,
 // the block initialises its own mbarriers at `bar`); sync_id > 0: the tile is a 128-thread group of a larger
 // block (the fused rollout kernel) synchronised with named barrier sync_id, whose mbarriers at `bar` were
-// initialised once and complete once per step (wait parity `par`).
+// initialised once and complete once per step (wait parity `par`).  With `pst` (fused, n % 4 == 0) the tile header,
+// ledger state and market rows come from the persistent state (the rows on mkt_bar, one completion per step), and
+// the tile issues the next step's row copies at its end when `issue_next`.
 // StepT: EnvStep, or EnvArgs itself (the standalone kernel reads its step slices straight from the parameters)
 template <int SELL_UNROLL, int BUY_UNROLL, typename StepT>
 __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs a, const StepT st, const int tile,
                                               const int tid, uint8_t* env_smem, const uint32_t bar_in, const uint32_t par,
-                                              const int sync_id) {
+                                              const int sync_id, uint8_t* pst = nullptr, const uint32_t mkt_bar = 0,
+                                              const bool issue_next = false) {
     auto sync = [sync_id] {
         if (sync_id == 0) __syncthreads();
         else named_bar_sync(static_cast<uint32_t>(sync_id), ENV_THREADS);
@@ -161,9 +213,10 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     double* p_t64 = unit_s + n;                                           // [n] p_t as float64
     double* p_164 = unit_s + 2 * n;                                       // [n] p_{t+1} as float64
     double* rcp_s = unit_s + 3 * n;                                       // [n] fl(1 / unit)
-    float* p_t = reinterpret_cast<float*>(env_smem + SL.p);
+    const uint16_t* poff = reinterpret_cast<const uint16_t*>(pst + ENVP_HDR + 24);
+    float* p_t = pst ? reinterpret_cast<float*>(pst + ENVP_MKT) + poff[0] : reinterpret_cast<float*>(env_smem + SL.p);
     float* p_1 = p_t + n;
-    float* p_0 = p_1 + n;
+    float* p_0 = pst ? reinterpret_cast<float*>(pst + ENVP_MKT) + poff[1] : p_1 + n;
     uint16_t* tmpl = reinterpret_cast<uint16_t*>(env_smem + SL.tmpl);
     uint16_t* stg = reinterpret_cast<uint16_t*>(env_smem + SL.stg);                           // [32][e_pad]
     double* ph_s = reinterpret_cast<double*>(env_smem + SL.ph);                               // [32]
@@ -199,16 +252,25 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     }
     // per-env ledger state (warp 0 owns the ledger)
     double cash0 = 0.0, v0 = 0.0, disc0 = 0.0;
-    if (warp == 0 && active && a.mode != 2) {
+    const double* pled = reinterpret_cast<const double*>(pst + ENVP_LEDGER);
+    if (pst) {
+        if (warp == 0) {
+            cash0 = pled[lane];
+            v0 = pled[32 + lane];
+            disc0 = pled[64 + lane];
+        }
+    } else if (warp == 0 && active && a.mode != 2) {
         cash0 = a.cash[e];
         if (stepping) {
             v0 = a.asset[e];
             disc0 = a.disc[e];
         }
     }
-    const int64_t s = a.tile_start[tile];
-    const int k = a.mode == 2 ? 0 : a.tile_k[tile];
-    const double gpow = a.mode == 2 ? 1.0 : a.tile_gpow[tile];
+    const int64_t s = pst ? *reinterpret_cast<const int64_t*>(pst + ENVP_HDR) : a.tile_start[tile];
+    const int k = pst ? *reinterpret_cast<const int32_t*>(pst + ENVP_HDR + 8)
+                      : (a.mode == 2 ? 0 : a.tile_k[tile]);
+    const double gpow = pst ? *reinterpret_cast<const double*>(pst + ENVP_HDR + 16)
+                            : (a.mode == 2 ? 1.0 : a.tile_gpow[tile]);
     const int64_t t = s + k;
     const bool done = stepping && ((k + 1 == a.horizon) || (t + 1 == a.T_data - 1));
     const int64_t t_obs = stepping ? (done ? s : t + 1) : t;   // market row of the next observation
@@ -231,7 +293,11 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
         }
     }
     // ---- 2. market rows: every thread issues all of its loads before using any
-    {
+    if (pst) {   // already in shared memory (the copies issued during the actor phase)
+        mbar_wait(mkt_bar, par);
+        const float* feat_s = reinterpret_cast<const float*>(pst + ENVP_MKT) + poff[2];
+        for (int j = tid; j < a.f * n; j += ENV_THREADS) tmpl[1 + 2 * n + j] = f2bf(feat_s[j]);
+    } else {
         const int total = 3 * n + a.f * n;
         constexpr int PER = (ENV_MAX_MARKET + ENV_THREADS - 1) / ENV_THREADS;
         float vals[PER];
@@ -507,6 +573,12 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
                 a.asset[e] = v;
                 a.disc[e] = disc;
             }
+            if (pst) {
+                double* pl = reinterpret_cast<double*>(pst + ENVP_LEDGER);
+                pl[lane] = cash;
+                pl[32 + lane] = v;
+                pl[64 + lane] = disc;
+            }
             stg[lane * e_pad] = f2bf(static_cast<float>(cash / a.C0));
         }
     } else {
@@ -542,6 +614,17 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     }
     sync();
     if (trc && tid == 0) trc[6] = clock64();
+    if (pst && stepping && tid == 0) {
+        // the next step's header, and (issue_next) its market rows, which land during the next actor phase; every
+        // thread of the tile is done reading the rows (the sync above)
+        const int k1 = done ? 0 : k + 1;
+        *reinterpret_cast<int32_t*>(pst + ENVP_HDR + 8) = k1;
+        *reinterpret_cast<double*>(pst + ENVP_HDR + 16) = done ? 1.0 : __dmul_rn(gpow, a.gamma);
+        if (issue_next) {
+            fence_proxy_async_smem();
+            env_mkt_issue(a, pst, s, k1, mkt_bar);
+        }
+    }
 #ifdef POD_EXP_GTIME
     if (sync_id == 0 && tid == 0 && a.mode == 0 && st.noise_t - 1 < 1024) atomicMax(&g_gtime[st.noise_t - 1][3], gtimer());
 #endif

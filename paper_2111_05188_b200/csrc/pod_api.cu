@@ -694,10 +694,13 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
         fe.sampling = sampling;
         fe.env_stride = (env_smem_bytes(n, e->k_pad) + 127) / 128 * 128;
         fe.k_pad = e->k_pad;
+        // the env tiles' persistent state (header, ledger, the next step's market rows by bulk copy)
+        fe.persist = p.actor_smem + 2 * static_cast<size_t>(env_persist_bytes(n, e->cfg.n_feat)) <= 232448
+                         ? env_persist_bytes(n, e->cfg.n_feat) : 0;
         cudaLaunchConfig_t lc{};
         lc.gridDim = dim3(static_cast<unsigned>(2 * aa.mtiles));
         lc.blockDim = dim3(ACT_THREADS);
-        lc.dynamicSmemBytes = p.actor_smem;
+        lc.dynamicSmemBytes = p.actor_smem + 2 * static_cast<size_t>(fe.persist);
         lc.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
