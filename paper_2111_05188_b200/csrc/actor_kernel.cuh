@@ -141,11 +141,14 @@ struct FusedMaps {
     ActorMaps am;
     EnvMaps em;
 };
-// shared memory of the two env tiles of a CTA fits in the activation buffer
+// per TMEM quadrant: the head's staged actions [64 tickers][32 envs] int16 and log-prob partials [2][32] float
+constexpr int FUSED_QUAD_STAGE = 2 * ACT_MAX_HQ * 64 + 256;
+// shared memory of the two env tiles of a CTA, and the head's four quadrant stages after them, fit in the
+// activation buffer
 inline bool fused_env_fits(int n, int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
     const int es = (env_smem_bytes(n, k_pad) + 127) / 128 * 128;
-    return 2 * es <= ka * 16384;
+    return 2 * es + 4 * FUSED_QUAD_STAGE <= ka * 16384;
 }
 
 // tanh(x) = 1 - 2 / (e^{2x} + 1) on the SFU (ex2.approx, approximate reciprocal): absolute error
@@ -223,6 +226,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t envdone_b = obs_b + 136u;
     const uint32_t envbar_b = obs_b + 144u;    // [2 tiles][1 + ENV_BUY_CHUNKS]
     const uint32_t envmkt_b = obs_b + 272u;    // [2 tiles] the next step's market rows landed (bulk copies)
+    const uint32_t envin_b = obs_b + 288u;     // [2 tiles] both CTAs' heads' actions + log-prob partials landed
     uint8_t* const env_pst = base + bias_off + ACT_BIAS_FLOATS * 4 + 512;   // [2 tiles][persist] (FUSED)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
@@ -274,6 +278,8 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                 mbar_init(envdone_b, 2);
                 mbar_init(envmkt_b, 1);
                 mbar_init(envmkt_b + 8u, 1);
+                mbar_init(envin_b, 1);        // the tile's own expect_tx arrival + the heads' st.async bytes
+                mbar_init(envin_b + 8u, 1);
                 for (int g = 0; g < 2; ++g) {
                     mbar_init(envbar_b + 64u * g, 1);   // the env tile's TMA barrier
                     for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(envbar_b + 64u * g + 8u * (c + 1), 32);
@@ -620,6 +626,17 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
 #endif
             if (tr && it == 0 && etid == 0) tr[24] = clock64();
             // the head: sampling, the action map and the log-prob partials
+            // FUSED: this thread's row is env lane `lane` of env tile `quad` of the M-tile (it lives in CTA quad >> 1, env
+            // group quad & 1).  The head stages that tile's actions of this CTA's tickers ([head_half][32] int16) and its
+            // two log-prob partials ([2][32] float) in this CTA's activation buffer past the env tiles' areas, and the
+            // quad's two warps ship them with two bulk DSMEM copies into the tile's aint_s / stg, counted on its envin_b
+            int16_t* aint_stage = nullptr;
+            float* logp_stage = nullptr;
+            if constexpr (FUSED) {
+                uint8_t* qs = base + 2 * fe->env_stride + quad * FUSED_QUAD_STAGE;
+                aint_stage = reinterpret_cast<int16_t*>(qs);
+                logp_stage = reinterpret_cast<float*>(qs + ACT_MAX_HQ * 2 * 64);
+            }
             auto head = [&] {
             const float* bias = bias_s + boff;
             const float* log_std = bias_s + boff + head_half;
@@ -669,7 +686,11 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                         const float u = tanh_sfu(raw[jj]);
                         const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
                         ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
-                        if (ok) a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
+                        if constexpr (FUSED) {
+                            if (ok) aint_stage[(i0 + jj - i00) * 32 + lane] = ai8[jj];
+                        } else {
+                            if (ok) a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
+                        }
                     }
                     if (dbg_aint) {
                         for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
@@ -697,32 +718,52 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             }
             if (bad && valid) atomicOr(a.err, 1u);
             if (tr && it == 0 && etid == 0) tr[25] = clock64();
-            // log-prob partial of (rank, hh) for row r -> the [4][N] scratch; the env step that follows combines
-            // the four partials ((p0 + p1) + p2) + p3, so the kernel's tail needs no cross-CTA exchange
-            if (valid && logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
+            // log-prob partial of (rank, hh) for row r -> the [4][N] scratch (FUSED: the env tile's stg); the env step
+            // that follows combines the four partials ((p0 + p1) + p2) + p3, so the kernel's tail needs no exchange
+            if constexpr (FUSED) {
+                if (!vo) logp_stage[hh * 32 + lane] = logp;
+            } else {
+                if (valid && logp_out) a.logp_parts[static_cast<int64_t>(rank * 2 + hh) * a.N + e] = logp;
+            }
             };
             if constexpr (FUSED) {
                 if (!vo) {
                     // ----- the env step of step it on this CTA's two env tiles of the M-tile (epilogue warps
-                    // 2-5: tile 2 rank, warps 6-9: tile 2 rank + 1), once both CTAs' heads are written.
-                    // (Issuing the tiles' holdings TMA and state loads before the head instead slowed the
-                    // head more than it hid: C3 37.6 -> 38.4 us per step.)
+                    // 2-5: tile 2 rank, warps 6-9: tile 2 rank + 1); the tiles wait for both CTAs' heads' st.async
+                    // deliveries on their envin_b, no fence or cluster barrier in between
+                    const int grp = ew >> 2;
+                    if ((etid & 127) == 0) {
+                        // this CTA's env tile: its holdings TMA (the activation buffer is free once this CTA's head
+                        // MMAs are done), and the bytes its envin_b awaits from both CTAs' heads
+                        const int etile = (tl.env0 >> 5) + 2 * static_cast<int>(rank) + grp;
+                        mbar_arrive_expect_tx(envbar_b + 64u * grp, static_cast<uint32_t>(a.n) * 128u);
+                        tma_load_2d(base_u32 + static_cast<uint32_t>(grp * fe->env_stride), &emaps->hold, etile * 32, 0,
+                                    envbar_b + 64u * grp);
+                        mbar_arrive_expect_tx(envin_b + 8u * grp, static_cast<uint32_t>(a.n) * 64u + 512u);
+                    }
                     head();
+                    // ship this quad's staged actions and log-prob partials to its env tile (this CTA or the peer;
+                    // the copies land in the tile's area of the activation buffer: the pair's head MMAs must be done)
+                    fence_proxy_async_smem();
+                    named_bar_sync(5 + static_cast<uint32_t>(quad), 64);
+                    if (hh == 0 && lane == 0) {
+                        const EnvSmemLayout ESL = env_smem_layout(a.n, a.k_pad);
+                        const uint32_t dst = static_cast<uint32_t>(quad >> 1);
+                        const uint32_t tb = base_u32 + static_cast<uint32_t>((quad & 1) * fe->env_stride);
+                        const uint32_t inb = mapa_shared(envin_b + 8u * static_cast<uint32_t>(quad & 1), dst);
+                        const int i00 = static_cast<int>(rank) * head_half;
+                        const int rows = (a.n < i00 + head_half ? a.n : i00 + head_half) - i00;
+                        mbar_wait(accum_b, static_cast<uint32_t>(gL) & 1u);
+                        if (rows > 0)
+                            bulk_s2peer(mapa_shared(tb + static_cast<uint32_t>(ESL.aint + i00 * 64), dst), smem_u32(aint_stage),
+                                        static_cast<uint32_t>(rows * 64), inb);
+                        bulk_s2peer(mapa_shared(tb + static_cast<uint32_t>(ESL.stg + rank * 256), dst), smem_u32(logp_stage),
+                                    256u, inb);
+                    }
 #ifdef POD_EXP_GTIME
                     if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][2] = gtimer();
-#endif
-                    __threadfence();
-                    fence_proxy_async_global();   // the actions, read by the env tiles' TMA
-                    named_bar_sync(1, 256);
-                    if (etid == 0) {
-                        mbar_arrive(headdone_b);
-                        mbar_arrive_remote(mapa_shared(headdone_b, peer));
-                    }
-                    mbar_wait_cluster(headdone_b, static_cast<uint32_t>(it) & 1u);
-#ifdef POD_EXP_GTIME
                     if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][3] = gtimer();
 #endif
-                    const int grp = ew >> 2;
                     const EnvArgs& ea = fe->env;
                     EnvStep st;
                     st.rew = ea.rew + so * a.N;
@@ -738,7 +779,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                                                            etid & 127, base + grp * fe->env_stride, envbar_b + 64u * grp,
                                                            static_cast<uint32_t>(it) & 1u, 3 + grp,
                                                            fe->persist ? env_pst + grp * fe->persist : nullptr,
-                                                           envmkt_b + 8u * grp, it + 1 < fe->T);
+                                                           envmkt_b + 8u * grp, it + 1 < fe->T, envin_b + 8u * grp);
 #ifdef POD_EXP_GTIME
                     if (blockIdx.x == 0 && etid == 0 && it < 1024) g_ftime[it][4] = gtimer();
 #endif

@@ -186,13 +186,15 @@ __device__ __forceinline__ void env_mkt_issue(const EnvArgs& a, uint8_t* pst, in
 // block (the fused rollout kernel) synchronised with named barrier sync_id, whose mbarriers at `bar` were
 // initialised once and complete once per step (wait parity `par`).  With `pst` (fused, n % 4 == 0) the tile header,
 // ledger state and market rows come from the persistent state (the rows on mkt_bar, one completion per step), and
-// the tile issues the next step's row copies at its end when `issue_next`.
+// the tile issues the next step's row copies at its end when `issue_next`.  With `in_bar` (fused) the caller has
+// issued the holdings TMA (n x 128 bytes on `bar`), and the actor's heads deliver the actions into aint_s and the
+// four log-prob partials of each env into the first 512 bytes of stg ([4][32] float) by st.async on in_bar.
 // StepT: EnvStep, or EnvArgs itself (the standalone kernel reads its step slices straight from the parameters)
 template <int SELL_UNROLL, int BUY_UNROLL, typename StepT>
 __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs a, const StepT st, const int tile,
                                               const int tid, uint8_t* env_smem, const uint32_t bar_in, const uint32_t par,
                                               const int sync_id, uint8_t* pst = nullptr, const uint32_t mkt_bar = 0,
-                                              const bool issue_next = false) {
+                                              const bool issue_next = false, const uint32_t in_bar = 0) {
     auto sync = [sync_id] {
         if (sync_id == 0) __syncthreads();
         else named_bar_sync(static_cast<uint32_t>(sync_id), ENV_THREADS);
@@ -241,7 +243,15 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     // (holdings, ledger state, market rows, tile constants) is loaded while the actor grid is still
     // running; griddepcontrol.wait precedes the first read of the actor's outputs (the actions) and the
     // first write the actor could observe (the next step's noise).
-    if (tma && tid == 0) {
+    if (in_bar) {
+        mbar_wait(in_bar, par);   // the actions and log-prob partials of this step have landed
+        if (warp == 1 && stepping && a.logp_parts && st.logp_out && active) {
+            // summed in the actor's own order; read before anything rewrites stg
+            const float* pp = reinterpret_cast<const float*>(stg) + lane;
+            st.logp_out[e] = ((pp[0] + pp[32]) + pp[64]) + pp[96];
+        }
+    }
+    if (!in_bar && tma && tid == 0) {
         if (sync_id == 0) {
             mbar_init(bar, 1);
             fence_mbar_init();
@@ -354,7 +364,7 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
 #ifdef POD_EXP_GTIME
     if (sync_id == 3 && tid == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][6] = gtimer();
 #endif
-    if (warp == 1 && stepping && a.logp_parts && st.logp_out && active) {
+    if (!in_bar && warp == 1 && stepping && a.logp_parts && st.logp_out && active) {
         // the actor's four log-prob partials of this env, summed in the actor's own order
         const float* pp = a.logp_parts + e;
         if (sync_id == 0) {
