@@ -408,6 +408,9 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
                 cash = __dadd_rn(cash, __dmul_rn(__dmul_rn(p_t64[i], static_cast<double>(q)), omc));
             }
             if (trc && lane == 0) trc[2] = clock64();
+#ifdef POD_EXP_GTIME
+            if (sync_id == 3 && lane == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][11] = gtimer();
+#endif
             // buying set (Eq. 3 "- (p^B)^T k^B"), tickers ascending.
             // The oracle computes qmax = floor(fl(b / unit)) (minus one if fl(qmax unit) > b),
             // q = max(0, min(a, qmax)), b -= fl(q unit).  Here, with y = fl(b fl(1/unit)) and
@@ -485,6 +488,9 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
                 mbar_arrive(chunk_bar + 8u * c);   // release: this lane's holdings of the chunk
             }
             if (trc && lane == 0) trc[3] = clock64();
+#ifdef POD_EXP_GTIME
+            if (sync_id == 3 && lane == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][10] = gtimer();
+#endif
         }
     } else {
         if (st.gen_noise) {
@@ -517,6 +523,18 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
             uint16_t* my = stg + lane * e_pad;
             if (warp == 1) {
                 for (int c = 1 + n; c < e_pad; ++c) my[c] = tmpl[c];
+            }
+            if (sync_id != 0 && st.obs_out) {
+                // fused: the tile-shared part of the 32 rows of s_{t+1} (16-byte chunks from e_pad on: p/p0,
+                // indicators, pad — the same for every env of the tile) leaves now, while the ledger runs; the
+                // tail writes only the per-env chunks
+                const int c0 = e_pad / 8, nc = a.k_pad / 8 - c0;
+                const int rows = min(32, a.N - tile * 32);
+                uint4* dst0 = reinterpret_cast<uint4*>(st.obs_out + static_cast<int64_t>(tile) * 32 * a.k_pad);
+                for (int idx = tid - 32; idx < rows * nc; idx += ENV_THREADS - 32) {
+                    const int row = idx / nc, c = c0 + idx % nc;
+                    dst0[static_cast<int64_t>(row) * (a.k_pad / 8) + c] = *reinterpret_cast<const uint4*>(tmpl + c * 8);
+                }
             }
             double ph = 0.0;
             for (int c = 0; c < nch; ++c) {
@@ -608,14 +626,18 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     }
     sync();
     if (trc && tid == 0) trc[5] = clock64();
+#ifdef POD_EXP_GTIME
+    if (sync_id == 3 && tid == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][8] = gtimer();
+#endif
     // ---- 6. write s_{t+1}: env rows spread over the 4 warps, 16-B chunks (512 B per instruction)
     if (st.obs_out) {
         const int chunks = a.k_pad / 8;
         const int rows = min(32, a.N - tile * 32);
 #pragma unroll 4
+        const int cend = (sync_id != 0 && stepping) ? e_pad / 8 : chunks;   // fused: the rest left early
         for (int row = warp; row < rows; row += 4) {
             uint4* dst = reinterpret_cast<uint4*>(st.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
-            for (int c = lane; c < chunks; c += 32) {
+            for (int c = lane; c < cend; c += 32) {
                 const uint4 val = c * 8 < e_pad ? *reinterpret_cast<const uint4*>(stg + row * e_pad + c * 8)
                                                 : *reinterpret_cast<const uint4*>(tmpl + c * 8);
                 dst[c] = val;
@@ -624,6 +646,9 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     }
     sync();
     if (trc && tid == 0) trc[6] = clock64();
+#ifdef POD_EXP_GTIME
+    if (sync_id == 3 && tid == 0 && blockIdx.x == 0 && st.noise_t - 1 < 1024) g_ftime[st.noise_t - 1][9] = gtimer();
+#endif
     if (pst && stepping && tid == 0) {
         // the next step's header, and (issue_next) its market rows, which land during the next actor phase; every
         // thread of the tile is done reading the rows (the sync above)

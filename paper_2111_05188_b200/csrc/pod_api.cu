@@ -1441,6 +1441,6 @@ extern "C" int pod_debug_gtime(unsigned long long* host, int reset) {
     return cudaMemcpyFromSymbol(host, pod::g_gtime, sizeof(unsigned long long) * 1024 * 4) == cudaSuccess ? 0 : 1;
 }
 extern "C" int pod_debug_ftime(unsigned long long* host) {
-    return cudaMemcpyFromSymbol(host, pod::g_ftime, sizeof(unsigned long long) * 1024 * 8) == cudaSuccess ? 0 : 1;
+    return cudaMemcpyFromSymbol(host, pod::g_ftime, sizeof(unsigned long long) * 1024 * 12) == cudaSuccess ? 0 : 1;
 }
 #endif

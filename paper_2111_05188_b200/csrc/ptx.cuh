@@ -254,7 +254,7 @@ __device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* 
 }
 #ifdef POD_EXP_GTIME
 __device__ unsigned long long g_gtime[1024][4];   // [step][actor start min, actor end max, env start min, env end max]
-__device__ unsigned long long g_ftime[1024][8];   // fused rollout, CTA 0: [step][phase stamps]
+__device__ unsigned long long g_ftime[1024][12];   // fused rollout, CTA 0: [step][phase stamps]
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -27,13 +27,13 @@ torch.cuda.synchronize()
 L.pod_debug_gtime(None, 1)
 env.rollout(T, tr, actor=actor)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * (1024 * 8))()
+buf = (C.c_ulonglong * (1024 * 12))()
 L.pod_debug_ftime(buf)
-g = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8)[:T].astype(np.float64)
+g = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 12)[:T].astype(np.float64)
 med = lambda x: float(np.median(x))
-names = ["actor layers", "head compute", "head fence+exchange", "env loads", "env ledger", "env stores",
-         "env fence+exchange"]
-order = [0, 1, 2, 3, 6, 7, 4, 5]   # stamp columns in time order
+names = ["actor layers", "head compute", "head fence+exchange", "env loads", "env sells", "env buys",
+         "env ledger sync", "env reward", "env obs rows", "env end", "env fence+exchange"]
+order = [0, 1, 2, 3, 6, 11, 10, 7, 8, 9, 4, 5]   # stamp columns in time order
 parts = [med(g[:, order[k + 1]] - g[:, order[k]]) for k in range(len(order) - 1)]
 obs = med(g[1:, 0] - g[:-1, 5])
 step = med(np.diff(g[:, 0]))
