@@ -776,7 +776,12 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     st.gen_noise = (fe->sampling && it + 1 < fe->T) ? 1 : 0;
                     st.noise_t = it + 1;
                     env_step_tile<SELL_UNROLL, BUY_UNROLL>(*emaps, ea, st, (tl.env0 >> 5) + 2 * static_cast<int>(rank) + grp,
-                                                           etid & 127, base + grp * fe->env_stride, envbar_b + 64u * grp,
+                                                           // group 1's roles rotated: its ledger warp is CTA warp 7
+                                                           // (sub-partition 3), group 0's warp 2 (sub-partition 2), so the
+                                                           // two float64 chains do not share a sub-partition (nor the ones
+                                                           // where the TMA and MMA threads wait)
+                                                           grp == 0 ? (etid & 127) : ((etid + 96) & 127),
+                                                           base + grp * fe->env_stride, envbar_b + 64u * grp,
                                                            static_cast<uint32_t>(it) & 1u, 3 + grp,
                                                            fe->persist ? env_pst + grp * fe->persist : nullptr,
                                                            envmkt_b + 8u * grp, it + 1 < fe->T, envin_b + 8u * grp);
