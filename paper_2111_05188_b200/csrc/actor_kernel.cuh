@@ -143,6 +143,15 @@ struct FusedMaps {
 };
 // per TMEM quadrant: the head's staged actions [64 tickers][32 envs] int16 and log-prob partials [2][32] float
 constexpr int FUSED_QUAD_STAGE = 2 * ACT_MAX_HQ * 64 + 256;
+// Fused rollout: the env-tile thread index of CTA warp w (2..9) — tile 0 on warps 2-5, tile 1 on warps 6-9 — with
+// the roles placed on sub-partitions (warp w runs on sub-partition w % 4): the two ledger warps (env warp 0) on
+// sub-partitions 2 and 3 (warps 2, 7), the two revaluation warps (env warp 1, float64 too) on 1 and 0 (warps 5, 8),
+// away from each other and from the TMA / MMA threads' sub-partitions where possible
+__device__ __forceinline__ int env_role_tid(int w, int lane) {
+    // warp:            2  3  4  5  6  7  8  9
+    constexpr int role[8] = {0, 2, 3, 1, 2, 0, 1, 3};
+    return role[w - 2] * 32 + lane;
+}
 // shared memory of the two env tiles of a CTA, and the head's four quadrant stages after them, fit in the
 // activation buffer
 inline bool fused_env_fits(int n, int k_pad, int hidden) {
@@ -776,11 +785,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     st.gen_noise = (fe->sampling && it + 1 < fe->T) ? 1 : 0;
                     st.noise_t = it + 1;
                     env_step_tile<SELL_UNROLL, BUY_UNROLL>(*emaps, ea, st, (tl.env0 >> 5) + 2 * static_cast<int>(rank) + grp,
-                                                           // group 1's roles rotated: its ledger warp is CTA warp 7
-                                                           // (sub-partition 3), group 0's warp 2 (sub-partition 2), so the
-                                                           // two float64 chains do not share a sub-partition (nor the ones
-                                                           // where the TMA and MMA threads wait)
-                                                           grp == 0 ? (etid & 127) : ((etid + 96) & 127),
+                                                           env_role_tid(warp, lane),
                                                            base + grp * fe->env_stride, envbar_b + 64u * grp,
                                                            static_cast<uint32_t>(it) & 1u, 3 + grp,
                                                            fe->persist ? env_pst + grp * fe->persist : nullptr,
