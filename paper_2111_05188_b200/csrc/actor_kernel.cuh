@@ -148,9 +148,8 @@ constexpr int FUSED_QUAD_STAGE = 2 * ACT_MAX_HQ * 64 + 256;
 // sub-partitions 2 and 3 (warps 2, 7), the two revaluation warps (env warp 1, float64 too) on 1 and 0 (warps 5, 8),
 // away from each other and from the TMA / MMA threads' sub-partitions where possible
 __device__ __forceinline__ int env_role_tid(int w, int lane) {
-    // warp:            2  3  4  5  6  7  8  9
-    constexpr int role[8] = {0, 2, 3, 1, 2, 0, 1, 3};
-    return role[w - 2] * 32 + lane;
+    // env warp of CTA warps 2..9 = {0, 2, 3, 1, 2, 0, 1, 3}, two bits each (a table would live in local memory)
+    return static_cast<int>((0xD278u >> (2 * (w - 2))) & 3u) * 32 + lane;
 }
 // shared memory of the two env tiles of a CTA, and the head's four quadrant stages after them, fit in the
 // activation buffer
@@ -653,6 +652,8 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             float logp = 0.0f;
             bool bad = false;
             const float half_ln_2pi = 0.918938533204672742f;
+            const bool fast_map = FUSED && a.h_max <= 128;
+            const float hmax_f = static_cast<float>(a.h_max);
             const bool vec = (a.n % 4) == 0;
             const int i00 = static_cast<int>(rank) * head_half;
     #pragma unroll
@@ -684,6 +685,11 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     // raw = mu + sigma z, log-prob term, tanh on the SFU, integer map in float64.  One straight-line
                     // body for all 8 columns of the chunk, the tickers past n masked (their stores and log-prob
                     // terms predicated off): half the code of a separate guarded copy for the last chunk
+                    // FUSED: the map's floor(|u| h_max + 1/2) is decided in float32 when that is provably the float64 result
+                    // (h_max <= 128: |fl32(fl32(|u| h) + 1/2) - (|u| h + 1/2)| <= 2^-16, so a fractional part d in
+                    // [2^-15, 1 - 2^-15] has the exact floor); a chunk in which any lane lands closer to a half-integer
+                    // redoes its map in float64, the oracle's precision (R#6)
+                    bool unsure = !fast_map;
     #pragma unroll
                     for (int jj = 0; jj < 8; ++jj) {
                         const bool ok = i0 + jj < a.n;
@@ -693,13 +699,31 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                         raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
                         if (ok) logp += (-0.5f * z * z - ls) - half_ln_2pi;
                         const float u = tanh_sfu(raw[jj]);
-                        const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
-                        ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
                         if constexpr (FUSED) {
-                            if (ok) aint_stage[(i0 + jj - i00) * 32 + lane] = ai8[jj];
+                            const float r = fmaf(fabsf(u), hmax_f, 0.5f);
+                            const float fl = floorf(r);
+                            const float d = r - fl;
+                            unsure |= d < 3.0517578125e-05f || d > 0.999969482421875f;
+                            const int m = static_cast<int>(fl);
+                            ai8[jj] = static_cast<int16_t>(u < 0.0f ? -m : m);
                         } else {
+                            const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
+                            ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
                             if (ok) a.aint[static_cast<int64_t>(i0 + jj) * a.N + e] = ai8[jj];
                         }
+                    }
+                    if (FUSED && __any_sync(0xffffffffu, unsure)) {
+    #pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const float u = tanh_sfu(raw[jj]);
+                            const double m = floor(static_cast<double>(fabsf(u)) * static_cast<double>(a.h_max) + 0.5);
+                            ai8[jj] = static_cast<int16_t>(u < 0.0f ? -static_cast<int>(m) : static_cast<int>(m));
+                        }
+                    }
+                    if constexpr (FUSED) {
+    #pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (i0 + jj < a.n) aint_stage[(i0 + jj - i00) * 32 + lane] = ai8[jj];
                     }
                     if (dbg_aint) {
                         for (int jj = 0; jj < 8 && i0 + jj < a.n; ++jj)
