@@ -235,6 +235,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t envbar_b = obs_b + 144u;    // [2 tiles][1 + ENV_BUY_CHUNKS]
     const uint32_t envmkt_b = obs_b + 272u;    // [2 tiles] the next step's market rows landed (bulk copies)
     const uint32_t envin_b = obs_b + 288u;     // [2 tiles] both CTAs' heads' actions + log-prob partials landed
+    const uint32_t obsa_b = obs_b + 304u;      // FUSED: [8] obs atom kb landed (layer 0 starts on the first atom)
     uint8_t* const env_pst = base + bias_off + ACT_BIAS_FLOATS * 4 + 512;   // [2 tiles][persist] (FUSED)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
@@ -286,8 +287,9 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                 mbar_init(envdone_b, 2);
                 mbar_init(envmkt_b, 1);
                 mbar_init(envmkt_b + 8u, 1);
-                mbar_init(envin_b, 1);        // the tile's own expect_tx arrival + the heads' st.async bytes
+                mbar_init(envin_b, 1);        // the tile's own expect_tx arrival + the heads' bulk-copy bytes
                 mbar_init(envin_b + 8u, 1);
+                for (int kb = 0; kb < 8; ++kb) mbar_init(obsa_b + 8u * kb, 1);
                 for (int g = 0; g < 2; ++g) {
                     mbar_init(envbar_b + 64u * g, 1);   // the env tile's TMA barrier
                     for (int c = 0; c < ENV_BUY_CHUNKS; ++c) mbar_init(envbar_b + 64u * g + 8u * (c + 1), 32);
@@ -331,9 +333,16 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     if (FUSED && it > 0) mbar_wait_cluster(envdone_b, static_cast<uint32_t>(it - 1) & 1u);
                     const int kb0 = a.k_pad / 64;
                     const int row0 = FUSED ? it * a.N : a.obs_row0;
-                    mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
-                    for (int kb = 0; kb < kb0; ++kb)
-                        tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, row0 + tl.env0, obs_b);
+                    if constexpr (FUSED) {   // one barrier per atom: layer 0's MMAs start as the first atom lands
+                        for (int kb = 0; kb < kb0; ++kb) {
+                            mbar_arrive_expect_tx(obsa_b + 8u * kb, 16384u);
+                            tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, row0 + tl.env0, obsa_b + 8u * kb);
+                        }
+                    } else {
+                        mbar_arrive_expect_tx(obs_b, static_cast<uint32_t>(kb0) * 16384u);
+                        for (int kb = 0; kb < kb0; ++kb)
+                            tma_load_2d(act_s + kb * 16384u, &maps.obs, kb * 64, row0 + tl.env0, obs_b);
+                    }
                     obs_issued = true;
                 };
                 auto before_stage = [&](int l) {
@@ -411,12 +420,11 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             const int na = a.hidden / 128;           // activation atoms (64 cols) per CTA half
             Tile tl;
             for (int it = 0; tile_of(it, tl); ++it) {
-                mbar_wait(obs_b, static_cast<uint32_t>(it) & 1u);
-                tc_fence_after();
-#ifdef POD_EXP_GTIME
-                // fused rollout, CTA 0: [step][obs landed, head accumulator ready, both heads written, env done]
-                if (FUSED && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
-#endif
+                if constexpr (!FUSED) {
+                    mbar_wait(obs_b, static_cast<uint32_t>(it) & 1u);
+                    tc_fence_after();
+                }
+
                 if (tr && it == 0) tr[1] = clock64();
                 for (int l = 0; l < a.n_layers; ++l) {
                     const int g = it * a.n_layers + l;                 // layer count over tiles: TMEM buffer g & 1
@@ -438,6 +446,14 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                             for (int q = 0; q < kp; ++q) {
                                 const int j = j0 + q;
                                 const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
+                                if (FUSED && l == 0 && (j & 1) == 0) {
+                                    mbar_wait(obsa_b + 8u * (j >> 1), static_cast<uint32_t>(it) & 1u);
+                                    tc_fence_after();
+                                }
+#ifdef POD_EXP_GTIME
+                                // fused rollout, CTA 0: [step][obs atom 0 landed, head accumulator ready, ...]
+                                if (FUSED && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
+#endif
                                 if (l > 0 && (j & 1) == 0) {
                                     const int ja = j >> 1;
                                     if (ja < na) {
@@ -467,6 +483,14 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     for (int c = 0; c < half / bn; ++c) {
                         for (int j = 0; j < KB; ++j) {
                             const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
+                            if (FUSED && l == 0 && c == 0 && (j & 1) == 0) {
+                                mbar_wait(obsa_b + 8u * (j >> 1), static_cast<uint32_t>(it) & 1u);
+                                tc_fence_after();
+                            }
+#ifdef POD_EXP_GTIME
+                            // fused rollout, CTA 0: [step][obs atom 0 landed, head accumulator ready, ...]
+                            if (FUSED && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
+#endif
                             if (l > 0 && c == 0 && (j & 1) == 0) {
                                 // h_l atom by atom: own atoms as the epilogue finishes them, then the
                                 // peer's atoms as its bulk copies land
