@@ -528,18 +528,20 @@ def test_fused_rollout_bit_identical(n, N, agents, nh, hid, det, monkeypatch):
     all T steps, rollout_fused_kernel; the default where it fits one wave) against the separate actor and
     env-step launches (POD_FUSED=0): every trajectory output — observations, actions, log-probs, mean
     actions, rewards, done flags, holdings, cash, equity, critic values including the bootstrap V(s_T) —
-    and the env state left for the next rollout are bit-identical, over two chained rollouts with
-    episode resets inside them (H = 5)."""
+    and the env state left for the next rollout are bit-identical, over chained rollouts of 7, 7, 1 and 2 steps
+    with episode resets inside them (H = 5)."""
     outs = []
     for flag in ("1", "0"):
         monkeypatch.setenv("POD_FUSED", flag)
         c = Case(n=n, f=3, T_data=600, N=N, H=5, n_agents=agents, seed=15)
         aws, params, actor = _actor(c, nh, hid, n_agents=agents)
         res = []
-        tr = api.Trajectory.allocate(7, N, n, c.k_pad, debug=True, critic=True, equity=True)
         c.env.reset(c.starts)
-        for _ in range(2):
-            c.env.rollout(7, tr, actor=actor, deterministic=det)
+        # rollouts of 7, 1 and 2 steps, with and without the critic (the fused kernel's iteration T is the
+        # bootstrap pass only with it)
+        for T, critic in ((7, True), (7, True), (1, True), (2, False)):
+            tr = api.Trajectory.allocate(T, N, n, c.k_pad, debug=True, critic=critic, equity=True)
+            c.env.rollout(T, tr, actor=actor, deterministic=det)
             torch.cuda.synchronize()
             res.append({k: v.clone() for k, v in vars(tr).items() if v is not None})
         res.append(dict(zip(("hold", "cash", "asset", "ep_ret"), c.env.read_state())))
