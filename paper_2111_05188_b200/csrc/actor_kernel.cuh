@@ -452,7 +452,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                                 }
 #ifdef POD_EXP_GTIME
                                 // fused rollout, CTA 0: [step][obs atom 0 landed, head accumulator ready, ...]
-                                if (FUSED && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
+                                if (FUSED && l == 0 && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
 #endif
                                 if (l > 0 && (j & 1) == 0) {
                                     const int ja = j >> 1;
@@ -489,7 +489,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                             }
 #ifdef POD_EXP_GTIME
                             // fused rollout, CTA 0: [step][obs atom 0 landed, head accumulator ready, ...]
-                            if (FUSED && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
+                            if (FUSED && l == 0 && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
 #endif
                             if (l > 0 && c == 0 && (j & 1) == 0) {
                                 // h_l atom by atom: own atoms as the epilogue finishes them, then the
