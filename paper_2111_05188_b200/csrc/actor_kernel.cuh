@@ -228,9 +228,8 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t actfree_b = obs_b + 80u;    // this CTA's MMAs of a tile are done reading act_s (commit)
     const uint32_t tslot_s = obs_b + 112u;
     const uint32_t accl_b = obs_b + 120u;      // this CTA's MMAs of a layer are complete (local commit)
-    // FUSED: both CTAs' heads of step t are written (2 arrivals: this CTA's and the peer's), both CTAs' env
-    // steps of step t are done (s_{t+1}, holdings and noise written), and the env tiles' own mbarriers
-    const uint32_t headdone_b = obs_b + 128u;
+    // FUSED: both CTAs' env steps of step t are done (s_{t+1}, holdings and noise written; 2 arrivals), and the
+    // env tiles' own mbarriers
     const uint32_t envdone_b = obs_b + 136u;
     const uint32_t envbar_b = obs_b + 144u;    // [2 tiles][1 + ENV_BUY_CHUNKS]
     const uint32_t envmkt_b = obs_b + 272u;    // [2 tiles] the next step's market rows landed (bulk copies)
@@ -283,7 +282,6 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                 mbar_init(peerrdy_b + 8u * j, 1);    // the MMA thread's expect_tx + the peer's bytes
             }
             if (FUSED) {
-                mbar_init(headdone_b, 2);
                 mbar_init(envdone_b, 2);
                 mbar_init(envmkt_b, 1);
                 mbar_init(envmkt_b + 8u, 1);
@@ -786,7 +784,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             if constexpr (FUSED) {
                 if (!vo) {
                     // ----- the env step of step it on this CTA's two env tiles of the M-tile (epilogue warps
-                    // 2-5: tile 2 rank, warps 6-9: tile 2 rank + 1); the tiles wait for both CTAs' heads' st.async
+                    // 2-5: tile 2 rank, warps 6-9: tile 2 rank + 1); the tiles wait for both CTAs' heads' bulk copies
                     // deliveries on their envin_b, no fence or cluster barrier in between
                     const int grp = ew >> 2;
                     if ((etid & 127) == 0) {

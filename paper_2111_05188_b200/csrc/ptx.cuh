@@ -219,16 +219,6 @@ __device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, uint32_t src_c
                  "r"(src_cta), "r"(bytes), "r"(bar_cluster)
                  : "memory");
 }
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr_cluster, float v) {
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr_cluster), "f"(v) : "memory");
-}
-// 4-byte store into (possibly another CTA's) shared memory whose completion is counted, in bytes, on an mbarrier
-// of the destination CTA (complete_tx): the consumer waits on its barrier; no release by the producer
-__device__ __forceinline__ void st_async_b32(uint32_t addr_cluster, uint32_t v, uint32_t bar_cluster) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr_cluster), "r"(v),
-                 "r"(bar_cluster)
-                 : "memory");
-}
 // tcgen05.commit arriving on the mbarrier at the same offset in every CTA of `mask`
 __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
