@@ -633,14 +633,24 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
     if (st.obs_out) {
         const int chunks = a.k_pad / 8;
         const int rows = min(32, a.N - tile * 32);
-#pragma unroll 4
-        const int cend = (sync_id != 0 && stepping) ? e_pad / 8 : chunks;   // fused: the rest left early
-        for (int row = warp; row < rows; row += 4) {
-            uint4* dst = reinterpret_cast<uint4*>(st.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
-            for (int c = lane; c < cend; c += 32) {
-                const uint4 val = c * 8 < e_pad ? *reinterpret_cast<const uint4*>(stg + row * e_pad + c * 8)
-                                                : *reinterpret_cast<const uint4*>(tmpl + c * 8);
-                dst[c] = val;
+        if (sync_id != 0 && stepping) {
+            // fused: only the per-env chunks are left (the rest left while the ledger ran), one 16-byte chunk
+            // per thread and pass
+            const int cpr = e_pad / 8;
+            uint4* dst0 = reinterpret_cast<uint4*>(st.obs_out + static_cast<int64_t>(tile) * 32 * a.k_pad);
+            for (int idx = tid; idx < rows * cpr; idx += ENV_THREADS) {
+                const int row = idx / cpr, c = idx - row * cpr;
+                dst0[static_cast<int64_t>(row) * chunks + c] = *reinterpret_cast<const uint4*>(stg + row * e_pad + c * 8);
+            }
+        } else {
+            // (no unroll pragma: measured faster at C5 than the former 4-deep unroll of this loop)
+            for (int row = warp; row < rows; row += 4) {
+                uint4* dst = reinterpret_cast<uint4*>(st.obs_out + (static_cast<int64_t>(tile) * 32 + row) * a.k_pad);
+                for (int c = lane; c < chunks; c += 32) {
+                    const uint4 val = c * 8 < e_pad ? *reinterpret_cast<const uint4*>(stg + row * e_pad + c * 8)
+                                                    : *reinterpret_cast<const uint4*>(tmpl + c * 8);
+                    dst[c] = val;
+                }
             }
         }
     }
