@@ -44,9 +44,15 @@
 namespace pod {
 
 constexpr int ACT_THREADS = 320;       // 10 warps
-constexpr int ACT_STAGES = 5;          // weight ring depth
-constexpr int ACT_BN = 256;            // weight rows per ring stage (max): one N = 256 MMA
-constexpr int ACT_BK = 32;             // K per ring stage (64-byte swizzled rows)
+#ifndef POD_ACT_BK
+#define POD_ACT_BK 32
+#endif
+// weight ring: ACT_STAGES stages of [ACT_BN rows x ACT_BK K] bf16 (80 KB either way)
+constexpr int ACT_STAGES = POD_ACT_BK == 16 ? 10 : 5;
+constexpr int ACT_BN = POD_ACT_BK == 64 ? 128 : 256;   // weight rows per ring stage (max): one N = ACT_BN MMA
+constexpr int ACT_BK = POD_ACT_BK;     // K per ring stage (32: 64-byte swizzled rows, 16: 32-byte)
+constexpr int ACT_KPA = 64 / ACT_BK;   // K blocks per 64-column activation atom
+constexpr int ACT_BAR_BYTES = 640;     // mbarrier region
 constexpr int ACT_MAX_LAYERS = 5;      // n_hidden <= 4
 constexpr int ACT_BIAS_FLOATS = 1792;  // per-CTA staged biases + log-std + sigma
 constexpr int ACT_MAX_HQ = 32;         // head tickers per epilogue thread (n_out_pad <= 128)
@@ -121,7 +127,7 @@ constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
     return 1024 + static_cast<size_t>(ka) * 16384 + static_cast<size_t>(ACT_STAGES) * ACT_STAGE_BYTES +
-           ACT_BIAS_FLOATS * 4 + 512;   // + barriers
+           ACT_BIAS_FLOATS * 4 + ACT_BAR_BYTES;   // + barriers
 }
 
 // The fused rollout (rollout_fused_kernel): one cluster per 128-env M-tile runs the actor AND the env step
@@ -235,7 +241,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     const uint32_t envmkt_b = obs_b + 272u;    // [2 tiles] the next step's market rows landed (bulk copies)
     const uint32_t envin_b = obs_b + 288u;     // [2 tiles] both CTAs' heads' actions + log-prob partials landed
     const uint32_t obsa_b = obs_b + 304u;      // FUSED: [8] obs atom kb landed (layer 0 starts on the first atom)
-    uint8_t* const env_pst = base + bias_off + ACT_BIAS_FLOATS * 4 + 512;   // [2 tiles][persist] (FUSED)
+    uint8_t* const env_pst = base + bias_off + ACT_BIAS_FLOATS * 4 + ACT_BAR_BYTES;   // [2 tiles][persist] (FUSED)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(base + (tslot_s - base_u32));
 
     // persistent over M-tiles: cluster c (one CTA pair per M-tile) takes tiles mtile0 + c + it * nclusters
@@ -412,7 +418,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
         // ===================== MMA issuer =====================
         if (lane == 0) {
             const uint64_t adesc0 = sw128_desc(act_s);
-            const uint64_t bdesc0 = sw64_desc(ring_s);
+            const uint64_t bdesc0 = ACT_BK == 16 ? sw32_desc(ring_s) : (ACT_BK == 64 ? sw128_desc(ring_s) : sw64_desc(ring_s));
             int stage = 0;
             uint32_t phase = 0;
             const int na = a.hidden / 128;           // activation atoms (64 cols) per CTA half
@@ -432,7 +438,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     const int bn = actor_bn(half);
                     const uint32_t idesc = idesc_bf16_f32(128, static_cast<uint32_t>(bn));
                     const int KB = K / ACT_BK;                 // 32-wide K blocks (two per activation atom)
-                    const int kbo = l == 0 ? 0 : static_cast<int>(rank) * na * 2;   // own atoms of h_l first
+                    const int kbo = l == 0 ? 0 : static_cast<int>(rank) * na * ACT_KPA;   // own atoms of h_l first
                     // phase of the atom barriers: one completion per hidden epilogue, over tiles
                     const uint32_t par = static_cast<uint32_t>(it * (a.n_layers - 1) + l - 1) & 1u;
                     const int kp = static_cast<int>((a.kpb_pack >> (5 * l)) & 31u);
@@ -444,16 +450,16 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                             for (int q = 0; q < kp; ++q) {
                                 const int j = j0 + q;
                                 const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
-                                if (FUSED && l == 0 && (j & 1) == 0) {
-                                    mbar_wait(obsa_b + 8u * (j >> 1), static_cast<uint32_t>(it) & 1u);
+                                if (FUSED && l == 0 && (j % ACT_KPA) == 0) {
+                                    mbar_wait(obsa_b + 8u * (j / ACT_KPA), static_cast<uint32_t>(it) & 1u);
                                     tc_fence_after();
                                 }
 #ifdef POD_EXP_GTIME
                                 // fused rollout, CTA 0: [step][obs atom 0 landed, head accumulator ready, ...]
                                 if (FUSED && l == 0 && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
 #endif
-                                if (l > 0 && (j & 1) == 0) {
-                                    const int ja = j >> 1;
+                                if (l > 0 && (j % ACT_KPA) == 0) {
+                                    const int ja = j / ACT_KPA;
                                     if (ja < na) {
                                         mbar_wait(ownrdy_b + 8u * ja, par);
                                     } else {
@@ -466,10 +472,12 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                                     mbar_wait(full_b + 8u * stage, phase);
                                     tc_fence_after();
                                 }
-                                const uint64_t ad = adesc0 + (((kb >> 1) * 16384u + (kb & 1) * 64u) >> 4);
+                                const uint64_t ad =
+                                    adesc0 + (((kb / ACT_KPA) * 16384u + (kb % ACT_KPA) * (ACT_BK * 2u)) >> 4);
                                 const uint64_t bd = bdesc0 + ((stage * stage_bytes) >> 4) + static_cast<uint32_t>(q) * sub16;
-                                mma_bf16(dt, ad, bd, idesc, j != 0);
-                                mma_bf16(dt, ad + 2, bd + 2, idesc, 1u);
+    #pragma unroll
+                                for (int h = 0; h < ACT_BK / 16; ++h)
+                                    mma_bf16(dt, ad + 2 * h, bd + 2 * h, idesc, (j != 0 || h > 0) ? 1u : 0u);
                             }
                             mma_commit(empty_b + 8u * stage);
                             if (++stage == ACT_STAGES) {
@@ -481,18 +489,18 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     for (int c = 0; c < half / bn; ++c) {
                         for (int j = 0; j < KB; ++j) {
                             const int kb = j + kbo < KB ? j + kbo : j + kbo - KB;
-                            if (FUSED && l == 0 && c == 0 && (j & 1) == 0) {
-                                mbar_wait(obsa_b + 8u * (j >> 1), static_cast<uint32_t>(it) & 1u);
+                            if (FUSED && l == 0 && c == 0 && (j % ACT_KPA) == 0) {
+                                mbar_wait(obsa_b + 8u * (j / ACT_KPA), static_cast<uint32_t>(it) & 1u);
                                 tc_fence_after();
                             }
 #ifdef POD_EXP_GTIME
                             // fused rollout, CTA 0: [step][obs atom 0 landed, head accumulator ready, ...]
                             if (FUSED && l == 0 && j == 0 && blockIdx.x == 0 && it < 1024) g_ftime[it][0] = gtimer();
 #endif
-                            if (l > 0 && c == 0 && (j & 1) == 0) {
+                            if (l > 0 && c == 0 && (j % ACT_KPA) == 0) {
                                 // h_l atom by atom: own atoms as the epilogue finishes them, then the
                                 // peer's atoms as its bulk copies land
-                                const int ja = j >> 1;
+                                const int ja = j / ACT_KPA;
                                 if (ja < na) {
                                     mbar_wait(ownrdy_b + 8u * ja, par);
                                 } else {
@@ -505,11 +513,13 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                             tc_fence_after();
                             if (tr && it == 0 && l == 0 && c * KB + j < 16) tr[32 + c * KB + j] = clock64();
                             // descriptors: precomputed bases + the start-address field (16-B units)
-                            const uint64_t ad = adesc0 + (((kb >> 1) * 16384u + (kb & 1) * 64u) >> 4);
+                            const uint64_t ad =
+                                adesc0 + (((kb / ACT_KPA) * 16384u + (kb % ACT_KPA) * (ACT_BK * 2u)) >> 4);
                             const uint64_t bd = bdesc0 + ((stage * stage_bytes) >> 4);
                             const uint32_t dt = tmem + (static_cast<uint32_t>(g) & 1u) * tbuf + static_cast<uint32_t>(c * bn);
-                            mma_bf16(dt, ad, bd, idesc, j != 0);
-                            mma_bf16(dt, ad + 2, bd + 2, idesc, 1u);
+    #pragma unroll
+                            for (int h = 0; h < ACT_BK / 16; ++h)
+                                mma_bf16(dt, ad + 2 * h, bd + 2 * h, idesc, (j != 0 || h > 0) ? 1u : 0u);
                             if (a.mc) mma_commit_mc(empty_b + 8u * stage, share_mask);   // free it in both CTAs
                             else mma_commit(empty_b + 8u * stage);
                             if (++stage == ACT_STAGES) {

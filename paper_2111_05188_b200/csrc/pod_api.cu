@@ -894,7 +894,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
                 const uint64_t str[2] = {static_cast<uint64_t>(L.w_cols[l]) * 2, actor->param_bytes};
                 const uint32_t box[3] = {ACT_BK, static_cast<uint32_t>(bn), 1};
                 st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 3, dims, str,
-                                 box, CU_TENSOR_MAP_SWIZZLE_64B);
+                                 box, ACT_BK == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : (ACT_BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B));
             } else {
                 // [agents][K block][out][32]: the K-block stride is 64 bytes inside each weight row
                 const uint64_t dims[4] = {static_cast<uint64_t>(ACT_BK), static_cast<uint64_t>(rows),
@@ -902,7 +902,7 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
                 const uint64_t str[3] = {static_cast<uint64_t>(L.w_cols[l]) * 2, ACT_BK * 2, actor->param_bytes};
                 const uint32_t box[4] = {ACT_BK, static_cast<uint32_t>(bn), static_cast<uint32_t>(kph), 1};
                 st = encode_bf16(&p.maps.w[l], static_cast<const char*>(actor->params) + L.w_offset[l], 4, dims, str,
-                                 box, CU_TENSOR_MAP_SWIZZLE_64B);
+                                 box, ACT_BK == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : (ACT_BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B));
             }
             if (st) return st;
         }

@@ -170,6 +170,16 @@ __device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
     d |= static_cast<uint64_t>(4) << 61;
     return d;
 }
+// Same for the 32-byte swizzle (rows of 32 B = 16 bf16, 8-row groups 256 B apart, layout 6 = SWIZZLE_32B).
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(256 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(6) << 61;
+    return d;
+}
 // Instruction descriptor, kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16
 // [10,13)=1, both K-major (bits 15, 16 = 0), N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
