@@ -94,7 +94,13 @@ struct ActorArgs {
     unsigned long long* trace;   // diagnostics: [grid][32] clock64 stamps, or null
     float* logp_parts;           // [4][N] log-prob partials (rank, half) for the env step to combine (required)
     uint32_t kpb_pack;           // K blocks per ring stage of layer l in bits [5l, 5l+5) (0/1: one 3-D box)
+    // the weights re-tiled in ring-stage order (actor_retile_kernel): each stage one contiguous, pre-swizzled
+    // block fetched with a 1-D bulk copy; null: the tensor maps
+    const char* wt;
+    uint64_t wt_agent_bytes;
+    uint64_t wt_layer_off[ACT_MAX_LAYERS];
 };
+
 
 struct ActorMaps {
     CUtensorMap obs;                     // 2-D bf16 [rows][k_pad], box {64, 128}
@@ -123,6 +129,42 @@ inline int actor_kpb(int KB, int bn, bool rotated) {
     return cap;
 }
 constexpr uint32_t ACT_STAGE_BYTES = ACT_BN * ACT_BK * 2;   // 16 KB
+
+// Re-tiled weights: per agent, per layer, per CTA half r, per column chunk c, per ring stage s (natural K order),
+// the stage's [bn rows x kp K blocks x 32 K] bf16 image exactly as the SWIZZLE_64B tensor-map load lands it in
+// shared memory (16-byte chunk q of row p of a [bn x 64 B] sub-tile at p*64 + ((q ^ ((p >> 1) & 3)) << 4)).
+struct RetileArgs {
+    const char* params;
+    uint64_t param_bytes;
+    int32_t n_layers;
+    uint64_t w_off[ACT_MAX_LAYERS];
+    int32_t rows[ACT_MAX_LAYERS], cols[ACT_MAX_LAYERS], kp[ACT_MAX_LAYERS];
+    uint64_t layer_off[ACT_MAX_LAYERS];
+    uint64_t agent_bytes;
+    char* wt;
+};
+__global__ void __launch_bounds__(256) actor_retile_kernel(const RetileArgs ra) {
+    // one thread per 16-byte chunk of one layer (blockIdx.y = layer, blockIdx.z = agent)
+    const int l = blockIdx.y, ag = blockIdx.z;
+    if (l >= ra.n_layers) return;
+    const int R = ra.rows[l], K = ra.cols[l], kp = ra.kp[l] > 1 ? ra.kp[l] : 1;
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c8n = K / 8;
+    if (idx >= static_cast<int64_t>(R) * c8n) return;
+    const int o = static_cast<int>(idx / c8n), c8 = static_cast<int>(idx % c8n);
+    const int half = R / 2, bn = actor_bn(half);
+    const int r = o / half, oh = o % half, c = oh / bn, p = oh % bn;
+    const int kb = c8 / (ACT_BK / 8), q = c8 % (ACT_BK / 8);
+    const int s = kb / kp, sub = kb % kp;
+    const uint64_t stage_bytes = static_cast<uint64_t>(bn) * kp * ACT_BK * 2;
+    const uint64_t dst = ra.agent_bytes * ag + ra.layer_off[l] + static_cast<uint64_t>(r) * half * K * 2 +
+                         static_cast<uint64_t>(c) * bn * K * 2 + static_cast<uint64_t>(s) * stage_bytes +
+                         static_cast<uint64_t>(sub) * bn * ACT_BK * 2 + static_cast<uint64_t>(p) * ACT_BK * 2 +
+                         (static_cast<uint64_t>(q ^ ((p >> 1) & 3)) << 4);
+    const uint4 v = *reinterpret_cast<const uint4*>(ra.params + ra.param_bytes * ag + ra.w_off[l] +
+                                                    (static_cast<uint64_t>(o) * K + static_cast<uint64_t>(c8) * 8) * 2);
+    *reinterpret_cast<uint4*>(ra.wt + dst) = v;
+}
 
 inline size_t actor_smem_bytes(int k_pad, int hidden) {
     const int ka = (k_pad > hidden ? k_pad : hidden) / 64;
@@ -373,9 +415,16 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                             const int ks = (j + kso) % ns;
                             before_stage(l);
                             mbar_wait(empty_b + 8u * stage, phase ^ 1u);
-                            mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn * kp) * (ACT_BK * 2));
-                            tma_load_4d(ring_s + stage * stage_bytes, &maps.w[l], 0, static_cast<int>(rank) * half,
-                                        ks * kp, tl.agent, full_b + 8u * stage);
+                            const uint32_t sbytes = static_cast<uint32_t>(bn * kp) * (ACT_BK * 2);
+                            mbar_arrive_expect_tx(full_b + 8u * stage, sbytes);
+                            if (a.wt)
+                                bulk_g2s(ring_s + stage * stage_bytes,
+                                         a.wt + a.wt_agent_bytes * tl.agent + a.wt_layer_off[l] +
+                                             static_cast<uint64_t>(rank) * half * K * 2 + static_cast<uint64_t>(ks) * sbytes,
+                                         sbytes, full_b + 8u * stage);
+                            else
+                                tma_load_4d(ring_s + stage * stage_bytes, &maps.w[l], 0, static_cast<int>(rank) * half,
+                                            ks * kp, tl.agent, full_b + 8u * stage);
                             ++seq;
                             if (++stage == ACT_STAGES) {
                                 stage = 0;
@@ -390,7 +439,14 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                             before_stage(l);
                             mbar_wait(empty_b + 8u * stage, phase ^ 1u);
                             mbar_arrive_expect_tx(full_b + 8u * stage, static_cast<uint32_t>(bn) * (ACT_BK * 2));
-                            if (!a.mc) {
+                            if (a.wt) {
+                                const uint32_t sbytes = static_cast<uint32_t>(bn) * (ACT_BK * 2);
+                                bulk_g2s(ring_s + stage * stage_bytes,
+                                         a.wt + a.wt_agent_bytes * tl.agent + a.wt_layer_off[l] +
+                                             static_cast<uint64_t>(rank) * half * K * 2 + static_cast<uint64_t>(c) * bn * K * 2 +
+                                             static_cast<uint64_t>(kb) * sbytes,
+                                         sbytes, full_b + 8u * stage);
+                            } else if (!a.mc) {
                                 tma_load_3d(ring_s + stage * stage_bytes, &maps.w[l], kb * ACT_BK,
                                             static_cast<int>(rank) * half + c * bn, tl.agent, full_b + 8u * stage);
                             } else if ((seq & (a.mc - 1)) == static_cast<int>(cr >> 1)) {

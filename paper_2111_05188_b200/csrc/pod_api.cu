@@ -280,6 +280,9 @@ struct pod_env {
     int persist;                // persistent actor clusters (POD_PERSIST=0 turns it off)
     int pdl;                    // env step as a programmatic dependent of the actor (POD_PDL=0 turns it off)
     int fused;                  // the fused rollout kernel where eligible (POD_FUSED=0 turns it off)
+    int wt_on;                  // weights re-tiled per rollout and streamed by 1-D bulk copies (POD_WT=0: tensor maps)
+    char* wt;                   // the re-tiled weights (cudaMalloc'd on first use, grown as needed)
+    size_t wt_bytes;
     int sm_count;
     int profile;                // 0 = off, k = bracket every k-th step
     unsigned long long* trace;  // diagnostics: actor clock64 stamps of the last launch
@@ -411,6 +414,10 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
         e->pdl = (pd && pd[0] == '0') ? 0 : ((pd && pd[0] == '2') ? 2 : 1);   // 2: every env step (experiments)
         const char* fu = getenv("POD_FUSED");
         e->fused = !(fu && fu[0] == '0');
+        const char* wv = getenv("POD_WT");
+        e->wt_on = !(wv && wv[0] == '0');
+        e->wt = nullptr;
+        e->wt_bytes = 0;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -485,6 +492,7 @@ extern "C" pod_status pod_env_create(const pod_env_config* cfg, const pod_market
 
 extern "C" pod_status pod_env_destroy(pod_env_t* e) {
     if (!e) return POD_OK;
+    if (e->wt) cudaFree(e->wt);
     for (auto& g : e->graphs) {
         cudaGraphExecDestroy(g.exec);
         if (g.prof) {
@@ -597,6 +605,7 @@ struct RolloutPlan {
     ActorMaps maps;
     ActorArgs aa;
     size_t actor_smem;
+    RetileArgs ra;       // the weight re-tiling of this rollout (ra.wt null: none)
 };
 
 // The fused rollout needs every M-tile's cluster resident at once (one wave: the clusters are independent
@@ -801,6 +810,14 @@ static void enqueue_group(pod_env* e, const RolloutPlan& p, int T, const pod_tra
 
 static pod_status enqueue_rollout(pod_env* e, const RolloutPlan& p, int T, const pod_traj* tr, const float* inj,
                                   double* fitness_out, cudaStream_t s, ProfEvents* prof) {
+    if (p.ra.wt) {
+        int maxc = 0;
+        for (int l = 0; l < p.ra.n_layers; ++l) maxc = std::max(maxc, p.ra.rows[l] * (p.ra.cols[l] / 8));
+        actor_retile_kernel<<<dim3(static_cast<unsigned>((maxc + 255) / 256), static_cast<unsigned>(p.ra.n_layers),
+                               static_cast<unsigned>(e->cfg.n_agents)),
+                              256, 0, s>>>(p.ra);
+        pod_note_launch(s);
+    }
     if (e->groups == 1) {
         enqueue_group(e, p, T, tr, inj, s, prof, 0);
     } else {
@@ -932,6 +949,38 @@ extern "C" pod_status pod_rollout(pod_env_t* e, const pod_actor* actor, int32_t 
         p.actor_smem = actor_smem_bytes(L.k_pad, actor->hidden);
         if (p.actor_smem > 232448) return pod_fail(POD_ERR_UNSUPPORTED, "actor needs %zu B of shared memory", p.actor_smem);
         p.fused = fused_eligible(e, p);
+        if (e->wt_on && !e->mc_ok) {
+            // the weights re-tiled in ring-stage order once per rollout (they may change between rollouts)
+            RetileArgs& ra = p.ra;
+            ra.params = static_cast<const char*>(actor->params);
+            ra.param_bytes = actor->param_bytes;
+            ra.n_layers = L.n_layers;
+            uint64_t off = 0;
+            for (int l = 0; l < L.n_layers; ++l) {
+                ra.w_off[l] = L.w_offset[l];
+                ra.rows[l] = L.w_rows[l];
+                ra.cols[l] = L.w_cols[l];
+                ra.kp[l] = static_cast<int32_t>((p.aa.kpb_pack >> (5 * l)) & 31u);
+                ra.layer_off[l] = off;
+                p.aa.wt_layer_off[l] = off;
+                off += static_cast<uint64_t>(L.w_rows[l]) * L.w_cols[l] * 2;
+            }
+            ra.agent_bytes = (off + 1023) / 1024 * 1024;
+            const size_t need = ra.agent_bytes * static_cast<size_t>(e->cfg.n_agents);
+            if (need > e->wt_bytes) {
+                if (e->wt) cudaFree(e->wt);
+                e->wt = nullptr;
+                e->wt_bytes = 0;
+                // a capture of the rollout graph may hold the old buffer: cached graphs are dropped with it
+                for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
+                e->graphs.clear();
+                POD_CUDA(cudaMalloc(reinterpret_cast<void**>(&e->wt), need));
+                e->wt_bytes = need;
+            }
+            ra.wt = e->wt;
+            p.aa.wt = e->wt;
+            p.aa.wt_agent_bytes = ra.agent_bytes;
+        }
     }
     if (!e->use_graphs) {
         ProfEvents* prof = nullptr;
