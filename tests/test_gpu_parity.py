@@ -520,6 +520,29 @@ def test_pdl_env_launch_bit_identical(n, N, nh, hid, monkeypatch):
         assert torch.equal(getattr(outs[0], name), getattr(outs[1], name)), name
 
 
+@pytest.mark.parametrize("n,N,agents,nh,hid", [(30, 512, 2, 2, 128), (100, 256, 1, 3, 512), (100, 20480, 1, 3, 512)])
+def test_weight_retile_bit_identical(n, N, agents, nh, hid, monkeypatch):
+    """The actor weights re-tiled per rollout into ring-stage order and streamed by 1-D bulk copies (default)
+    against the 2-D tensor-map boxes (POD_WT=0): every output bit-identical, in the fused kernel (N <= 9472 at
+    these shapes) and in the separate persistent actor (N = 20480: 160 M-tiles)."""
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("POD_WT", flag)
+        c = Case(n=n, f=3, T_data=600, N=N, H=6, n_agents=agents, seed=16)
+        aws, params, actor = _actor(c, nh, hid, n_agents=agents)
+        tr = api.Trajectory.allocate(4, N, n, c.k_pad, debug=True, critic=True)
+        c.env.reset(c.starts)
+        c.env.rollout(4, tr, actor=actor)
+        c.env.check()
+        torch.cuda.synchronize()
+        outs.append(tr)
+    for name in ("obs", "act", "logp", "mu", "rew", "done", "dbg_hold", "dbg_cash", "dbg_aint", "val"):
+        x, y = getattr(outs[0], name), getattr(outs[1], name)
+        if x.dtype == torch.bfloat16:
+            x, y = x.view(torch.int16), y.view(torch.int16)
+        assert torch.equal(x, y), name
+
+
 @pytest.mark.parametrize("n,N,agents,nh,hid,det", [(30, 512, 1, 2, 128, False), (30, 4096, 1, 2, 128, True),
                                                    (100, 8192, 1, 3, 512, False), (100, 8192, 8, 3, 512, False),
                                                    (100, 2048, 2, 3, 512, True)])
