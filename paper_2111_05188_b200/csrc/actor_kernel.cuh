@@ -279,6 +279,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
     // FUSED: both CTAs' env steps of step t are done (s_{t+1}, holdings and noise written; 2 arrivals), and the
     // env tiles' own mbarriers
     const uint32_t envdone_b = obs_b + 136u;
+    static_assert(1 + ENV_BUY_CHUNKS <= 8, "the env tiles' mbarriers take 8 slots per tile below");
     const uint32_t envbar_b = obs_b + 144u;    // [2 tiles][1 + ENV_BUY_CHUNKS]
     const uint32_t envmkt_b = obs_b + 272u;    // [2 tiles] the next step's market rows landed (bulk copies)
     const uint32_t envin_b = obs_b + 288u;     // [2 tiles] both CTAs' heads' actions + log-prob partials landed
