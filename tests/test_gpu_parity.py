@@ -543,7 +543,9 @@ def test_weight_retile_bit_identical(n, N, agents, nh, hid, monkeypatch):
         assert torch.equal(x, y), name
 
 
-@pytest.mark.parametrize("n,N,agents,nh,hid,det", [(30, 512, 1, 2, 128, False), (30, 4096, 1, 2, 128, True),
+@pytest.mark.parametrize("n,N,agents,nh,hid,det", [(1, 256, 1, 1, 128, False), (7, 384, 3, 1, 128, False),
+                                                   (64, 512, 1, 2, 256, False),
+                                                   (30, 512, 1, 2, 128, False), (30, 4096, 1, 2, 128, True),
                                                    (100, 8192, 1, 3, 512, False), (100, 8192, 8, 3, 512, False),
                                                    (100, 2048, 2, 3, 512, True)])
 def test_fused_rollout_bit_identical(n, N, agents, nh, hid, det, monkeypatch):
@@ -564,8 +566,11 @@ def test_fused_rollout_bit_identical(n, N, agents, nh, hid, det, monkeypatch):
         # bootstrap pass only with it)
         for T, critic in ((7, True), (7, True), (1, True), (2, False)):
             tr = api.Trajectory.allocate(T, N, n, c.k_pad, debug=True, critic=critic, equity=True)
+            k0 = api.kernel_launches()
             c.env.rollout(T, tr, actor=actor, deterministic=det)
             torch.cuda.synchronize()
+            if T == 7:   # the fused path is one launch for the steps (plus obs_0, the weight re-tiling, the bump)
+                assert (api.kernel_launches() - k0 < T) == (flag == "1"), "unexpected rollout path"
             res.append({k: v.clone() for k, v in vars(tr).items() if v is not None})
         res.append(dict(zip(("hold", "cash", "asset", "ep_ret"), c.env.read_state())))
         c.env.check()
