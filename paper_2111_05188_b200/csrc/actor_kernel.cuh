@@ -746,14 +746,21 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             const bool vec = (a.n % 4) == 0;
             const int i00 = static_cast<int>(rank) * head_half;
     #pragma unroll
+            // the next chunk's 8 accumulator columns are loaded while this chunk is processed (hn)
+            const uint32_t hbase = trow + (static_cast<uint32_t>(gL) & 1u) * tbuf + static_cast<uint32_t>(hh * hq);
+            uint32_t hn[8];
+            __syncwarp();
+            tmem_ld8(hbase, hn);
+            tmem_ld_wait();
             for (int cc = 0; cc < ACT_MAX_HQ / 8; ++cc) {
                 if (cc >= hq / 8) break;
                 const int tc = hh * hq + cc * 8;                         // TMEM column (local)
                 const int i0 = i00 + tc;                                 // global ticker
                 uint32_t hv[8];
+    #pragma unroll
+                for (int jj = 0; jj < 8; ++jj) hv[jj] = hn[jj];
                 __syncwarp();
-                tmem_ld8(trow + (static_cast<uint32_t>(gL) & 1u) * tbuf + static_cast<uint32_t>(tc), hv);
-                tmem_ld_wait();
+                if (cc + 1 < hq / 8) tmem_ld8(hbase + static_cast<uint32_t>(8 * (cc + 1)), hn);
                 if (valid && i0 <= a.n && val_out && a.n < i0 + 8) {
                     // critic: head row n over the same trunk (R#22)
                     float vh = 0.0f;
@@ -837,6 +844,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                         }
                     }
                 }
+                tmem_ld_wait();   // the next chunk's columns (hn)
             }
             if (bad && valid) atomicOr(a.err, 1u);
             if (tr && it == 0 && etid == 0) tr[25] = clock64();
