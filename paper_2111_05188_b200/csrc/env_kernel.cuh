@@ -24,6 +24,12 @@
 // part of s_{t+1} and store the 32 observation rows with 16-B vector stores
 // (512 contiguous bytes per warp instruction).  Warp 1 also sums the actor's four log-prob partials
 // of each env into traj.logp (fixed order), and the idle warps draw the next step's actor noise.
+//
+// The tile body (env_step_tile) serves two callers: env_step_kernel (one block per tile, the separate
+// launches) and the fused rollout kernel (actor_kernel.cuh, rollout_fused_kernel), where a 128-thread group of
+// the actor CTA's epilogue warps runs it every step with the tile's header, ledger state and market rows kept
+// in shared memory across steps (EnvPersist layout below), the actions and log-prob partials delivered by the
+// actor's head through DSMEM, and the tile-shared part of s_{t+1} written while the ledger runs.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -132,7 +138,7 @@ struct EnvStep {
     int32_t noise_t;
 };
 
-// Fused rollout: an env tile's state kept in the CTA's shared memory across the T steps (outside the activation
+// Fused rollout (EnvPersist): an env tile's state kept in the CTA's shared memory across the T steps (outside the activation
 // buffer the per-step tile area lives in): the tile header, its 32 envs' ledger state, and the next step's market
 // rows, which TMA bulk copies bring in during the actor phase.  Byte offsets; `mkt` holds three 16-byte aligned
 // windows, [p_t | p_{t+1}], [p_0], [feat[t_obs]] ((3 + f) n floats), each starting up to 3 floats before its row
