@@ -222,7 +222,10 @@ pod_status pod_env_reset(pod_env_t* env, const int64_t* tile_start_rows, uint16_
  * no profiling, the T steps run as ONE launch in which each CTA pair runs the
  * actor and the env step of its 128 envs for all steps (the rollout_fused
  * kernel; POD_FUSED=0 in the environment at pod_env_create turns it off);
- * otherwise as 2T launches (actor, env step).
+ * otherwise as 2T launches (actor, env step).  Each rollout first copies the
+ * actor's weights into ring-stage order in a device buffer the handle
+ * allocates on first use (n_agents x the weight bytes of the slab; freed by
+ * pod_env_destroy; POD_WT=0 at pod_env_create streams from the slab instead).
  * Errors (host, synchronous): ARG, SHAPE, UNSUPPORTED, CUDA. */
 pod_status pod_rollout(pod_env_t* env, const pod_actor* actor, int32_t T, const pod_traj* traj,
                        const float* injected_u, int32_t deterministic, double* fitness_out,
