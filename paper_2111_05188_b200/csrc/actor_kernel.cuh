@@ -772,9 +772,23 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                 if (valid && i0 < a.n && !vo) {
                     float raw[8], mu[8];
                     int16_t ai8[8];
+                    // the chunk's 8 staged biases, log-stds and sigmas as 16-byte loads (8-column aligned)
+                    float bz[8], lsz[8], sgz[8];
+                    {
+                        const float4* b4 = reinterpret_cast<const float4*>(bias + tc);
+                        const float4* l4 = reinterpret_cast<const float4*>(log_std + tc);
+                        const float4* s4 = reinterpret_cast<const float4*>(sigma + tc);
+    #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const float4 x = b4[h], y = l4[h], w = s4[h];
+                            bz[4 * h] = x.x; bz[4 * h + 1] = x.y; bz[4 * h + 2] = x.z; bz[4 * h + 3] = x.w;
+                            lsz[4 * h] = y.x; lsz[4 * h + 1] = y.y; lsz[4 * h + 2] = y.z; lsz[4 * h + 3] = y.w;
+                            sgz[4 * h] = w.x; sgz[4 * h + 1] = w.y; sgz[4 * h + 2] = w.z; sgz[4 * h + 3] = w.w;
+                        }
+                    }
     #pragma unroll
                     for (int jj = 0; jj < 8; ++jj) {
-                        mu[jj] = __uint_as_float(hv[jj]) + bias[tc + jj];
+                        mu[jj] = __uint_as_float(hv[jj]) + bz[jj];
                         raw[jj] = mu[jj];
                     }
                     // per ticker: noise z ~ N(0,1) for (env, step, ticker) generated by the previous env step,
@@ -790,9 +804,9 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                     for (int jj = 0; jj < 8; ++jj) {
                         const bool ok = i0 + jj < a.n;
                         const float z = zr[cc * 8 + jj];
-                        const float ls = log_std[tc + jj];
+                        const float ls = lsz[jj];
                         bad |= ok && !isfinite(mu[jj]);
-                        raw[jj] = fmaf(sigma[tc + jj], z, mu[jj]);
+                        raw[jj] = fmaf(sgz[jj], z, mu[jj]);
                         if (ok) logp += (-0.5f * z * z - ls) - half_ln_2pi;
                         const float u = tanh_sfu(raw[jj]);
                         if constexpr (FUSED) {
