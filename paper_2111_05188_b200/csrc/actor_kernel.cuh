@@ -739,7 +739,9 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
             const float* log_std = bias_s + boff + head_half;
             const float* sigma = bias_s + boff + 2 * head_half;
             float logp = 0.0f;
-            bool bad = false;
+            // non-finite mean detector: 0 * mu is 0 for finite mu and NaN for inf / NaN, so the sum turns NaN iff
+            // some (unmasked) mean is not finite — one predicated FMA per ticker
+            float nanacc = 0.0f;
             const float half_ln_2pi = 0.918938533204672742f;
             const bool fast_map = FUSED && a.h_max <= 128;
             const float hmax_f = static_cast<float>(a.h_max);
@@ -805,7 +807,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                         const bool ok = i0 + jj < a.n;
                         const float z = zr[cc * 8 + jj];
                         const float ls = lsz[jj];
-                        bad |= ok && !isfinite(mu[jj]);
+                        if (ok) nanacc = fmaf(mu[jj], 0.0f, nanacc);
                         raw[jj] = fmaf(sgz[jj], z, mu[jj]);
                         if (ok) logp += (-0.5f * z * z - ls) - half_ln_2pi;
                         const float u = tanh_sfu(raw[jj]);
@@ -860,7 +862,7 @@ __device__ __forceinline__ void actor_body(const ActorMaps& maps, const ActorArg
                 }
                 tmem_ld_wait();   // the next chunk's columns (hn)
             }
-            if (bad && valid) atomicOr(a.err, 1u);
+            if (nanacc != nanacc && valid) atomicOr(a.err, 1u);
             if (tr && it == 0 && etid == 0) tr[25] = clock64();
             // log-prob partial of (rank, hh) for row r -> the [4][N] scratch (FUSED: the env tile's stg); the env step
             // that follows combines the four partials ((p0 + p1) + p2) + p3, so the kernel's tail needs no exchange
