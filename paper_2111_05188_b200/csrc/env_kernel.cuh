@@ -459,7 +459,10 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
                     if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
                     const double ad = static_cast<double>(ai > 0 ? ai : 0);
                     const double y = __dmul_rn(cash, rcp);
-                    const double fl = floor(y);
+                    // floor(y) for 0 <= y < 2^52 as fl(y + 2^52, rounded down) - 2^52 (both exact): two
+                    // fixed-latency float64 adds on the chain instead of the variable-latency FRND.F64;
+                    // y >= 2^52 (never, cash / unit) still gives fl > a+, so q = a+ as with floor
+                    const double fl = __dadd_rn(__dadd_rd(y, 4503599627370496.0), -4503599627370496.0);
                     const double qd = fl < ad ? fl : ad;
                     const double cost = __dmul_rn(qd, unit);
                     const long long frb = __double_as_longlong(__dadd_rn(y, -fl));
