@@ -457,18 +457,21 @@ __device__ __forceinline__ void env_step_tile(const EnvMaps& maps, const EnvArgs
                         rc_n = rcp_s[i + 1];
                     }
                     if (ai < 0) h -= min(h, -ai);                      // post-sell holdings
-                    const double ad = static_cast<double>(ai > 0 ? ai : 0);
+                    // q = min(floor(y), a+) in the biased domain: fl(y + 2^52, rounded down) = 2^52 + floor(y)
+                    // exactly (0 <= y < 2^52; larger y, never reached, still compares above), and 2^52 + a+ is
+                    // built from the integer; both are positive doubles, so their bit patterns order as their
+                    // values and an integer min replaces FRND / I2F / DSETP / F2I on the float64 pipe.  The
+                    // min's low word is q; one exact DADD takes q back to a double for the cost
+                    const long long ab = 0x4330000000000000ll | static_cast<long long>(ai > 0 ? ai : 0);
                     const double y = __dmul_rn(cash, rcp);
-                    // floor(y) for 0 <= y < 2^52 as fl(y + 2^52, rounded down) - 2^52 (both exact): two
-                    // fixed-latency float64 adds on the chain instead of the variable-latency FRND.F64;
-                    // y >= 2^52 (never, cash / unit) still gives fl > a+, so q = a+ as with floor
-                    const double fl = __dadd_rn(__dadd_rd(y, 4503599627370496.0), -4503599627370496.0);
-                    const double qd = fl < ad ? fl : ad;
+                    const long long tb = __double_as_longlong(__dadd_rd(y, 4503599627370496.0));
+                    const bool cut = tb > ab;                           // floor(y) > a+: q = a+
+                    const long long mb = cut ? ab : tb;
+                    const double qd = __dadd_rn(__longlong_as_double(mb), -4503599627370496.0);
                     const double cost = __dmul_rn(qd, unit);
-                    const long long frb = __double_as_longlong(__dadd_rn(y, -fl));
-                    unsure |= !(ai <= 0 || __double_as_longlong(fl) > __double_as_longlong(ad) ||
-                                (frb >= FR_LO && frb <= FR_HI));
-                    h += static_cast<int>(qd);
+                    const long long frb = __double_as_longlong(__dadd_rn(y, -qd));   // y - floor(y) unless cut
+                    unsure |= !(ai <= 0 || cut || (frb >= FR_LO && frb <= FR_HI));
+                    h += static_cast<int>(static_cast<unsigned>(mb));
                     cash = __dadd_rn(cash, -cost);
                     hold_s[i * 32 + lane] = h;
                 }
